@@ -1,0 +1,406 @@
+#!/usr/bin/env python3
+"""Benchmark of the structured-spinner hot path on B200 (BASELINE.json metric:
+"spinner vectors/sec (and GB/s as % of HBM roofline) at 1/2/4/8 B200 vs host-CPU ref").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one pass of the hot path over one batch of the config's synthetic input:
+  c1  LSH, 1 table: 4096 x 1024 unit vectors -> int32 ids + fp32 y (scale 1)
+  c2  (default; BASELINE configs[1]) Gaussian RFF: 60000 x 784 -> pad 1024, 4 blocks,
+      k = 4096, sigma = 5 -> 60000 x 8192 fp32 features
+  c3  LSH, 8 tables: 2^20 x 16384 unit vectors (64 GiB, generated on device) -> ids, + NCCL all-gather
+  c4  sketch: A[131072][256] -> sqrt(N/m) P H D3 H D2 H D1 A, m = 2048 random rows
+  c5  all-Gaussian diagonals + ReLU: 256 x 2^20 -> 256 x 2^20
+Multi-GPU (torchrun, one process per GPU): weak scaling, each rank runs its own
+full batch (different seeds); c3 additionally all-gathers the codes over NCCL.
+`value` = vectors processed by all ranks / max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "spinner vectors/sec"
+UNIT = "vectors/s"
+
+CONFIGS = {
+    "c1": dict(workload="BASELINE configs[0]: cross-polytope LSH, 1 table, 4096 x n=1024, ids + fp32 y (scale 1)",
+               n=1024, batch=4096, bytes_per_vec=1024 * 4 * 2 + 4, flush=True),
+    "c2": dict(workload="BASELINE configs[1]: Gaussian RFF, 60000 x 784 (zero-pad 1024), 4 HD3HD2HD1 blocks "
+                        "(k=4096), sigma=5, out 60000 x 8192 fp32",
+               n=1024, n_in=784, batch=60000, k=4096, sigma=5.0, bytes_per_vec=784 * 4 + 8192 * 4, flush=False),
+    "c3": dict(workload="BASELINE configs[2]: cross-polytope LSH, 8 tables, 2^20 x n=16384 unit vectors -> int32 ids",
+               n=16384, batch=1 << 20, tables=8, bytes_per_vec=16384 * 4 + 8 * 4, flush=False),
+    "c4": dict(workload="BASELINE configs[3]: sketch sqrt(N/m) P H D3 H D2 H D1 A, A = 131072 x 256, m = 2048 "
+                        "random rows", N=1 << 17, d=256, m=2048, bytes_per_vec=(1 << 17) * 4 + 2048 * 4, flush=True),
+    "c5": dict(workload="BASELINE configs[4]: ReLU(H D3 H D2 H D1 x), Gaussian D's, 256 x n=2^20",
+               n=1 << 20, batch=256, bytes_per_vec=(1 << 20) * 8, flush=False),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------- distributed
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.samples, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ workloads
+class Workload:
+    """Device-resident inputs/outputs for one config + a `step()` that launches the hot path."""
+
+    def __init__(self, name, cfg, rank, device):
+        import torch
+        import paper_1610_06209_b200 as spn
+        self.spn, self.torch, self.name, self.cfg = spn, torch, name, cfg
+        self.device = device
+        g = torch.Generator(device="cuda")
+        g.manual_seed(1234 + rank)
+        V = spn.SpinnerVariant
+        self.launches_per_step = 1
+        if name == "c1":
+            self.sp = spn.StackedSpinner(V.hd3_hd2_hd1, 1024, 1024, 1024, 42 + rank, scale=1.0)
+            x = torch.randn((cfg["batch"], 1024), device="cuda", generator=g)
+            self.x = x / x.norm(dim=1, keepdim=True)
+            self.y = torch.empty_like(self.x)
+            self.vectors = cfg["batch"]
+        elif name == "c2":
+            self.sp = spn.StackedSpinner(V.hd3_hd2_hd1, 1024, 1024, cfg["k"], 5 + rank)
+            self.fm = spn.FeatureMap(self.sp, spn.KernelKind.gaussian(cfg["sigma"]))
+            self.x = torch.rand((cfg["batch"], cfg["n_in"]), device="cuda", generator=g)
+            self.out = torch.empty((cfg["batch"], 2 * cfg["k"]), device="cuda")
+            self.vectors = cfg["batch"]
+        elif name == "c3":
+            self.h = spn.MultiTableHasher(V.hd3_hd2_hd1, cfg["n"], cfg["n"], cfg["tables"], seed=3)
+            self.x = torch.empty((cfg["batch"], cfg["n"]), device="cuda")
+            for r0 in range(0, cfg["batch"], 1 << 16):  # N(0,1) then L2-normalised, generated on device
+                blk = torch.randn((min(1 << 16, cfg["batch"] - r0), cfg["n"]), device="cuda", generator=g)
+                self.x[r0:r0 + blk.shape[0]] = blk / blk.norm(dim=1, keepdim=True)
+                del blk
+            self.ids = torch.empty((cfg["batch"], cfg["tables"]), device="cuda", dtype=torch.int32)
+            self.vectors = cfg["batch"]
+        elif name == "c4":
+            self.sk = spn.SketchOperator(V.hd3_hd2_hd1, cfg["N"], cfg["m"], 11 + rank, mode="random", p_seed=77)
+            self.x = torch.randn((cfg["N"], cfg["d"]), device="cuda", generator=g)
+            self.out = torch.empty((cfg["m"], cfg["d"]), device="cuda")
+            self.vectors = cfg["d"]  # one column = one spinner vector
+            lsa = (17 + 1) // 2
+            groups = math.ceil(cfg["d"] / max(32, ((32 << 20) // (cfg["N"] * 4)) // 32 * 32))
+            self.launches_per_step = 4 * groups
+            del lsa
+        elif name == "c5":
+            self.sp = spn.StackedSpinner(V.gauss3, cfg["n"], cfg["n"], cfg["n"], 13 + rank, scale=1.0)
+            self.x = torch.randn((cfg["batch"], cfg["n"]), device="cuda", generator=g)
+            self.y = torch.empty_like(self.x)
+            self.vectors = cfg["batch"]
+            G = max(1, min(cfg["batch"], (32 << 20) // (cfg["n"] * 4)))
+            self.launches_per_step = 4 * math.ceil(cfg["batch"] / G)
+        torch.cuda.synchronize()
+
+    def step(self, stream):
+        if self.name == "c1":
+            return self.sp.plan.hash(self.x, y_out=self.y, stream=stream)
+        if self.name == "c2":
+            return self.spn.embed(self.fm, self.x, out=self.out, stream=stream)
+        if self.name == "c3":
+            return self.h.plan.hash(self.x, stream=stream)
+        if self.name == "c4":
+            return self.sk.apply(self.x, out=self.out, stream=stream)
+        return self.sp.apply(self.x, relu=True, out=self.y, stream=stream)
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    cfg = CONFIGS[args.config]
+    w = Workload(args.config, cfg, rank, local)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if cfg["flush"] else None
+    for _ in range(max(3, args.warmup)):
+        w.step(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.fill_(i & 0xFF)  # evict L2 (256 MB > 126 MB) outside the timed region
+            evs[i][0].record(stream)
+            w.step(stream)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    ids = None
+    if args.config == "c3" and world > 1:  # the real exchange step: all-gather the codes over NCCL
+        import torch.distributed as dist
+        ids = w.step(stream)
+        gathered = torch.empty((world * ids.shape[0], ids.shape[1]), dtype=ids.dtype, device="cuda")
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        dist.all_gather_into_tensor(gathered, ids)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        total_ms += t0.elapsed_time(t1) * args.steps
+    barrier(world)
+    torch.cuda.synchronize()
+    total_ms = max_over_ranks(total_ms, world)
+    ms_per_step = total_ms / args.steps
+    value = w.vectors * world * args.steps / (total_ms / 1e3)
+    peak, peak_src = measured_peaks()
+    kernel_ms = statistics.mean(step_ms) / w.launches_per_step  # dominant kernel = the whole step for c1-c3
+    alg_bytes = cfg["bytes_per_vec"] * w.vectors
+    achieved = alg_bytes / (statistics.mean(step_ms) / 1e3) / 1e9
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE config shapes)",
+        "config": {"workload": cfg["workload"], "name": args.config, "vectors_per_gpu_step": w.vectors,
+                   "l2": "L2 flushed (256 MB write) between timed steps" if cfg["flush"]
+                   else "inputs+outputs > 126 MB L2", "parallelism": f"dp{world} (independent shards)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic_from_profiles(args.config), "peak_source": peak_src,
+                     "algorithmic_bytes_per_step": alg_bytes, "mean_kernel_ms": kernel_ms},
+        "clocks": clk.summary(),
+        "gpu_launches": w.launches_per_step * args.steps,
+    }
+    if args.config in ("c1", "c2") and not args.no_e2e:
+        result["e2e"] = e2e_measure(args, w, world)
+    return result, w
+
+
+def traffic_from_profiles(config):
+    """dram bytes/launch from the committed `ncu --set full` summary, if present."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(config)
+    except Exception:
+        return None
+
+
+def e2e_measure(args, w, world):
+    """Same metric through the public API with HOST buffers: pinned host input in,
+    pinned host output back, the copies inside the timed region (spn_*_host)."""
+    import torch
+    cfg = CONFIGS[args.config]
+    xh = w.x.cpu().pin_memory().numpy()
+    if args.config == "c2":
+        outh = torch.empty((cfg["batch"], 2 * cfg["k"]), dtype=torch.float32).pin_memory().numpy()
+        run = lambda: w.spn.embed(w.fm, xh, out=outh)  # noqa: E731
+        bi, bo = xh.nbytes, outh.nbytes
+    else:
+        outh = torch.empty((cfg["batch"], 1024), dtype=torch.float32).pin_memory().numpy()
+        run = lambda: w.sp.plan.apply(xh, out=outh)  # noqa: E731
+        bi, bo = xh.nbytes, outh.nbytes
+    run()
+    steps = max(3, min(args.steps, 10))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run()
+    dt = time.perf_counter() - t0
+    dt = max_over_ranks(dt, world)
+    return {"value": w.vectors * world * steps / dt, "unit": UNIT, "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo, "steps": steps, "api": "spn_embed_f32_host" if args.config == "c2"
+            else "spn_apply_f32_host"}
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_reference(config, budget_s=20.0, threads=None):
+    """The reference's own CPU code (oracle/_ref: proj/src compiled unmodified) on the
+    host cores, over a bounded sample of the same workload.  Returns (vectors/s, info)."""
+    import numpy as np
+    from oracle.oracle import HD3, Oracle, Reference
+    threads = threads or os.cpu_count() or 1
+    r, o = Reference(), Oracle()
+    cfg = CONFIGS[config]
+    rng = np.random.default_rng(0)
+
+    def timed(fn, count):
+        t0 = time.perf_counter()
+        fn(count)
+        return time.perf_counter() - t0
+
+    if config == "c1":
+        x = rng.standard_normal((cfg["batch"], 1024)).astype(np.float32)
+        fn = lambda c: (r.hash(HD3, 1024, 1024, [42], x[:c], threads=threads),  # noqa: E731
+                        r.apply(HD3, 1024, 1024, 1024, 42, 1.0, x[:c], threads=threads))
+        total = cfg["batch"]
+        what = "CrossPolytopeHasher::hash + StructuredSpinner::apply(scale 1)"
+    elif config == "c2":
+        x = rng.random((cfg["batch"], cfg["n_in"])).astype(np.float32)
+        fn = lambda c: r.embed(HD3, 1024, cfg["k"], 5, 0, cfg["sigma"], x[:c], n_in=cfg["n_in"],  # noqa: E731
+                               threads=threads)
+        total = cfg["batch"]
+        what = "embed(FeatureMap{StackedSpinner(HD3,1024,1024,4096)}, gaussian sigma=5)"
+    elif config == "c3":
+        x = rng.standard_normal((4096, cfg["n"])).astype(np.float32)
+        seeds = [o.mix_seed(3, t) for t in range(cfg["tables"])]
+        fn = lambda c: r.hash(HD3, cfg["n"], cfg["n"], seeds, x[:c], threads=threads)  # noqa: E731
+        total = x.shape[0]
+        what = "8 x CrossPolytopeHasher::hash (n=16384)"
+    elif config == "c4":
+        a = rng.standard_normal((cfg["N"], cfg["d"])).astype(np.float32)
+        rows = o.sample_rows(cfg["N"], cfg["m"], 77)
+        fn = lambda c: r.sketch(HD3, np.ascontiguousarray(a[:, :c]), cfg["m"], 11, row_list=rows,  # noqa: E731
+                                threads=threads)
+        total = cfg["d"]
+        what = "SketchOperator::apply restated over the reference StackedSpinner, random P"
+    else:
+        n = cfg["n"]
+        d = [a[0].astype(np.float32).astype(np.float64) for a in o.realize(100, n, n, n, 13)]
+        x = rng.standard_normal((cfg["batch"], n)).astype(np.float32)
+        fn = lambda c: r.chain(d[0], d[1], d[2], 1.0, x[:c], relu=True, threads=threads)  # noqa: E731
+        total = cfg["batch"]
+        what = "fwht_normalized/diag_matvec chain + ReLU, Gaussian D's"
+    # size the sample: a small probe, then up to `budget_s` of work
+    probe = max(1, min(total, threads))
+    dt = timed(fn, probe)
+    count = int(min(total, max(probe, probe * budget_s / max(dt, 1e-6) * 0.5)))
+    dt = timed(fn, count)
+    return count / dt, {"kind": "reference", "cores": threads,
+                        "sample": f"{count} of {total} vectors of {config}: {what}; oracle/_ref on {threads} threads"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    cfg = CONFIGS[args.config]
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        v, info = cpu_reference(args.config, budget_s=4.0)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "name": args.config},
+            "cpu_baseline": dict(info, value=value, unit=UNIT),
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":  # host-CPU arm: rank 0 only, no GPU work
+        rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    rank, world, local = dist_init()
+    res, w = run_ours(args, rank, world, local)
+    if rank == 0:
+        if world == 1 and not args.no_cpu:
+            v, info = cpu_reference(args.config)
+            res["cpu_baseline"] = dict(info, value=v, unit=UNIT)
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

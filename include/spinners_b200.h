@@ -1,0 +1,152 @@
+/* spinners_b200 — C ABI of the B200-native structured-spinner hot path.
+ *
+ * The reference (arxiv 1610.06209 code, proj/) has no FFI: its boundary is the
+ * C++ headers in proj/include/spinners/.  Each entry point below is what a
+ * binding of those headers' hot-path entry points needs:
+ *
+ *   spn_plan_create          <- StructuredSpinner::build / StackedSpinner(v,n,m,k,seed)
+ *                               (proj/include/spinners/spinner.hpp:58,110;
+ *                                proj/src/spinner.cpp:137-151,248-256) and, with
+ *                               tables>1, make_hasher_factory(v,n,m)(seed_t)
+ *                               (proj/include/spinners/lsh.hpp:66, proj/src/lsh.cpp:32-36)
+ *   spn_apply_f32            <- StackedSpinner::apply / StructuredSpinner::apply
+ *                               (spinner.hpp:62,114; spinner.cpp:200-231,272-283)
+ *   spn_hash_f32             <- CrossPolytopeHasher::hash + signed_argmax
+ *                               (lsh.hpp:21,30; lsh.cpp:9-30)
+ *   spn_embed_f32            <- embed(FeatureMap, x) (kernels.hpp:33; kernels.cpp:17-36)
+ *   spn_sketch_f32           <- SketchOperator::apply (newton_sketch.hpp:64;
+ *                               newton_sketch.cpp:74-101)
+ *   spn_*_host               <- the same calls on host buffers (the reference's
+ *                               value-semantics API), with the H2D/D2H copies inside.
+ *
+ * Conventions: plain pointers and sizes; all sizes/strides in elements;
+ * device entry points are stream-ordered and asynchronous (stream = a
+ * cudaStream_t, NULL = legacy default stream); `_host` entry points are
+ * synchronous.  Errors are status codes; spn_last_error() holds the message
+ * of the calling thread's last failure.  Reference exceptions map as
+ * DimensionError -> SPN_EDIM, DomainError -> SPN_EDOMAIN (common.hpp:15-27).
+ *
+ * Numerics: fp32 arithmetic on the device with the reference's fp64 diagonals
+ * rounded to fp32 (±1 diagonals are exact).  Per-element finiteness checks of
+ * the reference (check_finite, common.hpp:37-41) are NOT done on the device
+ * path; spn_check_finite_f32 exists for callers that need them.
+ */
+#ifndef SPINNERS_B200_H
+#define SPINNERS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPN_API __attribute__((visibility("default")))
+
+typedef enum spn_status {
+  SPN_OK = 0,
+  SPN_EDIM = 1,         /* DimensionError: non-pow2 n, bad m/k, length mismatch */
+  SPN_EDOMAIN = 2,      /* DomainError: non-finite / zero input, bad variant or sigma */
+  SPN_ECUDA = 3,        /* CUDA runtime failure */
+  SPN_ENOMEM = 4,       /* device / pinned allocation failed */
+  SPN_EUNSUPPORTED = 5, /* valid request this build does not implement */
+  SPN_EINVAL = 6        /* null pointer / bad argument */
+} spn_status;
+
+typedef enum spn_variant {
+  SPN_HD3_HD2_HD1 = 0, /* SpinnerVariant::hd3_hd2_hd1 (spinner.hpp:19) */
+  SPN_HDG_HD2_HD1 = 1, /* SpinnerVariant::hdg_hd2_hd1 (spinner.hpp:20) */
+  SPN_GAUSS3 = 100     /* builder-defined: D1..D3 all N(0,1) (BASELINE config 5) */
+} spn_variant;
+
+typedef enum spn_embed_kind { SPN_EMBED_GAUSSIAN = 0, SPN_EMBED_ANGULAR = 1 } spn_embed_kind;
+
+typedef struct spn_plan spn_plan;
+
+typedef struct spn_plan_desc {
+  int32_t variant;             /* spn_variant */
+  int64_t n;                   /* input dimension, power of two, 2 <= n <= 2^20 */
+  int64_t m;                   /* rows per block, 1 <= m <= n */
+  int64_t k;                   /* rows per table (stacked blocks: ceil(k/m)), k >= 1 */
+  int64_t tables;              /* independent stacked spinners (LSH tables), >= 1 */
+  const uint64_t* table_seeds; /* [tables] StackedSpinner seeds; NULL => {seed} */
+  uint64_t seed;               /* used when table_seeds == NULL (tables must be 1) */
+  double scale;                /* 0 => default_scale(variant, n) = sqrt(n) (spinner.cpp:41-45) */
+  int32_t device;              /* CUDA device ordinal */
+} spn_plan_desc;
+
+SPN_API const char* spn_status_string(spn_status s);
+SPN_API const char* spn_last_error(void);
+SPN_API const char* spn_version(void);
+
+/* Realise the diagonals with the reference's seeded generator on the host
+ * (mix_seed + mt19937_64 + Box-Muller, common.hpp:51-92) and upload them. */
+SPN_API spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* desc);
+/* Same, with caller-provided diagonals [tables][blocks][n] (e.g. a fitted tail
+ * vector, StructuredSpinner::with_tail_vector, spinner.hpp:80). */
+SPN_API spn_status spn_plan_create_explicit(spn_plan** out, int64_t n, int64_t m, int64_t k,
+                                            int64_t tables, const double* d1, const double* d2,
+                                            const double* d3, double scale, int32_t device);
+SPN_API spn_status spn_plan_destroy(spn_plan* plan);
+SPN_API spn_status spn_plan_query(const spn_plan* plan, int64_t* n, int64_t* m, int64_t* k,
+                                  int64_t* tables, int64_t* blocks, double* scale);
+/* The realised fp64 diagonals, [tables][blocks][n] each (for parity checks). */
+SPN_API spn_status spn_plan_diagonals(const spn_plan* plan, double* d1, double* d2, double* d3);
+
+/* y[b*ld_y + r] = relu?( scale * (stacked spinner x_b)[r] ), r < k.  x rows are
+ * zero padded from n_in to n (dataset.cpp:162-168).  Requires tables == 1. */
+SPN_API spn_status spn_apply_f32(const spn_plan* plan, const float* x, int64_t batch,
+                                 int64_t ld_x, int64_t n_in, float* y, int64_t ld_y, int32_t relu,
+                                 void* stream);
+
+/* ids[b*tables + t] = index + (sign < 0 ? k : 0) of signed_argmax over table t's
+ * k rows (ties -> smallest index, sign(0) = +1).  If y != NULL (tables == 1)
+ * the projection is stored as by spn_apply_f32. */
+SPN_API spn_status spn_hash_f32(const spn_plan* plan, const float* x, int64_t batch,
+                                int64_t ld_x, int64_t n_in, int32_t* ids, float* y,
+                                int64_t ld_y, void* stream);
+
+/* Gaussian: out[b*ld + i] = cos(z_i/sigma)/sqrt(k), out[b*ld + k + i] = sin(z_i/sigma)/sqrt(k);
+ * angular: out[b*ld + i] = z_i < 0 ? -1 : +1.   z = scale * stacked(x). */
+SPN_API spn_status spn_embed_f32(const spn_plan* plan, int32_t kind, double sigma, const float* x,
+                                 int64_t batch, int64_t ld_x, int64_t n_in, float* out,
+                                 int64_t ld_out, void* stream);
+
+/* Sketch along the long (strided) axis of a row-major A[n_in][d] (ld_a):
+ * out[r*ld_out + c] = norm * scale * (H D3 H D2 H D1 a_c)[rows[r]] for r < m_out,
+ * a_c = column c zero padded to n.  rows == NULL => rows 0..m_out-1 (the
+ * reference's first-m P); rows is a HOST array of distinct indices < n.
+ * Requires tables == 1, blocks == 1. */
+SPN_API spn_status spn_sketch_f32(const spn_plan* plan, const float* a, int64_t n_in, int64_t d,
+                                  int64_t ld_a, const int64_t* rows, int64_t m_out, double norm,
+                                  float* out, int64_t ld_out, void* stream);
+
+/* Host-buffer variants: pinned or pageable host memory in and out; the copies
+ * are pipelined with the kernels in chunks.  Synchronous. */
+SPN_API spn_status spn_apply_f32_host(const spn_plan* plan, const float* x, int64_t batch,
+                                      int64_t ld_x, int64_t n_in, float* y, int64_t ld_y,
+                                      int32_t relu);
+SPN_API spn_status spn_hash_f32_host(const spn_plan* plan, const float* x, int64_t batch,
+                                     int64_t ld_x, int64_t n_in, int32_t* ids);
+SPN_API spn_status spn_embed_f32_host(const spn_plan* plan, int32_t kind, double sigma,
+                                      const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
+                                      float* out, int64_t ld_out);
+
+/* Builder-defined coordinate sampler P (BASELINE config 4): m distinct indices of
+ * [0, N) via a partial Fisher-Yates driven by Rng(mix_seed(seed, 0x5a3b)), sorted. */
+SPN_API spn_status spn_sample_rows(int64_t N, int64_t m, uint64_t seed, int64_t* out);
+/* One block's diagonals realised from its spec seed exactly as
+ * StructuredSpinner::build does (spinner.cpp:137-151): d1,d2 <- Rng(mix_seed(seed,1)),
+ * d3 (or g) <- Rng(mix_seed(seed,2)).  Each output has n doubles. */
+SPN_API spn_status spn_realize_block(int32_t variant, int64_t n, uint64_t spec_seed, double* d1,
+                                     double* d2, double* d3);
+/* The reference's splitmix64 seed mixer (common.hpp:51-56). */
+SPN_API uint64_t spn_mix_seed(uint64_t base, uint64_t stream);
+/* Device-side finiteness / all-zero check of a batch of rows: flags[b] bit0 =
+ * non-finite entry, bit1 = all zero (what hash/embed reject, lsh.cpp:24-28). */
+SPN_API spn_status spn_check_rows_f32(const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
+                                      int32_t* flags, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPINNERS_B200_H */

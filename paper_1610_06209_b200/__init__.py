@@ -1,0 +1,551 @@
+"""B200-native structured spinners (arxiv 1610.06209) — Python host mirror.
+
+A thin ctypes layer over the C ABI in ``include/spinners_b200.h`` whose classes
+mirror the reference's C++ entry points (``proj/include/spinners/*.hpp``):
+
+=========================  ==============================================================
+this module                reference
+=========================  ==============================================================
+``SpinnerVariant``         ``SpinnerVariant`` (spinner.hpp:18-25)
+``StructuredSpinner``      ``StructuredSpinner::build/apply`` (spinner.hpp:56-104)
+``StackedSpinner``         ``StackedSpinner(v,n,m,k,seed)/apply`` (spinner.hpp:108-123)
+``signed_argmax``          ``signed_argmax`` (lsh.hpp:21) — host helper on a projection
+``CrossPolytopeHasher``    ``CrossPolytopeHasher::hash`` (lsh.hpp:26-36)
+``make_hasher_factory``    ``make_hasher_factory`` (lsh.hpp:66, lsh.cpp:32-36)
+``MultiTableHasher``       L tables at once (builder-defined, BASELINE config 3)
+``KernelKind/FeatureMap``  ``KernelKind``/``FeatureMap`` (kernels.hpp:11-28)
+``embed``                  ``embed`` (kernels.hpp:33, kernels.cpp:17-36)
+``SketchOperator``         ``SketchOperator`` (newton_sketch.hpp:50-71)
+``mix_seed``               ``mix_seed`` (common.hpp:51-56)
+=========================  ==============================================================
+
+Inputs may be CUDA ``torch.Tensor`` s (device path: stream-ordered kernels, no
+copies) or host arrays (numpy / CPU tensors: the ``spn_*_host`` entry points,
+which pipeline the host<->device copies with the kernels).  All arithmetic runs
+in the sm_100a kernels of ``_lib/libspinners_b200.so``; there is no CPU
+fallback — importing this module without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libspinners_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the sm_100a extension first "
+        "(python -m paper_1610_06209_b200.build_ext or __graft_entry__.build())")
+
+_lib = C.CDLL(LIB_PATH)
+
+# ----------------------------------------------------------------------------- ABI
+_i64, _u64, _i32, _dbl, _vp = C.c_int64, C.c_uint64, C.c_int32, C.c_double, C.c_void_p
+
+
+class _Desc(C.Structure):
+    _fields_ = [("variant", _i32), ("n", _i64), ("m", _i64), ("k", _i64), ("tables", _i64),
+                ("table_seeds", C.POINTER(_u64)), ("seed", _u64), ("scale", _dbl), ("device", _i32)]
+
+
+def _sig(name, res, args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = args
+    return f
+
+
+_status_string = _sig("spn_status_string", C.c_char_p, [C.c_int])
+_last_error = _sig("spn_last_error", C.c_char_p, [])
+_version = _sig("spn_version", C.c_char_p, [])
+_plan_create = _sig("spn_plan_create", C.c_int, [C.POINTER(_vp), C.POINTER(_Desc)])
+_plan_create_explicit = _sig("spn_plan_create_explicit", C.c_int,
+                             [C.POINTER(_vp), _i64, _i64, _i64, _i64, _vp, _vp, _vp, _dbl, _i32])
+_plan_destroy = _sig("spn_plan_destroy", C.c_int, [_vp])
+_plan_query = _sig("spn_plan_query", C.c_int, [_vp] + [C.POINTER(_i64)] * 5 + [C.POINTER(_dbl)])
+_plan_diagonals = _sig("spn_plan_diagonals", C.c_int, [_vp, _vp, _vp, _vp])
+_apply = _sig("spn_apply_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i32, _vp])
+_hash = _sig("spn_hash_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp])
+_embed = _sig("spn_embed_f32", C.c_int, [_vp, _i32, _dbl, _vp, _i64, _i64, _i64, _vp, _i64, _vp])
+_sketch = _sig("spn_sketch_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _dbl, _vp, _i64, _vp])
+_apply_host = _sig("spn_apply_f32_host", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i32])
+_hash_host = _sig("spn_hash_f32_host", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp])
+_embed_host = _sig("spn_embed_f32_host", C.c_int, [_vp, _i32, _dbl, _vp, _i64, _i64, _i64, _vp, _i64])
+_sample_rows = _sig("spn_sample_rows", C.c_int, [_i64, _i64, _u64, _vp])
+_mix_seed = _sig("spn_mix_seed", _u64, [_u64, _u64])
+_check_rows = _sig("spn_check_rows_f32", C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp])
+
+SPN_OK, SPN_EDIM, SPN_EDOMAIN, SPN_ECUDA, SPN_ENOMEM, SPN_EUNSUPPORTED, SPN_EINVAL = range(7)
+ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_create",
+               "spn_plan_create_explicit", "spn_plan_destroy", "spn_plan_query", "spn_plan_diagonals",
+               "spn_apply_f32", "spn_hash_f32", "spn_embed_f32", "spn_sketch_f32", "spn_apply_f32_host",
+               "spn_hash_f32_host", "spn_embed_f32_host", "spn_sample_rows", "spn_mix_seed",
+               "spn_check_rows_f32", "spn_realize_block")
+
+
+# ----------------------------------------------------------------------- errors
+class SpinnerError(RuntimeError):
+    """CUDA / resource / unsupported-request failure (status >= 3)."""
+
+
+class DimensionError(ValueError):
+    """Mirrors spinners::DimensionError (common.hpp:15-17)."""
+
+
+class DomainError(ValueError):
+    """Mirrors spinners::DomainError (common.hpp:19-21)."""
+
+
+def _check(status: int) -> None:
+    if status == SPN_OK:
+        return
+    msg = f"{_status_string(status).decode()}: {_last_error().decode()}"
+    if status == SPN_EDIM:
+        raise DimensionError(msg)
+    if status == SPN_EDOMAIN:
+        raise DomainError(msg)
+    raise SpinnerError(msg)
+
+
+def version() -> str:
+    return _version().decode()
+
+
+def mix_seed(base: int, stream: int) -> int:
+    """splitmix64 seed derivation (common.hpp:51-56)."""
+    return int(_mix_seed(base & (2**64 - 1), stream & (2**64 - 1)))
+
+
+def sample_rows(N: int, m: int, seed: int) -> np.ndarray:
+    """Builder-defined coordinate sampler P: m distinct sorted indices of [0, N)."""
+    out = np.zeros(m, dtype=np.int64)
+    _check(_sample_rows(N, m, seed & (2**64 - 1), out.ctypes.data))
+    return out
+
+
+class SpinnerVariant(enum.IntEnum):
+    """spinner.hpp:18-25 (the Hadamard-only variants) + the all-Gaussian config-5 variant."""
+    hd3_hd2_hd1 = 0
+    hdg_hd2_hd1 = 1
+    gauss3 = 100  # builder-defined: D1..D3 iid N(0,1)
+
+
+_VARIANT_NAMES = {"HD3HD2HD1": SpinnerVariant.hd3_hd2_hd1, "HDgHD2HD1": SpinnerVariant.hdg_hd2_hd1,
+                  "Gauss3": SpinnerVariant.gauss3}
+
+
+def variant_from_string(s: str) -> SpinnerVariant:
+    """spinner.cpp:21-25 (only the variants this hot path implements)."""
+    try:
+        return _VARIANT_NAMES[s]
+    except KeyError:
+        raise DomainError(f"unknown spinner variant: {s}") from None
+
+
+# ------------------------------------------------------------------ buffers
+def _torch():
+    import torch
+    return torch
+
+
+def _is_cuda(x) -> bool:
+    try:
+        torch = _torch()
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return _torch().cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _rows2d(x):
+    one = x.ndim == 1
+    if one:
+        x = x.reshape(1, -1)
+    if x.ndim != 2:
+        raise DimensionError("expected a vector or a [batch, n] matrix")
+    return x, one
+
+
+class _Plan:
+    """Owns one spn_plan* (device-resident realised diagonals)."""
+
+    def __init__(self, handle: int, device: int):
+        self._h = _vp(handle)
+        self.device = device
+        n, m, k, t, b, sc = _i64(), _i64(), _i64(), _i64(), _i64(), _dbl()
+        _check(_plan_query(self._h, C.byref(n), C.byref(m), C.byref(k), C.byref(t), C.byref(b), C.byref(sc)))
+        self.n, self.m, self.k, self.tables, self.blocks, self.scale = (
+            n.value, m.value, k.value, t.value, b.value, sc.value)
+
+    @classmethod
+    def create(cls, variant, n, m, k, tables=1, table_seeds=None, seed=0, scale=0.0, device=0):
+        d = _Desc()
+        d.variant, d.n, d.m, d.k, d.tables = int(variant), n, m, k, tables
+        seeds = None
+        if table_seeds is not None:
+            seeds = (_u64 * len(table_seeds))(*[int(s) & (2**64 - 1) for s in table_seeds])
+            d.table_seeds = C.cast(seeds, C.POINTER(_u64))
+        d.seed, d.scale, d.device = int(seed) & (2**64 - 1), float(scale), int(device)
+        h = _vp()
+        _check(_plan_create(C.byref(h), C.byref(d)))
+        return cls(h.value, device)
+
+    @classmethod
+    def create_explicit(cls, d1, d2, d3, n, m, k, tables=1, scale=0.0, device=0):
+        arrs = [np.ascontiguousarray(a, dtype=np.float64).reshape(-1) for a in (d1, d2, d3)]
+        h = _vp()
+        _check(_plan_create_explicit(C.byref(h), n, m, k, tables, arrs[0].ctypes.data, arrs[1].ctypes.data,
+                                     arrs[2].ctypes.data, float(scale), int(device)))
+        return cls(h.value, device)
+
+    def diagonals(self):
+        size = self.tables * self.blocks * self.n
+        out = [np.zeros(size) for _ in range(3)]
+        _check(_plan_diagonals(self._h, out[0].ctypes.data, out[1].ctypes.data, out[2].ctypes.data))
+        shape = (self.tables, self.blocks, self.n)
+        return tuple(o.reshape(shape) for o in out)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _plan_destroy(h)
+            self._h = _vp()
+
+    # ---- device / host dispatch helpers
+    def _device_in(self, x):
+        torch = _torch()
+        if x.dtype != torch.float32:
+            raise DomainError("device inputs must be float32")
+        x, one = _rows2d(x)
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        if x.shape[1] > self.n:
+            raise DimensionError(f"expected length <= {self.n}, got {x.shape[1]}")
+        return x, one
+
+    @staticmethod
+    def _host_in(x):
+        x = np.asarray(x)
+        if x.dtype != np.float32:
+            x = x.astype(np.float32)
+        x, one = _rows2d(x)
+        return np.ascontiguousarray(x), one
+
+    def apply(self, x, relu=False, out=None, stream=None):
+        if _is_cuda(x):
+            torch = _torch()
+            x, one = self._device_in(x)
+            y = out if out is not None else torch.empty((x.shape[0], self.k), device=x.device, dtype=torch.float32)
+            _check(_apply(self._h, x.data_ptr(), x.shape[0], x.stride(0), x.shape[1], y.data_ptr(), y.stride(0),
+                          int(relu), _stream_ptr(stream)))
+            return y[0] if one else y
+        x, one = self._host_in(x)
+        y = out if out is not None else np.empty((x.shape[0], self.k), dtype=np.float32)
+        _check(_apply_host(self._h, x.ctypes.data, x.shape[0], x.shape[1], x.shape[1], y.ctypes.data, y.shape[1],
+                           int(relu)))
+        return y[0] if one else y
+
+    def hash(self, x, y_out=None, stream=None):
+        if _is_cuda(x):
+            torch = _torch()
+            x, one = self._device_in(x)
+            ids = torch.empty((x.shape[0], self.tables), device=x.device, dtype=torch.int32)
+            yp, ldy = (y_out.data_ptr(), y_out.stride(0)) if y_out is not None else (None, 0)
+            _check(_hash(self._h, x.data_ptr(), x.shape[0], x.stride(0), x.shape[1], ids.data_ptr(), yp, ldy,
+                         _stream_ptr(stream)))
+            return ids[0] if one else ids
+        x, one = self._host_in(x)
+        ids = np.empty((x.shape[0], self.tables), dtype=np.int32)
+        _check(_hash_host(self._h, x.ctypes.data, x.shape[0], x.shape[1], x.shape[1], ids.ctypes.data))
+        return ids[0] if one else ids
+
+    def embed(self, kind, sigma, x, out=None, stream=None):
+        w = 2 * self.k if kind == 0 else self.k
+        if _is_cuda(x):
+            torch = _torch()
+            x, one = self._device_in(x)
+            o = out if out is not None else torch.empty((x.shape[0], w), device=x.device, dtype=torch.float32)
+            _check(_embed(self._h, kind, float(sigma), x.data_ptr(), x.shape[0], x.stride(0), x.shape[1],
+                          o.data_ptr(), o.stride(0), _stream_ptr(stream)))
+            return o[0] if one else o
+        x, one = self._host_in(x)
+        o = out if out is not None else np.empty((x.shape[0], w), dtype=np.float32)
+        _check(_embed_host(self._h, kind, float(sigma), x.ctypes.data, x.shape[0], x.shape[1], x.shape[1],
+                           o.ctypes.data, o.shape[1]))
+        return o[0] if one else o
+
+    def sketch(self, a, m_out, norm, rows=None, out=None, stream=None):
+        torch = _torch()
+        host = not _is_cuda(a)
+        if host:
+            a = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32))).cuda(self.device)
+        if a.dim() != 2 or a.stride(1) != 1:
+            a = a.reshape(a.shape[0], -1).contiguous()
+        o = out if out is not None else torch.empty((m_out, a.shape[1]), device=a.device, dtype=torch.float32)
+        rl = None
+        if rows is not None:
+            rows = np.ascontiguousarray(rows, dtype=np.int64)
+            if rows.size != m_out:
+                raise DimensionError("rows must have m_out entries")
+            rl = rows.ctypes.data
+        _check(_sketch(self._h, a.data_ptr(), a.shape[0], a.shape[1], a.stride(0), rl, m_out, float(norm),
+                       o.data_ptr(), o.stride(0), _stream_ptr(stream)))
+        if host:
+            return o.cpu().numpy()
+        return o
+
+
+def check_rows(x, stream=None):
+    """Device finiteness / zero-row flags (bit0 non-finite, bit1 all-zero)."""
+    torch = _torch()
+    x, _ = _rows2d(x)
+    flags = torch.empty(x.shape[0], dtype=torch.int32, device=x.device)
+    _check(_check_rows(x.data_ptr(), x.shape[0], x.stride(0), x.shape[1], flags.data_ptr(), _stream_ptr(stream)))
+    return flags
+
+
+# ------------------------------------------------------------ reference mirror
+class SpinnerSpec:
+    """spinner.hpp:40-53 — (variant, n, m, seed, scale); scale 0 => default sqrt(n)."""
+
+    def __init__(self, variant=SpinnerVariant.hd3_hd2_hd1, n=0, m=0, seed=0, scale=0.0):
+        self.variant, self.n, self.m, self.seed, self.scale = SpinnerVariant(variant), n, m, seed, scale
+
+    @staticmethod
+    def make(variant, n, m, seed):
+        s = SpinnerSpec(variant, n, m, seed, 0.0)
+        s.validate()
+        return s
+
+    def validate(self):  # spinner.cpp:59-67
+        if self.n < 1:
+            raise DimensionError("SpinnerSpec: n must be >= 1")
+        if self.m < 1 or self.m > self.n:
+            raise DimensionError("SpinnerSpec: need 1 <= m <= n")
+        if self.n & (self.n - 1):
+            raise DimensionError(
+                f"SpinnerSpec: Hadamard-bearing variant requires power-of-two n, got {self.n}")
+        if self.scale != 0.0 and not math.isfinite(self.scale):
+            raise DomainError("SpinnerSpec: non-finite scale")
+
+    def effective_scale(self):  # spinner.cpp:69-71
+        return self.scale if self.scale != 0.0 else math.sqrt(self.n)
+
+
+class StackedSpinner:
+    """k x n operator of ceil(k/m) independently seeded blocks (spinner.cpp:248-283).
+
+    ``scale`` overrides every block's SpinnerSpec.scale (0 = default sqrt(n))."""
+
+    def __init__(self, variant, n, m, k, seed, scale=0.0, device=0, _plan=None):
+        if k < 1:
+            raise DimensionError("StackedSpinner: k must be >= 1")
+        self.variant = SpinnerVariant(variant) if variant is not None else None
+        self._p = _plan or _Plan.create(variant, n, m, k, seed=seed, scale=scale, device=device)
+        self.seed = seed
+
+    @classmethod
+    def from_diagonals(cls, d1, d2, d3, n, m, k, scale=0.0, device=0):
+        return cls(None, n, m, k, 0, _plan=_Plan.create_explicit(d1, d2, d3, n, m, k, 1, scale, device))
+
+    def rows(self):
+        return self._p.k
+
+    def input_dim(self):
+        return self._p.n
+
+    @property
+    def plan(self):
+        return self._p
+
+    def diagonals(self):
+        """Realised fp64 (d1, d2, d3) as [blocks][n] arrays (d3 = g for HDg)."""
+        d1, d2, d3 = self._p.diagonals()
+        return d1[0], d2[0], d3[0]
+
+    def apply(self, x, relu=False, out=None, stream=None):
+        """y = scale * stacked(x); x shorter than n is zero padded.  ReLU optional."""
+        return self._p.apply(x, relu=relu, out=out, stream=stream)
+
+
+class StructuredSpinner(StackedSpinner):
+    """One m x n block (spinner.hpp:56-104): StructuredSpinner.build(spec).
+
+    The block's diagonals come from spec.seed directly (spinner.cpp:137-151),
+    realised by the library's host generator (spn_realize_block)."""
+
+    @classmethod
+    def build(cls, spec: SpinnerSpec, device=0):
+        spec.validate()
+        d = realize_block(spec.variant, spec.n, spec.seed)
+        p = _Plan.create_explicit(*d, spec.n, spec.m, spec.m, 1, spec.scale, device)
+        obj = cls(None, spec.n, spec.m, spec.m, spec.seed, _plan=p)
+        obj.variant = spec.variant
+        obj.spec = spec
+        return obj
+
+
+_realize_block = _sig("spn_realize_block", C.c_int, [_i32, _i64, _u64, _vp, _vp, _vp])
+
+
+def realize_block(variant, n, spec_seed):
+    """(d1, d2, d3) of one block realised from spec seed `spec_seed` with the
+    reference's generator (d3 is g for HDg, all three Gaussian for gauss3)."""
+    d = [np.zeros(n) for _ in range(3)]
+    _check(_realize_block(int(variant), n, int(spec_seed) & (2**64 - 1), *(a.ctypes.data for a in d)))
+    return tuple(d)
+
+
+def signed_argmax(y) -> tuple[int, int]:
+    """lsh.cpp:9-21 on a host vector (ties -> smallest index, sign(0) = +1)."""
+    y = np.asarray(y, dtype=np.float64).reshape(-1)
+    if y.size == 0:
+        raise DimensionError("signed_argmax: empty vector")
+    a = np.abs(y)
+    i = int(np.argmax(a))  # numpy returns the first maximal index
+    return i, (-1 if y[i] < 0.0 else 1)
+
+
+def decode_id(bucket: int, k: int) -> tuple[int, int]:
+    """int32 bucket id -> (index, sign): id = index + (sign < 0 ? k : 0)."""
+    return (int(bucket) - k, -1) if bucket >= k else (int(bucket), 1)
+
+
+class CrossPolytopeHasher:
+    """lsh.hpp:26-36: signed argmax over a stacked spinner's rows."""
+
+    def __init__(self, projector: StackedSpinner):
+        self._proj = projector
+
+    @property
+    def projector(self):
+        return self._proj
+
+    def hash_ids(self, x, stream=None):
+        """Batch: int32 bucket ids (index + k if the sign is negative)."""
+        ids = self._proj.plan.hash(x, stream=stream)
+        return ids[..., 0] if not hasattr(ids, "shape") or ids.ndim else ids
+
+    def hash(self, x):
+        """Single vector -> (index, sign), like CrossPolytopeHasher::hash.  Rejects
+        non-finite and all-zero input as the reference does (lsh.cpp:24-28)."""
+        xv = np.asarray(x.detach().cpu() if _is_cuda(x) else x, dtype=np.float64).reshape(-1)
+        if not np.all(np.isfinite(xv)):
+            raise DomainError("CrossPolytopeHasher::hash: non-finite entry")
+        if not np.any(xv != 0.0):
+            raise DomainError("CrossPolytopeHasher::hash: zero vector")
+        bucket = int(np.asarray(self._proj.plan.hash(xv.astype(np.float32)[None, :]))[0, 0])
+        return decode_id(bucket, self._proj.rows())
+
+
+def make_hasher_factory(variant, n, m, device=0):
+    """lsh.cpp:32-36: seed -> CrossPolytopeHasher(StackedSpinner(v, n, min(m,n), m, seed))."""
+    def factory(seed):
+        return CrossPolytopeHasher(StackedSpinner(variant, n, min(m, n), m, seed, device=device))
+    return factory
+
+
+class MultiTableHasher:
+    """L independent cross-polytope tables evaluated in one fused launch.
+
+    Table t is make_hasher_factory(variant, n, m)(table_seeds[t]); by default
+    table_seeds[t] = mix_seed(seed, t) (the per-trial derivation of lsh.cpp:56)."""
+
+    def __init__(self, variant, n, m, tables, seed=0, table_seeds: Optional[Sequence[int]] = None, device=0):
+        if table_seeds is None:
+            table_seeds = [mix_seed(seed, t) for t in range(tables)]
+        self.table_seeds = [int(s) for s in table_seeds]
+        self.k = m
+        self._p = _Plan.create(variant, n, min(m, n), m, tables=len(self.table_seeds),
+                               table_seeds=self.table_seeds, device=device)
+
+    @property
+    def plan(self):
+        return self._p
+
+    def hash_ids(self, x, stream=None):
+        return self._p.hash(x, stream=stream)
+
+
+class KernelKind:
+    """kernels.hpp:11-24."""
+    gaussian_tag, angular_tag = 0, 1
+
+    def __init__(self, tag, sigma):
+        self.tag, self.sigma = tag, sigma
+
+    @staticmethod
+    def gaussian(sigma):
+        if not sigma > 0.0:
+            raise DomainError("KernelKind: sigma must be positive")
+        return KernelKind(0, float(sigma))
+
+    @staticmethod
+    def angular():
+        return KernelKind(1, 0.0)
+
+
+class FeatureMap:
+    """kernels.hpp:26-30: a projector plus a kernel recipe."""
+
+    def __init__(self, projector: StackedSpinner, kind: KernelKind):
+        self.projector, self.kind = projector, kind
+
+
+def embed(fm: FeatureMap, x, out=None, stream=None):
+    """kernels.cpp:17-36.  Gaussian -> [cos(z/sigma) || sin(z/sigma)] / sqrt(d');
+    angular -> sign(z) with sign(0) = +1.  Batch or single vector."""
+    return fm.projector.plan.embed(fm.kind.tag, fm.kind.sigma, x, out=out, stream=stream)
+
+
+class SketchOperator:
+    """newton_sketch.hpp:50-71 (the spinner sketch; `rows` output rows).
+
+    mode "first" reproduces the reference (first `rows` rows of the padded
+    StackedSpinner); mode "random" is the builder-defined P = sample_rows(...)
+    of BASELINE config 4.  Output = sqrt(padded)/sqrt(rows) * P H D3 H D2 H D1 a_c."""
+
+    def __init__(self, variant, input_dim, rows, seed, mode="first", p_seed=None, device=0):
+        padded = 1 << max(0, (input_dim - 1).bit_length())
+        if rows > padded:
+            raise SpinnerError("SketchOperator: rows > padded dimension (multi-block sketch) not supported")
+        self.input_dim, self.padded, self.m = input_dim, padded, rows
+        self.norm = 1.0 / math.sqrt(rows)
+        self._p = _Plan.create(variant, padded, min(rows, padded), rows, seed=seed, device=device)
+        self.row_list = None
+        if mode == "random":
+            self.row_list = sample_rows(padded, rows, seed if p_seed is None else p_seed)
+        elif mode != "first":
+            raise DomainError(f"unknown sketch mode {mode}")
+
+    @property
+    def plan(self):
+        return self._p
+
+    def rows(self, input_dim=None):
+        return self.m
+
+    def apply(self, columns, out=None, stream=None):
+        """columns: [input_dim, d] (row-major; the sketch runs along axis 0)."""
+        if columns.shape[0] != self.input_dim:
+            raise DimensionError("SketchOperator::apply: row count mismatch")
+        return self._p.sketch(columns, self.m, self.norm, rows=self.row_list, out=out, stream=stream)
+
+
+__all__ = [
+    "SpinnerVariant", "SpinnerSpec", "StructuredSpinner", "StackedSpinner", "CrossPolytopeHasher",
+    "MultiTableHasher", "make_hasher_factory", "signed_argmax", "decode_id", "KernelKind", "FeatureMap",
+    "embed", "SketchOperator", "mix_seed", "sample_rows", "realize_block", "check_rows", "DimensionError", "DomainError",
+    "SpinnerError", "variant_from_string", "version", "LIB_PATH", "ABI_SYMBOLS",
+]

@@ -1,0 +1,467 @@
+// Fused structured-spinner kernels for n <= 2^14 (one "group" of T threads per vector).
+//
+// Computes, per vector x (fp32), the reference chain
+//     y = scale * first_m( H D3 H D2 H D1 x )          (proj/src/spinner.cpp:186-231)
+// with H the normalised Walsh-Hadamard transform (proj/src/transforms.cpp:52-71)
+// and fuses the nonlinearity that consumes y:
+//     OP_HASH        signed argmax -> int32 bucket id     (proj/src/lsh.cpp:9-30)
+//     OP_APPLY       store y (optionally ReLU, optionally + hash ids)
+//     OP_EMBED_GAUSS (1/sqrt(k)) [cos(y/sigma) || sin(y/sigma)]   (proj/src/kernels.cpp:27-35)
+//     OP_EMBED_ANG   sign(y) with sign(0) = +1                    (proj/src/kernels.cpp:23-26)
+//
+// Data layout (n = R*T, R = 2^LOG_R registers per thread, T = 2^LOG_T threads):
+//   layout B: thread t holds elements i = j*T + t  (j = register) -> coalesced global I/O
+//   layout A: thread t holds elements i = t*R + j                  -> 16-B smem vectors
+// Every FWHT runs its butterflies on the element bits that currently live in
+// registers (packed FADD2 on register pairs), exchanges layouts once through a
+// swizzled shared-memory transpose, and finishes the remaining bits.  Three
+// H's therefore cost three transposes (plus one for a layout-B epilogue).
+// All 1/sqrt(n) factors and the scale are folded into one multiplier.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace spn {
+
+enum Op : int { OP_HASH = 0, OP_APPLY = 1, OP_EMBED_GAUSS = 2, OP_EMBED_ANG = 3 };
+enum Layout : int { LAY_B = 0, LAY_A = 1 };
+
+// One diagonal position (D1/D2/D3) in one layout, for every (table, block).
+struct DiagArrays {
+  const uint32_t* sgn;  // ±1 diagonals: [tables*blocks][WORDS][T] bit-packed sign masks
+  const float* flt;     // real diagonals: [tables*blocks][R/4][T][4] (fp32)
+};
+
+struct VecParams {
+  const float* x;
+  int64_t ld_x, n_in, batch;
+  int64_t m, k;  // rows per block, rows per table
+  int blocks, tables;
+  DiagArrays d[3][2];  // [diagonal][layout]
+  int dsign[3];        // 1: diagonal is ±1 (use sgn), 0: real (use flt)
+  float c;             // scale * n^{-3/2}
+  float c2;            // OP_EMBED_GAUSS: c / sigma
+  float norm;          // OP_EMBED_GAUSS: 1/sqrt(k)
+  int32_t* ids;        // OP_HASH / OP_APPLY (optional): [batch][tables]
+  float* y;            // OP_APPLY / OP_EMBED_*: output rows
+  int64_t ld_y;
+  int relu;
+};
+
+template <int LOG_R_, int LOG_T_>
+struct VCfg {
+  static constexpr int LOG_R = LOG_R_, LOG_T = LOG_T_, LOG_N = LOG_R + LOG_T;
+  static constexpr int R = 1 << LOG_R, T = 1 << LOG_T, N = 1 << LOG_N;
+  static constexpr int THREADS = T >= 32 ? T : 256;          // CTA size
+  static constexpr int GPC = THREADS / T;                     // groups (vectors) per CTA
+  static constexpr int WORDS = R >= 32 ? R / 32 : 1;          // sign words per thread
+  static constexpr int BITS = R >= 32 ? 32 : R;               // valid bits per word
+  static constexpr int XMASK = (N / 4 >= 8 ? 8 : (N / 4 > 0 ? N / 4 : 1)) - 1;
+  static constexpr int SMEM_FLOATS = GPC * N + (T > 32 ? 4 * (T / 32) : 0);
+  static constexpr size_t SMEM_BYTES = sizeof(float) * (size_t)SMEM_FLOATS;
+  static constexpr bool MULTI_WARP = T > 32;
+};
+
+// ---------------------------------------------------------------- primitives
+
+// (a0,a1),(b0,b1) <- (a+b, a-b) on packed f32x2 (sm_100a FADD2; one issue slot for two adds).
+__device__ __forceinline__ void bfly2(float& a0, float& a1, float& b0, float& b1) {
+  asm("{\n\t.reg .b64 pa, pb, ps, pd;\n\t"
+      "mov.b64 pa, {%0, %1};\n\t"
+      "mov.b64 pb, {%2, %3};\n\t"
+      "add.rn.f32x2 ps, pa, pb;\n\t"
+      "sub.rn.f32x2 pd, pa, pb;\n\t"
+      "mov.b64 {%0, %1}, ps;\n\t"
+      "mov.b64 {%2, %3}, pd;\n\t}"
+      : "+f"(a0), "+f"(a1), "+f"(b0), "+f"(b1));
+}
+
+// Unnormalised butterflies over register bits [BLO, BHI) (transforms.cpp:58-67 restricted
+// to the element bits this thread holds).  Register pairs (2q, 2q+1) share one FADD2.
+template <int R, int BLO, int BHI>
+__device__ __forceinline__ void reg_fwht(float (&r)[R]) {
+#pragma unroll
+  for (int b = BLO; b < BHI; ++b) {
+    const int h = 1 << b;
+    if (b == 0) {
+#pragma unroll
+      for (int j = 0; j < R; j += 2) {
+        const float u = r[j], v = r[j + 1];
+        r[j] = u + v;
+        r[j + 1] = u - v;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < R; j += 2) {
+        if (j & h) continue;
+        bfly2(r[j], r[j + 1], r[j + h], r[j + h + 1]);
+      }
+    }
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (C::MULTI_WARP)
+    __syncthreads();
+  else
+    __syncwarp();
+}
+
+// Swizzled smem slot of element i: the 16-B chunk index (bits 2-4) is XORed with the
+// layout-A owner thread, making both the A-side 16-B accesses and the B-side 4-B
+// accesses bank-conflict free for R >= 32.
+template <class C>
+__device__ __forceinline__ int sw(int i) {
+  return i ^ (((i >> C::LOG_R) & C::XMASK) << 2);
+}
+
+// Swizzled addresses with the runtime part hoisted into 8 base offsets so every
+// access is base + immediate (R >= 32 and T >= 32, the performance configurations):
+//   A side, chunk q of thread t:  t*R + 4*(q ^ (t&7))            = a[q&7] + 4*(q & ~7)
+//   B side, register j:           j*T + (t ^ (((j >> (LOG_R-LOG_T)) & 7) << 2))
+template <class C>
+struct Swz {
+  static constexpr bool FAST = C::R >= 32 && C::T >= 32;
+  int a[8], b[8];
+  __device__ __forceinline__ explicit Swz(int t) {
+    if constexpr (FAST) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        a[c] = t * C::R + 4 * (c ^ (t & 7));
+        b[c] = t ^ (c << 2);
+      }
+    }
+  }
+  __device__ __forceinline__ int A(int t, int q) const {
+    if constexpr (FAST)
+      return a[q & 7] + 4 * (q & ~7);
+    else
+      return sw<C>(t * C::R + 4 * q);
+  }
+  __device__ __forceinline__ int B(int t, int j) const {
+    if constexpr (FAST)
+      return j * C::T + b[(j >> (C::LOG_R - C::LOG_T)) & 7];
+    else
+      return sw<C>(j * C::T + t);
+  }
+};
+
+template <class C>
+__device__ __forceinline__ void xpose_A_to_B(float (&r)[C::R], float* sm, int t) {
+  const Swz<C> z(t);
+  if constexpr (C::R >= 4) {
+#pragma unroll
+    for (int q = 0; q < C::R / 4; ++q)
+      *reinterpret_cast<float4*>(sm + z.A(t, q)) =
+          make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < C::R; ++j) sm[sw<C>(t * C::R + j)] = r[j];
+  }
+  group_sync<C>();
+#pragma unroll
+  for (int j = 0; j < C::R; ++j) r[j] = sm[z.B(t, j)];
+  group_sync<C>();
+}
+
+template <class C>
+__device__ __forceinline__ void xpose_B_to_A(float (&r)[C::R], float* sm, int t) {
+  const Swz<C> z(t);
+#pragma unroll
+  for (int j = 0; j < C::R; ++j) sm[z.B(t, j)] = r[j];
+  group_sync<C>();
+  if constexpr (C::R >= 4) {
+#pragma unroll
+    for (int q = 0; q < C::R / 4; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(sm + z.A(t, q));
+      r[4 * q] = v.x;
+      r[4 * q + 1] = v.y;
+      r[4 * q + 2] = v.z;
+      r[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < C::R; ++j) r[j] = sm[sw<C>(t * C::R + j)];
+  }
+  group_sync<C>();
+}
+
+// H on a vector whose registers are in layout B; ends in layout A.
+template <class C>
+__device__ __forceinline__ void fwht_B_to_A(float (&r)[C::R], float* sm, int t) {
+  reg_fwht<C::R, 0, C::LOG_R>(r);
+  if constexpr (C::T > 1) {
+    xpose_B_to_A<C>(r, sm, t);
+    reg_fwht<C::R, 0, C::LOG_T>(r);
+  }
+}
+
+// H on a vector in layout A; ends in layout B.
+template <class C>
+__device__ __forceinline__ void fwht_A_to_B(float (&r)[C::R], float* sm, int t) {
+  reg_fwht<C::R, 0, C::LOG_R>(r);
+  if constexpr (C::T > 1) {
+    xpose_A_to_B<C>(r, sm, t);
+    reg_fwht<C::R, C::LOG_R - C::LOG_T, C::LOG_R>(r);
+  }
+}
+
+// r <- D r, D given in the current layout (diag_matvec, transforms.cpp:228-235).
+template <class C>
+__device__ __forceinline__ void apply_diag(float (&r)[C::R], const DiagArrays& d, int is_sign,
+                                           int64_t tb, int t) {
+  if (is_sign) {
+    const uint32_t* w = d.sgn + tb * (int64_t)(C::WORDS * C::T);
+#pragma unroll
+    for (int q = 0; q < C::WORDS; ++q) {
+      const uint32_t word = __ldg(w + q * C::T + t);
+#pragma unroll
+      for (int jj = 0; jj < C::BITS; ++jj) {
+        const int j = q * 32 + jj;
+        r[j] = __uint_as_float(__float_as_uint(r[j]) ^ ((word << (31 - jj)) & 0x80000000u));
+      }
+    }
+  } else {
+    if constexpr (C::R >= 4) {
+      const float4* f = reinterpret_cast<const float4*>(d.flt + tb * (int64_t)C::N);
+#pragma unroll
+      for (int q = 0; q < C::R / 4; ++q) {
+        const float4 v = __ldg(f + q * C::T + t);
+        r[4 * q] *= v.x;
+        r[4 * q + 1] *= v.y;
+        r[4 * q + 2] *= v.z;
+        r[4 * q + 3] *= v.w;
+      }
+    } else {
+      const float* f = d.flt + tb * (int64_t)C::N;
+#pragma unroll
+      for (int j = 0; j < C::R; ++j) r[j] *= __ldg(f + j * C::T + t);
+    }
+  }
+}
+
+// Load row v in layout B (coalesced), zero padded beyond n_in (dataset.cpp:162-168).
+template <class C>
+__device__ __forceinline__ void load_x_B(float (&r)[C::R], const float* __restrict__ xrow,
+                                         int64_t n_in, int t) {
+  if (n_in >= C::N) {  // uniform fast path: no padding
+#pragma unroll
+    for (int j = 0; j < C::R; ++j) r[j] = __ldg(xrow + j * C::T + t);
+  } else {
+#pragma unroll
+    for (int j = 0; j < C::R; ++j) {
+      const int i = j * C::T + t;
+      r[j] = (i < n_in) ? __ldg(xrow + i) : 0.0f;
+    }
+  }
+}
+
+// Per-thread signed argmax over this thread's registers, whose element indices
+// increase with j (both layouts).  Branch-free: pass 1 takes max |y| (FMNMX on the
+// ALU pipe), pass 2 walks j downward so the FIRST register reaching the max wins
+// (strict '>' / smallest index, lsh.cpp:13-18).  Elements with index >= rows are
+// excluded.  Returns (|y|max, j*, y[j*]) with j* = -1 if nothing valid.
+template <class C>
+__device__ __forceinline__ void thread_argmax(const float (&r)[C::R], int first_i, int stride_i,
+                                              int rows, float& amax, int& jbest, float& vbest) {
+  float m = -1.0f;
+  if (first_i + (C::R - 1) * stride_i < rows) {
+#pragma unroll
+    for (int j = 0; j < C::R; ++j) m = fmaxf(m, fabsf(r[j]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < C::R; ++j)
+      if (first_i + j * stride_i < rows) m = fmaxf(m, fabsf(r[j]));
+  }
+  int jb = -1;
+  float vb = 0.0f;
+#pragma unroll
+  for (int j = C::R - 1; j >= 0; --j) {
+    const bool hit = fabsf(r[j]) == m;
+    jb = hit ? j : jb;
+    vb = hit ? r[j] : vb;
+  }
+  amax = m;
+  jbest = (m >= 0.0f) ? jb : -1;
+  vbest = vb;
+}
+
+// Running signed-argmax state (lsh.cpp:9-21): max |y|, ties to the smallest row.
+struct ArgBest {
+  float a;    // |y| (unscaled)
+  int gi;     // row within the table
+  float val;  // signed unscaled value
+};
+
+__device__ __forceinline__ void argbest_update(ArgBest& b, float v, int gi) {
+  const float a = fabsf(v);
+  if (a > b.a || (a == b.a && gi < b.gi)) {
+    b.a = a;
+    b.gi = gi;
+    b.val = v;
+  }
+}
+
+__device__ __forceinline__ void argbest_merge(ArgBest& b, float a, int gi, float val) {
+  if (a > b.a || (a == b.a && gi < b.gi)) {
+    b.a = a;
+    b.gi = gi;
+    b.val = val;
+  }
+}
+
+// Reduce the argmax over the T threads of a group; returns the winner in every thread
+// of the group (T <= 32) or in thread 0 of the CTA (T > 32).
+template <class C>
+__device__ __forceinline__ ArgBest group_argmax(ArgBest b, float* red) {
+  constexpr int LIM = C::T < 32 ? C::T : 32;
+#pragma unroll
+  for (int off = LIM / 2; off > 0; off >>= 1) {
+    const float oa = __shfl_xor_sync(0xffffffffu, b.a, off);
+    const int og = __shfl_xor_sync(0xffffffffu, b.gi, off);
+    const float ov = __shfl_xor_sync(0xffffffffu, b.val, off);
+    argbest_merge(b, oa, og, ov);
+  }
+  if constexpr (C::MULTI_WARP) {
+    constexpr int W = C::T / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+      red[w] = b.a;
+      reinterpret_cast<int*>(red)[W + w] = b.gi;
+      red[2 * W + w] = b.val;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 1; q < W; ++q) argbest_merge(b, red[q], reinterpret_cast<int*>(red)[W + q], red[2 * W + q]);
+    }
+    __syncthreads();
+  }
+  return b;
+}
+
+// ------------------------------------------------------------------- kernel
+
+template <int LOG_R, int LOG_T, int OP>
+__global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS)
+    spinner_vec_kernel(const VecParams p) {
+  using C = VCfg<LOG_R, LOG_T>;
+  extern __shared__ __align__(16) float smem[];
+  constexpr bool END_B = OP != OP_HASH;  // epilogue needs coalesced layout B
+  constexpr bool KEEP_X = (OP == OP_EMBED_GAUSS || OP == OP_EMBED_ANG) && C::R <= 32;
+
+  const int t = threadIdx.x & (C::T - 1);
+  const int g = threadIdx.x >> LOG_T;
+  float* sm = smem + g * C::N;
+  float* red = smem + C::GPC * C::N;
+
+  const int64_t per_vec = (OP == OP_HASH) ? p.tables : 1;
+  const int64_t total = p.batch * per_vec;
+  const bool want_ids = (OP == OP_HASH) || (OP == OP_APPLY && p.ids != nullptr);
+
+  for (int64_t base = (int64_t)blockIdx.x * C::GPC; base < total;
+       base += (int64_t)gridDim.x * C::GPC) {
+    const int64_t item = base + g;
+    const bool active = item < total;
+    const int64_t v = active ? item / per_vec : 0;
+    const int64_t tab = active ? item - v * per_vec : 0;
+    const float* xrow = p.x + v * p.ld_x;
+
+    float r[C::R];
+    float xk[KEEP_X ? C::R : 1];
+    load_x_B<C>(r, xrow, p.n_in, t);
+    if constexpr (END_B) {
+      if constexpr (C::T > 1) xpose_B_to_A<C>(r, sm, t);
+    }
+    if constexpr (KEEP_X) {
+#pragma unroll
+      for (int j = 0; j < C::R; ++j) xk[j] = r[j];
+    }
+
+    ArgBest best{-1.0f, 0x7fffffff, 0.0f};
+    for (int b = 0; b < p.blocks; ++b) {
+      if (b > 0) {
+        if constexpr (KEEP_X) {
+#pragma unroll
+          for (int j = 0; j < C::R; ++j) r[j] = xk[j];
+        } else {
+          load_x_B<C>(r, xrow, p.n_in, t);
+          if constexpr (END_B) {
+            if constexpr (C::T > 1) xpose_B_to_A<C>(r, sm, t);
+          }
+        }
+      }
+      const int64_t tb = tab * p.blocks + b;
+      const int64_t row0 = (int64_t)b * p.m;
+      const int64_t rows = min(p.m, p.k - row0);  // valid rows of this block (stacking, spinner.cpp:272-283)
+      if constexpr (!END_B) {
+        apply_diag<C>(r, p.d[0][LAY_B], p.dsign[0], tb, t);
+        fwht_B_to_A<C>(r, sm, t);
+        apply_diag<C>(r, p.d[1][LAY_A], p.dsign[1], tb, t);
+        fwht_A_to_B<C>(r, sm, t);
+        apply_diag<C>(r, p.d[2][LAY_B], p.dsign[2], tb, t);
+        fwht_B_to_A<C>(r, sm, t);
+        // layout A: element i = t*R + j, increasing j
+        float am, vb;
+        int jb;
+        thread_argmax<C>(r, t * C::R, 1, (int)rows, am, jb, vb);
+        if (jb >= 0) argbest_merge(best, am, (int)row0 + t * C::R + jb, vb);
+      } else {
+        apply_diag<C>(r, p.d[0][LAY_A], p.dsign[0], tb, t);
+        fwht_A_to_B<C>(r, sm, t);
+        apply_diag<C>(r, p.d[1][LAY_B], p.dsign[1], tb, t);
+        fwht_B_to_A<C>(r, sm, t);
+        apply_diag<C>(r, p.d[2][LAY_A], p.dsign[2], tb, t);
+        fwht_A_to_B<C>(r, sm, t);
+        // layout B: element i = j*T + t -> coalesced stores
+        float* yrow = p.y + v * p.ld_y + row0;
+        if constexpr (OP == OP_APPLY) {
+          if (want_ids) {
+            float am, vb;
+            int jb;
+            thread_argmax<C>(r, t, C::T, (int)rows, am, jb, vb);
+            if (jb >= 0) argbest_merge(best, am, (int)row0 + jb * C::T + t, vb);
+          }
+          if (p.y && active) {
+            const bool all_rows = rows >= C::N;
+#pragma unroll
+            for (int j = 0; j < C::R; ++j) {
+              const int i = j * C::T + t;
+              float out = r[j] * p.c;
+              if (p.relu) out = fmaxf(out, 0.0f);
+              if (all_rows || i < rows) __stcs(yrow + i, out);
+            }
+          }
+          continue;
+        }
+#pragma unroll
+        for (int j = 0; j < C::R; ++j) {
+          const int i = j * C::T + t;
+          if (!active || i >= rows) continue;
+          if constexpr (OP == OP_EMBED_GAUSS) {
+            float s, co;
+            sincosf(r[j] * p.c2, &s, &co);
+            __stcs(yrow + i, co * p.norm);
+            __stcs(yrow + p.k + i, s * p.norm);
+          } else {  // OP_EMBED_ANG
+            __stcs(yrow + i, (r[j] * p.c < 0.0f) ? -1.0f : 1.0f);
+          }
+        }
+      }
+    }
+
+    if (want_ids) {
+      best = group_argmax<C>(best, red);
+      const bool writer = C::MULTI_WARP ? (threadIdx.x == 0) : (t == 0);
+      if (writer && active) {
+        const float yb = best.val * p.c;
+        const int id = best.gi + ((yb < 0.0f) ? (int)p.k : 0);  // sign(0) = +1 (lsh.cpp:20)
+        p.ids[v * p.tables + tab] = id;
+      }
+    }
+  }
+}
+
+}  // namespace spn

@@ -1,0 +1,563 @@
+// spinners_b200: plan management + C ABI (include/spinners_b200.h) over the
+// sm_100a spinner kernels.  No CPU fallback: every compute entry point launches
+// a CUDA kernel or fails with a status code.
+#include "../../include/spinners_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "errors.hpp"
+#include "host_params.hpp"
+#include "spinner_big.cuh"
+#include "spinner_vec.cuh"
+#include "vec_launch.cuh"
+
+namespace {
+
+spn_status fail(spn_status s, const std::string& msg) { return spn::set_error(s, msg); }
+spn_status cuda_fail(cudaError_t e, const char* where) { return spn::cuda_error(e, where); }
+
+#define SPN_CUDA(call)                                         \
+  do {                                                         \
+    cudaError_t e_ = (call);                                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);        \
+  } while (0)
+
+bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+int ilog2(int64_t n) {
+  int l = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  return l;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+using spn::kMaxLogNVec;
+constexpr int kMaxLogN = 20;     // multi-pass path up to 2^20
+
+}  // namespace
+
+// ----------------------------------------------------------------------------- plan
+
+struct spn_plan {
+  int variant = 0;
+  int64_t n = 0, m = 0, k = 0, tables = 0, blocks = 0;
+  int log_n = 0;
+  double scale = 0.0;
+  int device = 0;
+  int sms = 0;
+  std::vector<double> d[3];  // realised fp64 diagonals [tables][blocks][n]
+  int dsign[3] = {0, 0, 0};
+
+  // vector-kernel layouts (n <= 2^14): [diag][layout]
+  uint32_t* vsgn[3][2] = {};
+  float* vflt[3][2] = {};
+  // multi-pass layouts (n > 2^14)
+  spn::BigPlan big;
+
+  // host-API staging (lazily grown; guarded by mu)
+  std::mutex mu;
+  cudaStream_t hs[2] = {nullptr, nullptr};
+  void* hbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  size_t hbuf_bytes[2][2] = {{0, 0}, {0, 0}};
+
+  ~spn_plan() {
+    DeviceGuard g(device);
+    for (auto& a : vsgn)
+      for (auto* p : a)
+        if (p) cudaFree(p);
+    for (auto& a : vflt)
+      for (auto* p : a)
+        if (p) cudaFree(p);
+    big.release();
+    for (auto& a : hbuf)
+      for (auto* p : a)
+        if (p) cudaFree(p);
+    for (auto s : hs)
+      if (s) cudaStreamDestroy(s);
+  }
+};
+
+namespace {
+
+// Element held by thread t in register j of a (LOG_R, LOG_T) group, per layout.
+inline int64_t elem(int layout, int LOG_R, int LOG_T, int64_t t, int64_t j) {
+  return layout == spn::LAY_A ? (t << LOG_R) + j : (j << LOG_T) + t;
+}
+
+spn_status upload(const void* src, size_t bytes, void** dst) {
+  SPN_CUDA(cudaMalloc(dst, bytes));
+  SPN_CUDA(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+  return SPN_OK;
+}
+
+// Pack the diagonals in the exact register order each kernel layout consumes.
+spn_status build_vec_layouts(spn_plan* p) {
+  const int LOG_R = (p->log_n + 1) / 2, LOG_T = p->log_n / 2;
+  const int64_t R = int64_t(1) << LOG_R, T = int64_t(1) << LOG_T, N = p->n;
+  const int64_t WORDS = R >= 32 ? R / 32 : 1, BITS = R >= 32 ? 32 : R;
+  const int64_t TB = p->tables * p->blocks;
+  for (int di = 0; di < 3; ++di) {
+    const double* D = p->d[di].data();
+    for (int lay = 0; lay < 2; ++lay) {
+      if (p->dsign[di]) {
+        std::vector<uint32_t> w(static_cast<size_t>(TB * WORDS * T), 0u);
+        for (int64_t tb = 0; tb < TB; ++tb)
+          for (int64_t q = 0; q < WORDS; ++q)
+            for (int64_t t = 0; t < T; ++t) {
+              uint32_t word = 0;
+              for (int64_t jj = 0; jj < BITS; ++jj)
+                if (D[tb * N + elem(lay, LOG_R, LOG_T, t, q * 32 + jj)] < 0.0) word |= 1u << jj;
+              w[static_cast<size_t>(tb * WORDS * T + q * T + t)] = word;
+            }
+        spn_status s = upload(w.data(), w.size() * 4, reinterpret_cast<void**>(&p->vsgn[di][lay]));
+        if (s) return s;
+      } else {
+        std::vector<float> f(static_cast<size_t>(TB * N));
+        for (int64_t tb = 0; tb < TB; ++tb)
+          for (int64_t t = 0; t < T; ++t)
+            for (int64_t j = 0; j < R; ++j) {
+              const int64_t pos = R >= 4 ? ((j / 4) * T + t) * 4 + (j % 4) : j * T + t;
+              f[static_cast<size_t>(tb * N + pos)] =
+                  static_cast<float>(D[tb * N + elem(lay, LOG_R, LOG_T, t, j)]);
+            }
+        spn_status s = upload(f.data(), f.size() * 4, reinterpret_cast<void**>(&p->vflt[di][lay]));
+        if (s) return s;
+      }
+    }
+  }
+  return SPN_OK;
+}
+
+spn_status finish_plan(spn_plan* p) {
+  p->log_n = ilog2(p->n);
+  for (int di = 0; di < 3; ++di) {
+    bool all = true;
+    for (double v : p->d[di])
+      if (v != 1.0 && v != -1.0) {
+        all = false;
+        break;
+      }
+    p->dsign[di] = all ? 1 : 0;
+  }
+  DeviceGuard g(p->device);
+  if (!g.ok) return fail(SPN_ECUDA, "cudaSetDevice failed");
+  SPN_CUDA(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device));
+  if (p->log_n <= kMaxLogNVec) return build_vec_layouts(p);
+  return p->big.build(p->n, p->tables * p->blocks, p->d, p->dsign);
+}
+
+spn_status validate_shape(int64_t n, int64_t m, int64_t k, int64_t tables) {
+  if (!is_pow2(n) || n < 2)
+    return fail(SPN_EDIM, "n must be a power of two >= 2, got " + std::to_string(n));
+  if (ilog2(n) > kMaxLogN) return fail(SPN_EUNSUPPORTED, "n > 2^20 not supported");
+  if (m < 1 || m > n) return fail(SPN_EDIM, "need 1 <= m <= n");
+  if (k < 1) return fail(SPN_EDIM, "k must be >= 1");
+  if (tables < 1) return fail(SPN_EDIM, "tables must be >= 1");
+  if (k > (int64_t(1) << 30)) return fail(SPN_EDIM, "k too large");
+  return SPN_OK;
+}
+
+// ------------------------------------------------------------ vector-kernel dispatch
+
+spn::LaunchFn vec_launcher(int log_n, int op) {
+  switch (op) {
+    case spn::OP_HASH: return spn::vec_launcher_hash(log_n);
+    case spn::OP_APPLY: return spn::vec_launcher_apply(log_n);
+    case spn::OP_EMBED_GAUSS: return spn::vec_launcher_gauss(log_n);
+    default: return spn::vec_launcher_ang(log_n);
+  }
+}
+
+spn::VecParams base_params(const spn_plan* p) {
+  spn::VecParams v{};
+  v.m = p->m;
+  v.k = p->k;
+  v.blocks = static_cast<int>(p->blocks);
+  v.tables = static_cast<int>(p->tables);
+  for (int di = 0; di < 3; ++di) {
+    v.dsign[di] = p->dsign[di];
+    for (int lay = 0; lay < 2; ++lay) v.d[di][lay] = {p->vsgn[di][lay], p->vflt[di][lay]};
+  }
+  v.c = static_cast<float>(p->scale * std::pow(static_cast<double>(p->n), -1.5));
+  return v;
+}
+
+spn_status check_io(const spn_plan* p, const void* x, int64_t batch, int64_t ld_x, int64_t n_in) {
+  if (!p) return fail(SPN_EINVAL, "null plan");
+  if (batch < 0) return fail(SPN_EINVAL, "batch < 0");
+  if (batch > 0 && !x) return fail(SPN_EINVAL, "null input");
+  if (n_in < 1 || n_in > p->n)
+    return fail(SPN_EDIM, "input length " + std::to_string(n_in) + " not in [1, n=" + std::to_string(p->n) + "]");
+  if (ld_x < n_in) return fail(SPN_EINVAL, "ld_x < n_in");
+  return SPN_OK;
+}
+
+spn_status run_vec(const spn_plan* p, int op, spn::VecParams& v, cudaStream_t s) {
+  const int64_t items = v.batch * (op == spn::OP_HASH ? p->tables : 1);
+  if (items == 0) return SPN_OK;
+  DeviceGuard g(p->device);
+  cudaError_t e = vec_launcher(p->log_n, op)(v, s, p->sms, items);
+  if (e != cudaSuccess) return cuda_fail(e, "spinner_vec_kernel launch");
+  return SPN_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+
+extern "C" {
+
+const char* spn_status_string(spn_status s) {
+  switch (s) {
+    case SPN_OK: return "ok";
+    case SPN_EDIM: return "dimension error";
+    case SPN_EDOMAIN: return "domain error";
+    case SPN_ECUDA: return "cuda error";
+    case SPN_ENOMEM: return "out of memory";
+    case SPN_EUNSUPPORTED: return "unsupported";
+    case SPN_EINVAL: return "invalid argument";
+  }
+  return "unknown status";
+}
+
+const char* spn_last_error(void) { return spn::last_error().c_str(); }
+const char* spn_version(void) { return "spinners_b200 0.1 (sm_100a)"; }
+uint64_t spn_mix_seed(uint64_t base, uint64_t stream) { return spn::mix_seed(base, stream); }
+
+spn_status spn_sample_rows(int64_t N, int64_t m, uint64_t seed, int64_t* out) {
+  if (!out) return fail(SPN_EINVAL, "null out");
+  if (N < 1 || m < 0 || m > N) return fail(SPN_EDIM, "need 0 <= m <= N, N >= 1");
+  std::vector<int64_t> r = spn::sample_rows(N, m, seed);
+  std::copy(r.begin(), r.end(), out);
+  return SPN_OK;
+}
+
+spn_status spn_realize_block(int32_t variant, int64_t n, uint64_t spec_seed, double* d1, double* d2,
+                             double* d3) {
+  if (!d1 || !d2 || !d3) return fail(SPN_EINVAL, "null argument");
+  if (variant != SPN_HD3_HD2_HD1 && variant != SPN_HDG_HD2_HD1 && variant != SPN_GAUSS3)
+    return fail(SPN_EDOMAIN, "unknown spinner variant " + std::to_string(variant));
+  if (n < 1) return fail(SPN_EDIM, "n must be >= 1");
+  spn::realize_block(variant, n, spec_seed, d1, d2, d3);
+  return SPN_OK;
+}
+
+spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) {
+  if (!out || !d) return fail(SPN_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->variant != SPN_HD3_HD2_HD1 && d->variant != SPN_HDG_HD2_HD1 && d->variant != SPN_GAUSS3)
+    return fail(SPN_EDOMAIN, "unknown spinner variant " + std::to_string(d->variant));
+  if (spn_status s = validate_shape(d->n, d->m, d->k, d->tables)) return s;
+  if (!d->table_seeds && d->tables != 1) return fail(SPN_EINVAL, "tables > 1 needs table_seeds");
+  if (d->scale != 0.0 && !std::isfinite(d->scale)) return fail(SPN_EDOMAIN, "non-finite scale");
+  auto* p = new spn_plan();
+  p->variant = d->variant;
+  p->n = d->n;
+  p->m = d->m;
+  p->k = d->k;
+  p->tables = d->tables;
+  p->blocks = (d->k + d->m - 1) / d->m;
+  p->device = d->device;
+  // default_scale: sqrt(n) for the Hadamard-only variants (spinner.cpp:41-45,69-71)
+  p->scale = d->scale != 0.0 ? d->scale : std::sqrt(static_cast<double>(d->n));
+  const int64_t per = p->blocks * p->n;
+  for (auto& v : p->d) v.resize(static_cast<size_t>(p->tables * per));
+  for (int64_t t = 0; t < p->tables; ++t) {
+    const uint64_t seed = d->table_seeds ? d->table_seeds[t] : d->seed;
+    for (int64_t b = 0; b < p->blocks; ++b) {
+      const int64_t off = t * per + b * p->n;
+      spn::realize_block(d->variant, p->n, spn::mix_seed(seed, static_cast<uint64_t>(b)),
+                         p->d[0].data() + off, p->d[1].data() + off, p->d[2].data() + off);
+    }
+  }
+  if (spn_status s = finish_plan(p)) {
+    delete p;
+    return s;
+  }
+  *out = p;
+  return SPN_OK;
+}
+
+spn_status spn_plan_create_explicit(spn_plan** out, int64_t n, int64_t m, int64_t k,
+                                    int64_t tables, const double* d1, const double* d2,
+                                    const double* d3, double scale, int32_t device) {
+  if (!out || !d1 || !d2 || !d3) return fail(SPN_EINVAL, "null argument");
+  *out = nullptr;
+  if (spn_status s = validate_shape(n, m, k, tables)) return s;
+  if (scale != 0.0 && !std::isfinite(scale)) return fail(SPN_EDOMAIN, "non-finite scale");
+  auto* p = new spn_plan();
+  p->variant = -1;
+  p->n = n;
+  p->m = m;
+  p->k = k;
+  p->tables = tables;
+  p->blocks = (k + m - 1) / m;
+  p->device = device;
+  p->scale = scale != 0.0 ? scale : std::sqrt(static_cast<double>(n));
+  const size_t total = static_cast<size_t>(tables * p->blocks * n);
+  const double* src[3] = {d1, d2, d3};
+  for (int di = 0; di < 3; ++di) {
+    p->d[di].assign(src[di], src[di] + total);
+    for (double v : p->d[di])
+      if (!std::isfinite(v)) {
+        delete p;
+        return fail(SPN_EDOMAIN, "non-finite diagonal entry");  // diag_matvec check, transforms.cpp:230
+      }
+  }
+  if (spn_status s = finish_plan(p)) {
+    delete p;
+    return s;
+  }
+  *out = p;
+  return SPN_OK;
+}
+
+spn_status spn_plan_destroy(spn_plan* p) {
+  delete p;
+  return SPN_OK;
+}
+
+spn_status spn_plan_query(const spn_plan* p, int64_t* n, int64_t* m, int64_t* k, int64_t* tables,
+                          int64_t* blocks, double* scale) {
+  if (!p) return fail(SPN_EINVAL, "null plan");
+  if (n) *n = p->n;
+  if (m) *m = p->m;
+  if (k) *k = p->k;
+  if (tables) *tables = p->tables;
+  if (blocks) *blocks = p->blocks;
+  if (scale) *scale = p->scale;
+  return SPN_OK;
+}
+
+spn_status spn_plan_diagonals(const spn_plan* p, double* d1, double* d2, double* d3) {
+  if (!p) return fail(SPN_EINVAL, "null plan");
+  double* dst[3] = {d1, d2, d3};
+  for (int di = 0; di < 3; ++di)
+    if (dst[di]) std::copy(p->d[di].begin(), p->d[di].end(), dst[di]);
+  return SPN_OK;
+}
+
+spn_status spn_apply_f32(const spn_plan* p, const float* x, int64_t batch, int64_t ld_x,
+                         int64_t n_in, float* y, int64_t ld_y, int32_t relu, void* stream) {
+  if (spn_status s = check_io(p, x, batch, ld_x, n_in)) return s;
+  if (p->tables != 1) return fail(SPN_EINVAL, "apply needs a single-table plan");
+  if (batch > 0 && !y) return fail(SPN_EINVAL, "null output");
+  if (ld_y < p->k) return fail(SPN_EINVAL, "ld_y < k");
+  if (p->log_n > kMaxLogNVec) {
+    DeviceGuard g(p->device);
+    return const_cast<spn_plan*>(p)->big.apply(x, batch, ld_x, n_in, y, ld_y, relu, p->k, p->m, p->blocks,
+                        p->scale * std::pow(static_cast<double>(p->n), -1.5), p->sms,
+                        static_cast<cudaStream_t>(stream));
+  }
+  spn::VecParams v = base_params(p);
+  v.x = x;
+  v.ld_x = ld_x;
+  v.n_in = n_in;
+  v.batch = batch;
+  v.y = y;
+  v.ld_y = ld_y;
+  v.relu = relu;
+  return run_vec(p, spn::OP_APPLY, v, static_cast<cudaStream_t>(stream));
+}
+
+spn_status spn_hash_f32(const spn_plan* p, const float* x, int64_t batch, int64_t ld_x,
+                        int64_t n_in, int32_t* ids, float* y, int64_t ld_y, void* stream) {
+  if (spn_status s = check_io(p, x, batch, ld_x, n_in)) return s;
+  if (batch > 0 && !ids) return fail(SPN_EINVAL, "null ids");
+  if (y && p->tables != 1) return fail(SPN_EINVAL, "y output needs a single-table plan");
+  if (y && ld_y < p->k) return fail(SPN_EINVAL, "ld_y < k");
+  if (p->k >= (int64_t(1) << 30)) return fail(SPN_EDIM, "2k must fit int32 ids");
+  if (p->log_n > kMaxLogNVec) return fail(SPN_EUNSUPPORTED, "hash with n > 2^14 not implemented");
+  spn::VecParams v = base_params(p);
+  v.x = x;
+  v.ld_x = ld_x;
+  v.n_in = n_in;
+  v.batch = batch;
+  v.ids = ids;
+  v.y = y;
+  v.ld_y = ld_y;
+  return run_vec(p, y ? spn::OP_APPLY : spn::OP_HASH, v, static_cast<cudaStream_t>(stream));
+}
+
+spn_status spn_embed_f32(const spn_plan* p, int32_t kind, double sigma, const float* x,
+                         int64_t batch, int64_t ld_x, int64_t n_in, float* out, int64_t ld_out,
+                         void* stream) {
+  if (spn_status s = check_io(p, x, batch, ld_x, n_in)) return s;
+  if (p->tables != 1) return fail(SPN_EINVAL, "embed needs a single-table plan");
+  if (kind != SPN_EMBED_GAUSSIAN && kind != SPN_EMBED_ANGULAR) return fail(SPN_EDOMAIN, "unknown kernel kind");
+  if (kind == SPN_EMBED_GAUSSIAN && !(sigma > 0.0))
+    return fail(SPN_EDOMAIN, "KernelKind: sigma must be positive");  // kernels.hpp:17
+  if (batch > 0 && !out) return fail(SPN_EINVAL, "null output");
+  if (ld_out < (kind == SPN_EMBED_GAUSSIAN ? 2 * p->k : p->k)) return fail(SPN_EINVAL, "ld_out too small");
+  if (p->log_n > kMaxLogNVec) return fail(SPN_EUNSUPPORTED, "embed with n > 2^14 not implemented");
+  spn::VecParams v = base_params(p);
+  v.x = x;
+  v.ld_x = ld_x;
+  v.n_in = n_in;
+  v.batch = batch;
+  v.y = out;
+  v.ld_y = ld_out;
+  v.c2 = static_cast<float>(p->scale * std::pow(static_cast<double>(p->n), -1.5) / sigma);
+  v.norm = static_cast<float>(1.0 / std::sqrt(static_cast<double>(p->k)));
+  return run_vec(p, kind == SPN_EMBED_GAUSSIAN ? spn::OP_EMBED_GAUSS : spn::OP_EMBED_ANG, v,
+                 static_cast<cudaStream_t>(stream));
+}
+
+spn_status spn_sketch_f32(const spn_plan* p, const float* a, int64_t n_in, int64_t d, int64_t ld_a,
+                          const int64_t* rows, int64_t m_out, double norm, float* out,
+                          int64_t ld_out, void* stream) {
+  if (!p) return fail(SPN_EINVAL, "null plan");
+  if (p->tables != 1 || p->blocks != 1) return fail(SPN_EUNSUPPORTED, "sketch needs one table of one block");
+  if (n_in < 1 || n_in > p->n) return fail(SPN_EDIM, "SketchOperator::apply: row count mismatch");
+  if (d < 0 || m_out < 0 || m_out > p->n) return fail(SPN_EDIM, "bad sketch shape");
+  if (ld_a < d || ld_out < d) return fail(SPN_EINVAL, "bad leading dimension");
+  if (d > 0 && m_out > 0 && (!a || !out)) return fail(SPN_EINVAL, "null pointer");
+  if (!rows && m_out > p->k) return fail(SPN_EDIM, "first-m sketch: m_out > k");
+  if (rows)
+    for (int64_t r = 0; r < m_out; ++r)
+      if (rows[r] < 0 || rows[r] >= p->n) return fail(SPN_EDIM, "row index out of range");
+  if (d == 0 || m_out == 0) return SPN_OK;
+  DeviceGuard g(p->device);
+  return spn::sketch_run(p->n, p->d, p->dsign, a, n_in, d, ld_a, rows, m_out,
+                         p->scale * std::pow(static_cast<double>(p->n), -1.5) * norm, out, ld_out,
+                         p->sms, static_cast<cudaStream_t>(stream), const_cast<spn::BigPlan*>(&p->big));
+}
+
+// --------------------------------------------------------------------- host-buffer API
+
+}  // extern "C"
+
+namespace {
+
+// Pipelined host->device->host execution over row chunks on two streams.
+template <class Launch>
+spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
+                         void* out, int64_t out_row_bytes, int64_t ld_out_bytes, Launch launch) {
+  if (batch == 0) return SPN_OK;
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard g(p->device);
+  const int64_t in_row = n_in * 4;
+  // ~48 MB of output per chunk keeps copies and kernels overlapped on PCIe/HBM.
+  int64_t chunk = std::max<int64_t>(1, (int64_t(48) << 20) / std::max<int64_t>(out_row_bytes, 1));
+  chunk = std::min(chunk, batch);
+  for (int s = 0; s < 2; ++s) {
+    if (!p->hs[s]) SPN_CUDA(cudaStreamCreateWithFlags(&p->hs[s], cudaStreamNonBlocking));
+    const size_t need[2] = {static_cast<size_t>(chunk * in_row), static_cast<size_t>(chunk * out_row_bytes)};
+    for (int b = 0; b < 2; ++b)
+      if (p->hbuf_bytes[s][b] < need[b]) {
+        if (p->hbuf[s][b]) cudaFree(p->hbuf[s][b]);
+        p->hbuf[s][b] = nullptr;
+        SPN_CUDA(cudaMalloc(&p->hbuf[s][b], need[b]));
+        p->hbuf_bytes[s][b] = need[b];
+      }
+  }
+  int c = 0;
+  for (int64_t r0 = 0; r0 < batch; r0 += chunk, ++c) {
+    const int s = c & 1;
+    const int64_t rows = std::min(chunk, batch - r0);
+    float* dx = static_cast<float*>(p->hbuf[s][0]);
+    char* dout = static_cast<char*>(p->hbuf[s][1]);
+    SPN_CUDA(cudaMemcpy2DAsync(dx, in_row, x + r0 * ld_x, ld_x * 4, in_row, rows, cudaMemcpyHostToDevice,
+                               p->hs[s]));
+    if (spn_status st = launch(dx, rows, n_in, dout, p->hs[s])) return st;
+    SPN_CUDA(cudaMemcpy2DAsync(static_cast<char*>(out) + r0 * ld_out_bytes, ld_out_bytes, dout, out_row_bytes,
+                               out_row_bytes, rows, cudaMemcpyDeviceToHost, p->hs[s]));
+  }
+  SPN_CUDA(cudaStreamSynchronize(p->hs[0]));
+  SPN_CUDA(cudaStreamSynchronize(p->hs[1]));
+  return SPN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+spn_status spn_apply_f32_host(const spn_plan* cp, const float* x, int64_t batch, int64_t ld_x,
+                              int64_t n_in, float* y, int64_t ld_y, int32_t relu) {
+  if (spn_status s = check_io(cp, x, batch, ld_x, n_in)) return s;
+  if (batch > 0 && !y) return fail(SPN_EINVAL, "null output");
+  if (ld_y < cp->k) return fail(SPN_EINVAL, "ld_y < k");
+  auto* p = const_cast<spn_plan*>(cp);
+  return host_pipeline(p, x, batch, ld_x, n_in, y, p->k * 4, ld_y * 4,
+                       [&](const float* dx, int64_t rows, int64_t nin, char* dout, cudaStream_t s) {
+                         return spn_apply_f32(p, dx, rows, nin, nin, reinterpret_cast<float*>(dout), p->k, relu, s);
+                       });
+}
+
+spn_status spn_hash_f32_host(const spn_plan* cp, const float* x, int64_t batch, int64_t ld_x,
+                             int64_t n_in, int32_t* ids) {
+  if (spn_status s = check_io(cp, x, batch, ld_x, n_in)) return s;
+  if (batch > 0 && !ids) return fail(SPN_EINVAL, "null ids");
+  auto* p = const_cast<spn_plan*>(cp);
+  return host_pipeline(p, x, batch, ld_x, n_in, ids, p->tables * 4, p->tables * 4,
+                       [&](const float* dx, int64_t rows, int64_t nin, char* dout, cudaStream_t s) {
+                         return spn_hash_f32(p, dx, rows, nin, nin, reinterpret_cast<int32_t*>(dout), nullptr, 0, s);
+                       });
+}
+
+spn_status spn_embed_f32_host(const spn_plan* cp, int32_t kind, double sigma, const float* x,
+                              int64_t batch, int64_t ld_x, int64_t n_in, float* out, int64_t ld_out) {
+  if (spn_status s = check_io(cp, x, batch, ld_x, n_in)) return s;
+  const int64_t w = kind == SPN_EMBED_GAUSSIAN ? 2 * cp->k : cp->k;
+  if (batch > 0 && !out) return fail(SPN_EINVAL, "null output");
+  if (ld_out < w) return fail(SPN_EINVAL, "ld_out too small");
+  auto* p = const_cast<spn_plan*>(cp);
+  return host_pipeline(p, x, batch, ld_x, n_in, out, w * 4, ld_out * 4,
+                       [&](const float* dx, int64_t rows, int64_t nin, char* dout, cudaStream_t s) {
+                         return spn_embed_f32(p, kind, sigma, dx, rows, nin, nin, reinterpret_cast<float*>(dout), w, s);
+                       });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ row checks
+
+namespace {
+__global__ void check_rows_kernel(const float* __restrict__ x, int64_t batch, int64_t ld, int64_t n_in,
+                                  int32_t* flags) {
+  for (int64_t r = blockIdx.x; r < batch; r += gridDim.x) {
+    int bad = 0, nz = 0;
+    for (int64_t i = threadIdx.x; i < n_in; i += blockDim.x) {
+      const float v = x[r * ld + i];
+      bad |= !isfinite(v);
+      nz |= (v != 0.0f);
+    }
+    bad = __syncthreads_or(bad);
+    nz = __syncthreads_or(nz);
+    if (threadIdx.x == 0) flags[r] = (bad ? 1 : 0) | (nz ? 0 : 2);
+  }
+}
+}  // namespace
+
+extern "C" spn_status spn_check_rows_f32(const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
+                                         int32_t* flags, void* stream) {
+  if (batch < 0 || n_in < 1 || ld_x < n_in) return fail(SPN_EINVAL, "bad shape");
+  if (batch == 0) return SPN_OK;
+  if (!x || !flags) return fail(SPN_EINVAL, "null pointer");
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(batch, 65535));
+  check_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, batch, ld_x, n_in, flags);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "check_rows_kernel");
+  return SPN_OK;
+}

@@ -1,0 +1,107 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol the
+header declares, and its host logic (seeded generator, sampler, argument
+validation) matches the reference.  No kernel launches here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import cases
+from conftest import ROOT
+from oracle.oracle import GAUSS3, HD3, HDG
+
+HEADER = os.path.join(ROOT, "include", "spinners_b200.h")
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"SPN_API\s+[\w\s\*]+?\b(spn_\w+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol(spn):
+    lib = ctypes.CDLL(spn.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(spn.ABI_SYMBOLS) <= set(syms)
+
+
+def test_library_is_sm100a(spn):
+    import subprocess
+    out = subprocess.run(["cuobjdump", "-lelf", spn.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_status_strings(spn):
+    assert "sm_100a" in spn.version()
+    assert spn._status_string(1).decode() == "dimension error"
+
+
+def test_mix_seed_matches_reference(spn, golden):
+    for (a, b), want in zip(golden["mix_seed_in"], golden["mix_seed_out"]):
+        assert spn.mix_seed(int(a), int(b)) == int(want)
+
+
+@pytest.mark.parametrize("v", [HD3, HDG, GAUSS3])
+@pytest.mark.parametrize("n,seed", [(16, 21), (1024, 7), (1 << 17, 11)])
+def test_host_generator_is_the_reference_generator(spn, oracle, v, n, seed):
+    got = spn.realize_block(v, n, seed)
+    want = oracle.realize_block(v, n, seed)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+def test_stacked_block_seeds_match_reference(spn, golden):
+    # StackedSpinner block b uses spec seed mix_seed(seed, b) (spinner.cpp:255)
+    for b in range(3):
+        d = spn.realize_block(HD3, 16, spn.mix_seed(44, b))
+        assert np.array_equal(d[0], golden["realize_v0_n16_k40_s44_d1"][b])
+        assert np.array_equal(d[2], golden["realize_v0_n16_k40_s44_d3"][b])
+
+
+def test_sampler_matches_oracle(spn, oracle):
+    for N, m, s in [(10, 3, 1), (1 << 17, 2048, 77), (64, 64, 2)]:
+        assert np.array_equal(spn.sample_rows(N, m, s), oracle.sample_rows(N, m, s))
+
+
+def test_config4_rows_fixture(spn, golden):
+    c = cases.C4
+    assert np.array_equal(spn.sample_rows(c["N"], c["m"], c["p_seed"]), golden["c4_rows"])
+
+
+def test_validation_errors_before_any_device_work(spn):
+    # spinner.cpp:59-67 -> DimensionError / DomainError, raised before CUDA is touched
+    with pytest.raises(spn.DimensionError):
+        spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, 6, 6, 6, 0)
+    with pytest.raises(spn.DimensionError):
+        spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, 8, 9, 9, 0)
+    with pytest.raises(spn.DimensionError):
+        spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, 8, 0, 8, 0)
+    with pytest.raises(spn.DimensionError):
+        spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, 8, 8, 0, 0)
+    with pytest.raises(spn.DomainError):
+        spn.variant_from_string("NotAVariant")
+    with pytest.raises(spn.DomainError):
+        spn.KernelKind.gaussian(0.0)
+    with pytest.raises(spn.DimensionError):
+        spn.sample_rows(4, 5, 0)
+    with pytest.raises(spn.DimensionError):
+        spn.SpinnerSpec.make(spn.SpinnerVariant.hd3_hd2_hd1, 12, 4, 0)
+
+
+def test_raw_abi_null_and_bad_arguments(spn):
+    lib = spn._lib
+    assert lib.spn_plan_create(None, None) == spn.SPN_EINVAL
+    assert lib.spn_plan_destroy(None) == spn.SPN_OK
+    assert spn._apply(None, None, 0, 0, 1, None, 0, 0, None) == spn.SPN_EINVAL
+    assert spn._realize_block(7, 8, 0, None, None, None) == spn.SPN_EINVAL
+
+
+def test_signed_argmax_host_helper(spn):
+    assert spn.signed_argmax([0.1, -0.9, 0.3]) == (1, -1)
+    assert spn.signed_argmax([-2.0, 2.0]) == (0, -1)
+    assert spn.signed_argmax([0.0, 0.0]) == (0, 1)
+    assert spn.decode_id(1030, 1024) == (6, -1) and spn.decode_id(6, 1024) == (6, 1)
