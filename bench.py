@@ -214,13 +214,19 @@ def run_ours(args, rank, world, local):
     w = Workload(args.config, cfg, rank, local)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if cfg["flush"] else None
-    for _ in range(max(3, args.warmup)):
-        w.step(stream)
-    torch.cuda.synchronize()
-    barrier(world)
-    torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        # warm-up, continued (untimed) until nvidia-smi has seen the GPU under this load
+        t_end = time.time() + 3.0
+        i = 0
+        while i < max(3, args.warmup) or (len(clk.samples) < 3 and time.time() < t_end):
+            w.step(stream)
+            i += 1
+            if i >= max(3, args.warmup):
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
         for i in range(args.steps):
             if flush is not None:
                 flush.fill_(i & 0xFF)  # evict L2 (256 MB > 126 MB) outside the timed region

@@ -41,12 +41,13 @@ struct VecParams {
   DiagArrays d[3][2];  // [diagonal][layout]
   int dsign[3];        // 1: diagonal is ±1 (use sgn), 0: real (use flt)
   float c;             // scale * n^{-3/2}
-  float c2;            // OP_EMBED_GAUSS: c / sigma
+  float c2;            // OP_EMBED_GAUSS: c / (2 pi sigma)  (argument in revolutions)
   float norm;          // OP_EMBED_GAUSS: 1/sqrt(k)
   int32_t* ids;        // OP_HASH / OP_APPLY (optional): [batch][tables]
   float* y;            // OP_APPLY / OP_EMBED_*: output rows
   int64_t ld_y;
   int relu;
+  int x_vec_ok;        // x and ld_x 16-B aligned (cp.async staging allowed)
 };
 
 template <int LOG_R_, int LOG_T_>
@@ -57,11 +58,29 @@ struct VCfg {
   static constexpr int GPC = THREADS / T;                     // groups (vectors) per CTA
   static constexpr int WORDS = R >= 32 ? R / 32 : 1;          // sign words per thread
   static constexpr int BITS = R >= 32 ? 32 : R;               // valid bits per word
-  static constexpr int XMASK = (N / 4 >= 8 ? 8 : (N / 4 > 0 ? N / 4 : 1)) - 1;
-  static constexpr int SMEM_FLOATS = GPC * N + (T > 32 ? 4 * (T / 32) : 0);
-  static constexpr size_t SMEM_BYTES = sizeof(float) * (size_t)SMEM_FLOATS;
+  // swizzle only the 16-B chunk bits inside one thread's layout-A run (bits 2..LOG_R-1)
+  static constexpr int XMASK = (R / 4 >= 8 ? 8 : (R / 4 > 0 ? R / 4 : 1)) - 1;
   static constexpr bool MULTI_WARP = T > 32;
+  // register budget: resident warps/SM we ask ptxas to allow (R data registers + ~50)
+  static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 24 : (R == 64 ? 12 : 8));
+  static constexpr int MIN_CTAS = TARGET_WARPS / (THREADS / 32) > 0 ? TARGET_WARPS / (THREADS / 32) : 1;
+  // per group: transpose buffer (+ an x staging buffer for the embed ops, which reuse
+  // x across blocks and prefetch the next row with cp.async)
+  __host__ __device__ static constexpr bool xbuf(int op) { return op == 2 || op == 3; }
+  __host__ __device__ static constexpr int smem_floats(int op) {
+    return GPC * N * (xbuf(op) ? 2 : 1) + (T > 32 ? 4 * (T / 32) : 0);
+  }
+  __host__ __device__ static constexpr size_t smem_bytes(int op) { return sizeof(float) * (size_t)smem_floats(op); }
 };
+
+// 16-B global->shared async copy, zero-filling beyond src_bytes (cp.async, LDGSTS).
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // ---------------------------------------------------------------- primitives
 
@@ -288,6 +307,39 @@ __device__ __forceinline__ void thread_argmax(const float (&r)[C::R], int first_
   vbest = vb;
 }
 
+// sin/cos for the random-feature epilogue (kernels.cpp:29-34): Cody-Waite reduction by
+// 2*pi (two-constant split, FFMA) to |r| <= pi, then the SFU (MUFU.SIN/COS, max abs
+// error 2^-21.4 on [-pi, pi]).  Runs on the XU pipe, off the FP32 pipe that the
+// butterflies saturate; abs error ~4e-7 against features of rms 0.7.
+//
+// The argument arrives in revolutions (u = t / 2pi, the 1/2pi folded into the host-side
+// multiplier): f = u - rint(u) is exact, a = 2pi f in [-pi, pi].
+__device__ __forceinline__ void sincos_rev(float u, float& s, float& c) {
+  const float f = u - rintf(u);
+  const float a = f * 6.28318530717958648f;
+  s = __sinf(a);
+  c = __cosf(a);
+}
+
+// Embed epilogue in layout B (element i = j*T + t): coalesced 4-B streaming stores.
+template <class C, int OP, bool CHECK>
+__device__ __forceinline__ void embed_store(const float (&r)[C::R], float* __restrict__ yrow,
+                                            const VecParams& p, int t, int rows) {
+#pragma unroll
+  for (int j = 0; j < C::R; ++j) {
+    const int i = j * C::T + t;
+    if (CHECK && i >= rows) continue;
+    if constexpr (OP == OP_EMBED_GAUSS) {
+      float s, co;
+      sincos_rev(r[j] * p.c2, s, co);
+      __stcs(yrow + i, co * p.norm);
+      __stcs(yrow + p.k + i, s * p.norm);
+    } else {  // OP_EMBED_ANG: sign with sign(0) = +1 (kernels.cpp:23-26)
+      __stcs(yrow + i, (r[j] * p.c < 0.0f) ? -1.0f : 1.0f);
+    }
+  }
+}
+
 // Running signed-argmax state (lsh.cpp:9-21): max |y|, ties to the smallest row.
 struct ArgBest {
   float a;    // |y| (unscaled)
@@ -342,27 +394,51 @@ __device__ __forceinline__ ArgBest group_argmax(ArgBest b, float* red) {
   return b;
 }
 
+// Issue the cp.async copies of one row (n_in valid floats, zero fill to N) into the
+// swizzled staging buffer; 16-B chunk c = t + T*u, coalesced across the group.
+template <class C>
+__device__ __forceinline__ void stage_x(float* xb, const float* __restrict__ xrow, int64_t n_in, int t) {
+#pragma unroll
+  for (int u = 0; u < C::R / 4; ++u) {
+    const int c = t + C::T * u;
+    const int64_t rem = n_in - 4 * (int64_t)c;
+    const int bytes = rem >= 4 ? 16 : (rem > 0 ? (int)rem * 4 : 0);
+    cp_async16(xb + sw<C>(4 * c), bytes > 0 ? xrow + 4 * c : xrow, bytes);
+  }
+}
+
 // ------------------------------------------------------------------- kernel
 
-template <int LOG_R, int LOG_T, int OP>
-__global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS)
+template <int LOG_R, int LOG_T, int OP, bool SIGNS>
+__global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T>::MIN_CTAS)
     spinner_vec_kernel(const VecParams p) {
   using C = VCfg<LOG_R, LOG_T>;
   extern __shared__ __align__(16) float smem[];
   constexpr bool END_B = OP != OP_HASH;  // epilogue needs coalesced layout B
-  constexpr bool KEEP_X = (OP == OP_EMBED_GAUSS || OP == OP_EMBED_ANG) && C::R <= 32;
+  // embed ops reuse x for every block: stage it in smem with cp.async (16-B chunks,
+  // zero-filled past n_in, swizzled like the transpose buffer) and prefetch the next
+  // row during the last block.  Needs 16-B aligned rows (p.x_vec_ok).
+  constexpr bool STAGE_X = C::xbuf(OP) && C::R >= 4;
 
   const int t = threadIdx.x & (C::T - 1);
   const int g = threadIdx.x >> LOG_T;
-  float* sm = smem + g * C::N;
-  float* red = smem + C::GPC * C::N;
+  float* sm = smem + g * C::N * (C::xbuf(OP) ? 2 : 1);
+  float* xb = sm + C::N;
+  float* red = smem + C::smem_floats(OP) - (C::T > 32 ? 4 * (C::T / 32) : 0);
 
   const int64_t per_vec = (OP == OP_HASH) ? p.tables : 1;
   const int64_t total = p.batch * per_vec;
+  const int64_t stride = (int64_t)gridDim.x * C::GPC;
   const bool want_ids = (OP == OP_HASH) || (OP == OP_APPLY && p.ids != nullptr);
+  const bool staged = STAGE_X && p.x_vec_ok;
 
-  for (int64_t base = (int64_t)blockIdx.x * C::GPC; base < total;
-       base += (int64_t)gridDim.x * C::GPC) {
+  if constexpr (STAGE_X) {
+    const int64_t item0 = (int64_t)blockIdx.x * C::GPC + g;
+    if (staged && item0 < total) stage_x<C>(xb, p.x + item0 * p.ld_x, p.n_in, t);
+    cp_async_commit();
+  }
+
+  for (int64_t base = (int64_t)blockIdx.x * C::GPC; base < total; base += stride) {
     const int64_t item = base + g;
     const bool active = item < total;
     const int64_t v = active ? item / per_vec : 0;
@@ -370,38 +446,46 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS)
     const float* xrow = p.x + v * p.ld_x;
 
     float r[C::R];
-    float xk[KEEP_X ? C::R : 1];
-    load_x_B<C>(r, xrow, p.n_in, t);
-    if constexpr (END_B) {
-      if constexpr (C::T > 1) xpose_B_to_A<C>(r, sm, t);
-    }
-    if constexpr (KEEP_X) {
-#pragma unroll
-      for (int j = 0; j < C::R; ++j) xk[j] = r[j];
+    if constexpr (STAGE_X) {
+      cp_async_wait_all();
+      group_sync<C>();
     }
 
     ArgBest best{-1.0f, 0x7fffffff, 0.0f};
     for (int b = 0; b < p.blocks; ++b) {
-      if (b > 0) {
-        if constexpr (KEEP_X) {
+      if (STAGE_X && staged) {
+        if constexpr (STAGE_X) {
+          const Swz<C> z(t);
 #pragma unroll
-          for (int j = 0; j < C::R; ++j) r[j] = xk[j];
-        } else {
-          load_x_B<C>(r, xrow, p.n_in, t);
-          if constexpr (END_B) {
-            if constexpr (C::T > 1) xpose_B_to_A<C>(r, sm, t);
+          for (int q = 0; q < C::R / 4; ++q) {
+            const float4 xv = *reinterpret_cast<const float4*>(xb + z.A(t, q));
+            r[4 * q] = xv.x;
+            r[4 * q + 1] = xv.y;
+            r[4 * q + 2] = xv.z;
+            r[4 * q + 3] = xv.w;
           }
+          if (b == p.blocks - 1) {  // x consumed: prefetch the next row into xb
+            group_sync<C>();
+            const int64_t nxt = item + stride;
+            if (nxt < total) stage_x<C>(xb, p.x + nxt * p.ld_x, p.n_in, t);
+            cp_async_commit();
+          }
+        }
+      } else {
+        load_x_B<C>(r, xrow, p.n_in, t);
+        if constexpr (END_B) {
+          if constexpr (C::T > 1) xpose_B_to_A<C>(r, sm, t);
         }
       }
       const int64_t tb = tab * p.blocks + b;
       const int64_t row0 = (int64_t)b * p.m;
       const int64_t rows = min(p.m, p.k - row0);  // valid rows of this block (stacking, spinner.cpp:272-283)
       if constexpr (!END_B) {
-        apply_diag<C>(r, p.d[0][LAY_B], p.dsign[0], tb, t);
+        apply_diag<C>(r, p.d[0][LAY_B], SIGNS || p.dsign[0], tb, t);
         fwht_B_to_A<C>(r, sm, t);
-        apply_diag<C>(r, p.d[1][LAY_A], p.dsign[1], tb, t);
+        apply_diag<C>(r, p.d[1][LAY_A], SIGNS || p.dsign[1], tb, t);
         fwht_A_to_B<C>(r, sm, t);
-        apply_diag<C>(r, p.d[2][LAY_B], p.dsign[2], tb, t);
+        apply_diag<C>(r, p.d[2][LAY_B], SIGNS || p.dsign[2], tb, t);
         fwht_B_to_A<C>(r, sm, t);
         // layout A: element i = t*R + j, increasing j
         float am, vb;
@@ -409,11 +493,11 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS)
         thread_argmax<C>(r, t * C::R, 1, (int)rows, am, jb, vb);
         if (jb >= 0) argbest_merge(best, am, (int)row0 + t * C::R + jb, vb);
       } else {
-        apply_diag<C>(r, p.d[0][LAY_A], p.dsign[0], tb, t);
+        apply_diag<C>(r, p.d[0][LAY_A], SIGNS || p.dsign[0], tb, t);
         fwht_A_to_B<C>(r, sm, t);
-        apply_diag<C>(r, p.d[1][LAY_B], p.dsign[1], tb, t);
+        apply_diag<C>(r, p.d[1][LAY_B], SIGNS || p.dsign[1], tb, t);
         fwht_B_to_A<C>(r, sm, t);
-        apply_diag<C>(r, p.d[2][LAY_A], p.dsign[2], tb, t);
+        apply_diag<C>(r, p.d[2][LAY_A], SIGNS || p.dsign[2], tb, t);
         fwht_A_to_B<C>(r, sm, t);
         // layout B: element i = j*T + t -> coalesced stores
         float* yrow = p.y + v * p.ld_y + row0;
@@ -436,19 +520,11 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS)
           }
           continue;
         }
-#pragma unroll
-        for (int j = 0; j < C::R; ++j) {
-          const int i = j * C::T + t;
-          if (!active || i >= rows) continue;
-          if constexpr (OP == OP_EMBED_GAUSS) {
-            float s, co;
-            sincosf(r[j] * p.c2, &s, &co);
-            __stcs(yrow + i, co * p.norm);
-            __stcs(yrow + p.k + i, s * p.norm);
-          } else {  // OP_EMBED_ANG
-            __stcs(yrow + i, (r[j] * p.c < 0.0f) ? -1.0f : 1.0f);
-          }
-        }
+        if (!active) continue;
+        if (rows >= C::N)
+          embed_store<C, OP, false>(r, yrow, p, t, (int)rows);
+        else
+          embed_store<C, OP, true>(r, yrow, p, t, (int)rows);
       }
     }
 

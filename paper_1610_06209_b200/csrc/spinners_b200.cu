@@ -180,12 +180,12 @@ spn_status validate_shape(int64_t n, int64_t m, int64_t k, int64_t tables) {
 
 // ------------------------------------------------------------ vector-kernel dispatch
 
-spn::LaunchFn vec_launcher(int log_n, int op) {
+spn::LaunchFn vec_launcher(int log_n, int op, int signs) {
   switch (op) {
-    case spn::OP_HASH: return spn::vec_launcher_hash(log_n);
-    case spn::OP_APPLY: return spn::vec_launcher_apply(log_n);
-    case spn::OP_EMBED_GAUSS: return spn::vec_launcher_gauss(log_n);
-    default: return spn::vec_launcher_ang(log_n);
+    case spn::OP_HASH: return spn::vec_launcher_hash(log_n, signs);
+    case spn::OP_APPLY: return spn::vec_launcher_apply(log_n, signs);
+    case spn::OP_EMBED_GAUSS: return spn::vec_launcher_gauss(log_n, signs);
+    default: return spn::vec_launcher_ang(log_n, signs);
   }
 }
 
@@ -217,7 +217,8 @@ spn_status run_vec(const spn_plan* p, int op, spn::VecParams& v, cudaStream_t s)
   const int64_t items = v.batch * (op == spn::OP_HASH ? p->tables : 1);
   if (items == 0) return SPN_OK;
   DeviceGuard g(p->device);
-  cudaError_t e = vec_launcher(p->log_n, op)(v, s, p->sms, items);
+  const int signs = p->dsign[0] && p->dsign[1] && p->dsign[2];
+  cudaError_t e = vec_launcher(p->log_n, op, signs)(v, s, p->sms, items);
   if (e != cudaSuccess) return cuda_fail(e, "spinner_vec_kernel launch");
   return SPN_OK;
 }
@@ -418,8 +419,9 @@ spn_status spn_embed_f32(const spn_plan* p, int32_t kind, double sigma, const fl
   v.batch = batch;
   v.y = out;
   v.ld_y = ld_out;
-  v.c2 = static_cast<float>(p->scale * std::pow(static_cast<double>(p->n), -1.5) / sigma);
+  v.c2 = static_cast<float>(p->scale * std::pow(static_cast<double>(p->n), -1.5) / (sigma * 2.0 * M_PI));
   v.norm = static_cast<float>(1.0 / std::sqrt(static_cast<double>(p->k)));
+  v.x_vec_ok = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (ld_x % 4 == 0);
   return run_vec(p, kind == SPN_EMBED_GAUSSIAN ? spn::OP_EMBED_GAUSS : spn::OP_EMBED_ANG, v,
                  static_cast<cudaStream_t>(stream));
 }

@@ -1,6 +1,6 @@
-// Launch helpers for spinner_vec_kernel.  Each OP's 14 size instantiations
-// (n = 2^1 .. 2^14) live in their own translation unit (vec_op<OP>.cu) so the
-// build compiles them in parallel.
+// Launch helpers for spinner_vec_kernel.  Each (OP, all-sign-diagonals) pair's 14 size
+// instantiations (n = 2^1 .. 2^14) live in their own translation unit
+// (vec_op_<op>_<s|g>.cu) so the build compiles them in parallel.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -18,36 +18,37 @@ constexpr int kMaxLogNVec = 14;  // fused single-kernel path: n <= 2^14
 
 using LaunchFn = cudaError_t (*)(const VecParams&, cudaStream_t, int, int64_t);
 
-LaunchFn vec_launcher_hash(int log_n);
-LaunchFn vec_launcher_apply(int log_n);
-LaunchFn vec_launcher_gauss(int log_n);
-LaunchFn vec_launcher_ang(int log_n);
+// signs = 1: every diagonal is ±1 (bit-packed XOR path only, smaller kernel)
+LaunchFn vec_launcher_hash(int log_n, int signs);
+LaunchFn vec_launcher_apply(int log_n, int signs);
+LaunchFn vec_launcher_gauss(int log_n, int signs);
+LaunchFn vec_launcher_ang(int log_n, int signs);
 
 // Persistent grid: min(work, SMs x resident CTAs per SM).
-template <int LOG_N, int OP>
+template <int LOG_N, int OP, bool SIGNS>
 cudaError_t launch_vec(const VecParams& p, cudaStream_t s, int sms, int64_t items) {
   using C = VCfg<(LOG_N + 1) / 2, LOG_N / 2>;
-  auto kern = spinner_vec_kernel<C::LOG_R, C::LOG_T, OP>;
+  auto kern = spinner_vec_kernel<C::LOG_R, C::LOG_T, OP, SIGNS>;
   static std::atomic<int> occ_cache{0};
   int occ = occ_cache.load();
   if (occ == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(C::SMEM_BYTES));
+                                         static_cast<int>(C::smem_bytes(OP)));
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM_BYTES);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::smem_bytes(OP));
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     occ_cache.store(occ);
   }
   const int64_t ctas = (items + C::GPC - 1) / C::GPC;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ctas, int64_t(sms) * occ));
-  kern<<<static_cast<unsigned>(grid), C::THREADS, C::SMEM_BYTES, s>>>(p);
+  kern<<<static_cast<unsigned>(grid), C::THREADS, C::smem_bytes(OP), s>>>(p);
   return cudaGetLastError();
 }
 
-template <int OP, int... L>
+template <int OP, bool SIGNS, int... L>
 std::array<LaunchFn, sizeof...(L)> make_vec_table(std::integer_sequence<int, L...>) {
-  return {{&launch_vec<L + 1, OP>...}};
+  return {{&launch_vec<L + 1, OP, SIGNS>...}};
 }
 
 }  // namespace spn
