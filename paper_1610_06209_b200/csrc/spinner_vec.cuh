@@ -62,7 +62,10 @@ struct VCfg {
   static constexpr int XMASK = (R / 4 >= 8 ? 8 : (R / 4 > 0 ? R / 4 : 1)) - 1;
   static constexpr bool MULTI_WARP = T > 32;
   // register budget: resident warps/SM we ask ptxas to allow (R data registers + ~50)
-  static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 24 : (R == 64 ? 12 : 8));
+  static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 24 : (R == 64 ? 12 : 12));
+  // looped six-half-transform chain (smaller SASS) — measured slower on B200 for
+  // n = 1024 and n = 16384 (r4: 0.498 vs 0.475 ms, 339 vs 328 ms), so kept off.
+  static constexpr bool LOOPED = false;
   static constexpr int MIN_CTAS = TARGET_WARPS / (THREADS / 32) > 0 ? TARGET_WARPS / (THREADS / 32) : 1;
   // per group: transpose buffer (+ an x staging buffer for the embed ops, which reuse
   // x across blocks and prefetch the next row with cp.async)
@@ -258,6 +261,83 @@ __device__ __forceinline__ void apply_diag(float (&r)[C::R], const DiagArrays& d
 #pragma unroll
       for (int j = 0; j < C::R; ++j) r[j] *= __ldg(f + j * C::T + t);
     }
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void xor_signs(float (&r)[C::R], const uint32_t (&w)[C::WORDS]) {
+#pragma unroll
+  for (int q = 0; q < C::WORDS; ++q)
+#pragma unroll
+    for (int jj = 0; jj < C::BITS; ++jj) {
+      const int j = q * 32 + jj;
+      r[j] = __uint_as_float(__float_as_uint(r[j]) ^ ((w[q] << (31 - jj)) & 0x80000000u));
+    }
+}
+
+template <class C>
+__device__ __forceinline__ void load_words(uint32_t (&w)[C::WORDS], const uint32_t* base, int64_t tb, int t) {
+  const uint32_t* s = base + tb * (int64_t)(C::WORDS * C::T);
+#pragma unroll
+  for (int q = 0; q < C::WORDS; ++q) w[q] = __ldg(s + q * C::T + t);
+}
+
+// The three rounds D1 -> H -> D2 -> H -> D3 -> H of one (table, block) on registers r.
+// Start layout B (END_B = false) or A (END_B = true); each H flips the layout.
+//  * sign diagonals: all three bit-masks are fetched up front so their L1/L2 latency
+//    overlaps the first butterflies (they were the top long-scoreboard stall);
+//  * LOG_R == LOG_T (n = 4^k, incl. 1024 and 16384): both halves of every H cover
+//    all register bits, so the six half-transforms run as a loop over ONE copy of
+//    the butterfly code with a runtime transpose direction — a third of the SASS of
+//    the unrolled chain, which keeps the n = 16384 kernel inside the instruction cache.
+template <class C, bool END_B, bool SIGNS>
+__device__ __forceinline__ void spinner_chain(float (&r)[C::R], float* sm, const VecParams& p, int64_t tb,
+                                              int t) {
+  constexpr int L0 = END_B ? LAY_A : LAY_B, L1 = END_B ? LAY_B : LAY_A;
+  if constexpr (SIGNS && C::LOOPED) {
+    uint32_t w0[C::WORDS], w1[C::WORDS], w2[C::WORDS];
+    load_words<C>(w0, p.d[0][L0].sgn, tb, t);
+    load_words<C>(w1, p.d[1][L1].sgn, tb, t);
+    load_words<C>(w2, p.d[2][L0].sgn, tb, t);
+    bool a_to_b = END_B;  // direction of the next transpose
+#pragma unroll 1
+    for (int part = 0; part < 6; ++part) {
+      const bool even = (part & 1) == 0;
+      if (even) {
+        xor_signs<C>(r, w0);
+#pragma unroll
+        for (int q = 0; q < C::WORDS; ++q) {
+          w0[q] = w1[q];
+          w1[q] = w2[q];
+        }
+      }
+      reg_fwht<C::R, 0, C::LOG_R>(r);
+      if (even) {
+        if (a_to_b)
+          xpose_A_to_B<C>(r, sm, t);
+        else
+          xpose_B_to_A<C>(r, sm, t);
+        a_to_b = !a_to_b;
+      }
+    }
+  } else if constexpr (SIGNS) {
+    uint32_t w0[C::WORDS], w1[C::WORDS], w2[C::WORDS];
+    load_words<C>(w0, p.d[0][L0].sgn, tb, t);
+    load_words<C>(w1, p.d[1][L1].sgn, tb, t);
+    load_words<C>(w2, p.d[2][L0].sgn, tb, t);
+    xor_signs<C>(r, w0);
+    if constexpr (END_B) fwht_A_to_B<C>(r, sm, t); else fwht_B_to_A<C>(r, sm, t);
+    xor_signs<C>(r, w1);
+    if constexpr (END_B) fwht_B_to_A<C>(r, sm, t); else fwht_A_to_B<C>(r, sm, t);
+    xor_signs<C>(r, w2);
+    if constexpr (END_B) fwht_A_to_B<C>(r, sm, t); else fwht_B_to_A<C>(r, sm, t);
+  } else {
+    apply_diag<C>(r, p.d[0][L0], p.dsign[0], tb, t);
+    if constexpr (END_B) fwht_A_to_B<C>(r, sm, t); else fwht_B_to_A<C>(r, sm, t);
+    apply_diag<C>(r, p.d[1][L1], p.dsign[1], tb, t);
+    if constexpr (END_B) fwht_B_to_A<C>(r, sm, t); else fwht_A_to_B<C>(r, sm, t);
+    apply_diag<C>(r, p.d[2][L0], p.dsign[2], tb, t);
+    if constexpr (END_B) fwht_A_to_B<C>(r, sm, t); else fwht_B_to_A<C>(r, sm, t);
   }
 }
 
@@ -480,25 +560,14 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
       const int64_t tb = tab * p.blocks + b;
       const int64_t row0 = (int64_t)b * p.m;
       const int64_t rows = min(p.m, p.k - row0);  // valid rows of this block (stacking, spinner.cpp:272-283)
+      spinner_chain<C, END_B, SIGNS>(r, sm, p, tb, t);
       if constexpr (!END_B) {
-        apply_diag<C>(r, p.d[0][LAY_B], SIGNS || p.dsign[0], tb, t);
-        fwht_B_to_A<C>(r, sm, t);
-        apply_diag<C>(r, p.d[1][LAY_A], SIGNS || p.dsign[1], tb, t);
-        fwht_A_to_B<C>(r, sm, t);
-        apply_diag<C>(r, p.d[2][LAY_B], SIGNS || p.dsign[2], tb, t);
-        fwht_B_to_A<C>(r, sm, t);
         // layout A: element i = t*R + j, increasing j
         float am, vb;
         int jb;
         thread_argmax<C>(r, t * C::R, 1, (int)rows, am, jb, vb);
         if (jb >= 0) argbest_merge(best, am, (int)row0 + t * C::R + jb, vb);
       } else {
-        apply_diag<C>(r, p.d[0][LAY_A], SIGNS || p.dsign[0], tb, t);
-        fwht_A_to_B<C>(r, sm, t);
-        apply_diag<C>(r, p.d[1][LAY_B], SIGNS || p.dsign[1], tb, t);
-        fwht_B_to_A<C>(r, sm, t);
-        apply_diag<C>(r, p.d[2][LAY_A], SIGNS || p.dsign[2], tb, t);
-        fwht_A_to_B<C>(r, sm, t);
         // layout B: element i = j*T + t -> coalesced stores
         float* yrow = p.y + v * p.ld_y + row0;
         if constexpr (OP == OP_APPLY) {
