@@ -238,13 +238,12 @@ def run_ours(args, rank, world, local):
     total_ms = sum(step_ms)
     ids = None
     if args.config == "c3" and world > 1:  # the real exchange step: all-gather the codes over NCCL
-        import torch.distributed as dist
+        from paper_1610_06209_b200.shard import gather_codes
         ids = w.step(stream)
-        gathered = torch.empty((world * ids.shape[0], ids.shape[1]), dtype=ids.dtype, device="cuda")
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        dist.all_gather_into_tensor(gathered, ids)
+        gather_codes(ids, world)
         t1.record(stream)
         torch.cuda.synchronize()
         total_ms += t0.elapsed_time(t1) * args.steps
