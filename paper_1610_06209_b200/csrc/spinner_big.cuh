@@ -36,17 +36,20 @@ namespace spn {
 // Thread (warp w, lane) holds column col0+lane and R = 2^LR rows:
 //   layout A: s = w*R + j      layout B: s = j*W + w
 // Loads/stores are 128-B coalesced in both layouts (lanes = columns); the
-// transpose goes through smem[s][32] (bank = lane: conflict free).
+// transpose goes through smem[s][32] (bank = lane: conflict free).  The pass
+// program (number of H parts, where the diagonals go, start layout, epilogue) is
+// a template so every address and layout decision folds at compile time; element
+// addresses are tile-uniform 64-bit bases + one 32-bit IMAD per element.
 
 template <int LS_>
 struct ColCfg {
   static constexpr int LS = LS_;
-  // <= 16 warps per CTA (<= 128 regs/thread at 512 threads): 32 rows per thread up to
-  // LS = 9, 64 rows per thread at LS = 10.
-  static constexpr int LR = LS <= 5 ? LS : (LS - 4 > 5 ? LS - 4 : 5);
-  static constexpr int LW = LS - LR;
+  static constexpr int LR = LS < 5 ? LS : 5;  // 32 rows per thread
+  static constexpr int LW = LS - LR;          // <= 32 warps
   static constexpr int R = 1 << LR, W = 1 << LW, S = 1 << LS;
   static constexpr int THREADS = 32 * W;
+  // 1024 resident threads/SM -> <= 64 regs; single-warp tiles get 128 regs (16 CTAs)
+  static constexpr int MIN_CTAS = W == 1 ? 16 : (1024 / THREADS > 0 ? 1024 / THREADS : 1);
   static constexpr size_t SMEM = W > 1 ? sizeof(float) * S * 32 : 16;
 };
 
@@ -60,16 +63,29 @@ struct ColParams {
   int64_t ncols, nstripes;
   int s0;                // bit position of the transformed sub-index inside e
   int64_t nhi, nlo, nvec;
-  int nparts;            // number of H parts (1..3)
-  const float* dd[3];    // D applied before part p (nullable)
-  int dmode;             // DM_PER_ROW: dd[p][(lo*nhi + hi)*S + s]; DM_PER_ELEM: dd[p][e*d_ld + col]
-  int64_t d_ld;
-  int start_b;           // start in layout B
-  const int32_t* rowmap; // gather epilogue: out row of e, or -1
+  const float* dd[3];    // D applied before part p (DMASK bit p)
+  int64_t d_ld;          // DM_PER_ELEM: dd[p][e*d_ld + col];  DM_PER_ROW: dd[p][(lo*nhi + hi)*S + s]
+  const int32_t* rowmap; // GATHER: output row of e, or -1
   int64_t ld_out;
   float cscale;
-  int scale_out, relu;
+  int64_t rows_valid;    // EPI_Y: flat elements < rows_valid are stored
+  int relu;
+  // filled by set_tiling(): fast division by nstripes, log2 of nlo / nhi (powers of two)
+  uint32_t fd_m, fd_l;
+  int lg_nlo, lg_nhi;
 };
+
+// Host: magic numbers for fdiv() and the pow2 logs used by the staged kernels' tile decode.
+inline void set_tiling(ColParams& p) {
+  const uint32_t d = static_cast<uint32_t>(p.nstripes);
+  uint32_t l = 0;
+  while ((uint64_t(1) << l) < d) ++l;
+  p.fd_l = l;
+  p.fd_m = d <= 1 ? 0u : static_cast<uint32_t>(((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1);
+  auto lg = [](int64_t x) { int k = 0; while ((int64_t(1) << k) < x) ++k; return k; };
+  p.lg_nlo = lg(p.nlo);
+  p.lg_nhi = lg(p.nhi);
+}
 
 template <int LS>
 __device__ __forceinline__ void col_xpose(float (&r)[ColCfg<LS>::R], float* sm, int w, int lane,
@@ -89,8 +105,14 @@ __device__ __forceinline__ void col_xpose(float (&r)[ColCfg<LS>::R], float* sm, 
   __syncthreads();
 }
 
-template <int LS>
-__global__ void __launch_bounds__(ColCfg<LS>::THREADS) colpass_kernel(const ColParams p) {
+// s held in register j for a layout (compile-time after unrolling).
+template <class C>
+__device__ __forceinline__ uint32_t col_s(bool lay_b, int w, int j) {
+  return lay_b ? (uint32_t)(j * C::W + w) : (uint32_t)(w * C::R + j);
+}
+
+template <int LS, int NPARTS, int DMASK, bool START_B, int DMODE, bool GATHER>
+__global__ void __launch_bounds__(ColCfg<LS>::THREADS, ColCfg<LS>::MIN_CTAS) colpass_kernel(const ColParams p) {
   using C = ColCfg<LS>;
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -103,37 +125,43 @@ __global__ void __launch_bounds__(ColCfg<LS>::THREADS) colpass_kernel(const ColP
     tmp /= p.nlo;
     const int64_t hi = tmp % p.nhi;
     const int64_t v = tmp / p.nhi;
-    const int64_t col = cs * 32 + lane;
-    const bool colok = col < p.ncols;
-    // Tile-uniform bases + 32-bit per-element offsets: element s of this tile sits at
-    // e = e0 + (s << s0), i.e. base + s * (2^s0 * ld) + lane.
+    const bool colok = cs * 32 + lane < p.ncols;
     const int64_t e0 = (hi << (p.s0 + LS)) + lo;
-    const float* sb = p.src + v * p.src_vstride + e0 * p.src_ld + cs * 32;
-    const uint32_t s_step = (uint32_t)(p.src_ld << p.s0);
-    const int64_t s_lim = p.src_valid - (e0 * p.src_ld + cs * 32);
-    bool lay_b = p.start_b;
-    auto s_of = [&](int j) -> uint32_t { return lay_b ? (uint32_t)(j * C::W + w) : (uint32_t)(w * C::R + j); };
 
     float r[C::R];
-    if (colok && s_lim >= (int64_t)C::S * s_step) {  // whole tile in range (uniform except last stripe)
+    {
+      const float* sb = p.src + v * p.src_vstride + e0 * p.src_ld + cs * 32;
+      const uint32_t step = (uint32_t)(p.src_ld << p.s0);
+      const int64_t lim = p.src_valid - (e0 * p.src_ld + cs * 32);
+      constexpr bool LB = START_B && C::W > 1;
+      if (colok && lim >= (int64_t)C::S * step) {
 #pragma unroll
-      for (int j = 0; j < C::R; ++j) r[j] = __ldg(sb + (s_of(j) * s_step + lane));
-    } else {
+        for (int j = 0; j < C::R; ++j) r[j] = __ldg(sb + (col_s<C>(LB, w, j) * step + lane));
+      } else {
 #pragma unroll
-      for (int j = 0; j < C::R; ++j) {
-        const uint32_t off = s_of(j) * s_step + lane;
-        r[j] = (colok && (int64_t)off < s_lim) ? __ldg(sb + off) : 0.0f;
+        for (int j = 0; j < C::R; ++j) {
+          const uint32_t off = col_s<C>(LB, w, j) * step + lane;
+          r[j] = (colok && (int64_t)off < lim) ? __ldg(sb + off) : 0.0f;
+        }
       }
     }
-    for (int part = 0; part < p.nparts; ++part) {
-      const float* D = p.dd[part];
-      if (D) {
-        if (p.dmode == DM_PER_ELEM) {
-          const float* dbase = D + e0 * p.d_ld + cs * 32;
-          const uint32_t d_step = (uint32_t)(p.d_ld << p.s0);
 #pragma unroll
-          for (int j = 0; j < C::R; ++j)
-            if (colok) r[j] *= __ldg(dbase + (s_of(j) * d_step + lane));
+    for (int part = 0; part < NPARTS; ++part) {
+      const bool lay_b = C::W > 1 && (START_B ^ ((part & 1) != 0));
+      if ((DMASK >> part) & 1) {
+        const float* D = p.dd[part];
+        if constexpr (DMODE == DM_PER_ELEM) {
+          const float* db = D + e0 * p.d_ld + cs * 32;
+          const uint32_t dstep = (uint32_t)(p.d_ld << p.s0);
+          if (colok) {
+            // 8 loads in flight at a time: all R at once would need R more registers
+#pragma unroll
+            for (int q = 0; q < C::R; q += 8) {
+#pragma unroll
+              for (int j = q; j < q + 8 && j < C::R; ++j) r[j] *= __ldg(db + (col_s<C>(lay_b, w, j) * dstep + lane));
+              asm volatile("" ::: "memory");
+            }
+          }
         } else {
           const float* Dt = D + (lo * p.nhi + hi) * C::S;
           if (!lay_b && C::R >= 4) {
@@ -147,7 +175,7 @@ __global__ void __launch_bounds__(ColCfg<LS>::THREADS) colpass_kernel(const ColP
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < C::R; ++j) r[j] *= __ldg(Dt + s_of(j));
+            for (int j = 0; j < C::R; ++j) r[j] *= __ldg(Dt + col_s<C>(lay_b, w, j));
           }
         }
       }
@@ -159,25 +187,24 @@ __global__ void __launch_bounds__(ColCfg<LS>::THREADS) colpass_kernel(const ColP
           reg_fwht<C::R, C::LR - C::LW, C::LR>(r);
         else
           reg_fwht<C::R, 0, C::LW>(r);
-        lay_b = !lay_b;
       }
     }
-    if (p.rowmap) {
+    constexpr bool END_B = C::W > 1 && (START_B ^ ((NPARTS & 1) != 0));
+    if constexpr (GATHER) {
       const int32_t* rm = p.rowmap + e0;
+      const float* unused = nullptr;
+      (void)unused;
 #pragma unroll
       for (int j = 0; j < C::R; ++j) {
-        const int32_t orow = __ldg(rm + (s_of(j) << p.s0));
-        if (colok && orow >= 0) __stcs(p.dst + (int64_t)orow * p.ld_out + col, r[j] * p.cscale);
+        const int32_t orow = __ldg(rm + ((int64_t)col_s<C>(END_B, w, j) << p.s0));
+        if (colok && orow >= 0) __stcs(p.dst + (int64_t)orow * p.ld_out + cs * 32 + lane, r[j] * p.cscale);
       }
     } else {
       float* db = p.dst + v * p.dst_vstride + e0 * p.dst_ld + cs * 32;
-      const uint32_t o_step = (uint32_t)(p.dst_ld << p.s0);
+      const uint32_t ostep = (uint32_t)(p.dst_ld << p.s0);
+      if (colok) {
 #pragma unroll
-      for (int j = 0; j < C::R; ++j) {
-        float o = r[j];
-        if (p.scale_out) o *= p.cscale;
-        if (p.relu) o = fmaxf(o, 0.0f);
-        if (colok) db[s_of(j) * o_step + lane] = o;
+        for (int j = 0; j < C::R; ++j) db[col_s<C>(END_B, w, j) * ostep + lane] = r[j];
       }
     }
   }
@@ -189,14 +216,14 @@ struct RowParams {
   float* buf;            // [nvec][vstride] in place (mid pass) / source (last pass)
   int64_t vstride, nseg, nvec;
   const float* d_mid;    // mid pass: D2 per segment in layout-A float format ([seg][8][32][4])
-  int last;              // last pass: store y
   float* y;
   int64_t ld_y, rows_valid;
   float c;
   int relu;
 };
 
-__global__ void __launch_bounds__(256) rowpass_kernel(const RowParams p) {
+template <bool LAST>
+__global__ void __launch_bounds__(256, 3) rowpass_kernel(const RowParams p) {
   using C = VCfg<5, 5>;
   __shared__ __align__(16) float smem[8 * 1024];
   const int t = threadIdx.x & 31, g = threadIdx.x >> 5;
@@ -211,7 +238,7 @@ __global__ void __launch_bounds__(256) rowpass_kernel(const RowParams p) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) r[j] = row[j * 32 + t];
     fwht_B_to_A<C>(r, sm, t);
-    if (!p.last) {
+    if constexpr (!LAST) {
       const float4* f = reinterpret_cast<const float4*>(p.d_mid + seg * 1024);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -226,13 +253,13 @@ __global__ void __launch_bounds__(256) rowpass_kernel(const RowParams p) {
       for (int j = 0; j < 32; ++j) row[j * 32 + t] = r[j];
     } else {
       xpose_A_to_B<C>(r, sm, t);
-      float* yrow = p.y + v * p.ld_y;
+      float* yrow = p.y + v * p.ld_y + seg * 1024;
+      const bool all = seg * 1024 + 1024 <= p.rows_valid;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const int64_t e = seg * 1024 + j * 32 + t;
         float o = r[j] * p.c;
         if (p.relu) o = fmaxf(o, 0.0f);
-        if (e < p.rows_valid) __stcs(yrow + e, o);
+        if (all || seg * 1024 + j * 32 + t < p.rows_valid) __stcs(yrow + j * 32 + t, o);
       }
     }
   }
@@ -240,52 +267,80 @@ __global__ void __launch_bounds__(256) rowpass_kernel(const RowParams p) {
 
 // ------------------------------------------------------------------- host side
 
-template <int LS>
+template <int LS, int NPARTS, int DMASK, bool START_B, int DMODE, bool GATHER>
 inline cudaError_t launch_col(const ColParams& p, int sms, cudaStream_t s) {
   using C = ColCfg<LS>;
+  auto kern = colpass_kernel<LS, NPARTS, DMASK, START_B, DMODE, GATHER>;
   static int occ = 0;
   if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(colpass_kernel<LS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(C::SMEM));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, colpass_kernel<LS>, C::THREADS, C::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM);
     if (e != cudaSuccess) return e;
     occ = std::max(occ, 1);
   }
   const int64_t tiles = p.nvec * p.nhi * p.nlo * p.nstripes;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sms) * occ));
-  colpass_kernel<LS><<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, s>>>(p);
+  kern<<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, s>>>(p);
   return cudaGetLastError();
 }
 
-inline cudaError_t launch_col_ls(int ls, const ColParams& p, int sms, cudaStream_t s) {
+// The pass programs used by the drivers below.
+enum ColProg : int {
+  CP_FIRST = 0,   // [D] H            start A          (vector P1 / sketch P1)
+  CP_MID = 1,     // H [D] H          start B          (vector P3 / sketch P2, P3)
+  CP_LAST = 2,    // H, gather rows   start A          (sketch P4)
+  CP_SINGLE = 3,  // [D]H[D]H[D]H, gather             (sketch with n <= 2^10)
+};
+
+template <int LS>
+inline cudaError_t launch_col_prog(int prog, int dmode, const ColParams& p, int sms, cudaStream_t s) {
+  if (dmode == DM_PER_ELEM) {
+    if (prog == CP_FIRST) return launch_col<LS, 1, 1, false, DM_PER_ELEM, false>(p, sms, s);
+    if (prog == CP_MID) return launch_col<LS, 2, 2, true, DM_PER_ELEM, false>(p, sms, s);
+    return cudaErrorInvalidValue;
+  }
+  switch (prog) {
+    case CP_FIRST: return launch_col<LS, 1, 1, false, DM_PER_ROW, false>(p, sms, s);
+    case CP_MID: return launch_col<LS, 2, 2, true, DM_PER_ROW, false>(p, sms, s);
+    case CP_LAST: return launch_col<LS, 1, 0, false, DM_PER_ROW, true>(p, sms, s);
+    default: return launch_col<LS, 3, 7, false, DM_PER_ROW, true>(p, sms, s);
+  }
+}
+
+inline cudaError_t launch_col_ls(int ls, int prog, int dmode, const ColParams& p, int sms, cudaStream_t s) {
   switch (ls) {
-    case 1: return launch_col<1>(p, sms, s);
-    case 2: return launch_col<2>(p, sms, s);
-    case 3: return launch_col<3>(p, sms, s);
-    case 4: return launch_col<4>(p, sms, s);
-    case 5: return launch_col<5>(p, sms, s);
-    case 6: return launch_col<6>(p, sms, s);
-    case 7: return launch_col<7>(p, sms, s);
-    case 8: return launch_col<8>(p, sms, s);
-    case 9: return launch_col<9>(p, sms, s);
-    case 10: return launch_col<10>(p, sms, s);
+    case 1: return launch_col_prog<1>(prog, dmode, p, sms, s);
+    case 2: return launch_col_prog<2>(prog, dmode, p, sms, s);
+    case 3: return launch_col_prog<3>(prog, dmode, p, sms, s);
+    case 4: return launch_col_prog<4>(prog, dmode, p, sms, s);
+    case 5: return launch_col_prog<5>(prog, dmode, p, sms, s);
+    case 6: return launch_col_prog<6>(prog, dmode, p, sms, s);
+    case 7: return launch_col_prog<7>(prog, dmode, p, sms, s);
+    case 8: return launch_col_prog<8>(prog, dmode, p, sms, s);
+    case 9: return launch_col_prog<9>(prog, dmode, p, sms, s);
+    case 10: return launch_col_prog<10>(prog, dmode, p, sms, s);
   }
   return cudaErrorInvalidValue;
 }
 
+template <bool LAST>
 inline cudaError_t launch_row(const RowParams& p, int sms, cudaStream_t s) {
   static int occ = 0;
   if (occ == 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_kernel, 256, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_kernel<LAST>, 256, 0);
     if (e != cudaSuccess) return e;
     occ = std::max(occ, 1);
   }
   const int64_t ctas = (p.nvec * p.nseg + 7) / 8;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ctas, int64_t(sms) * occ));
-  rowpass_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(p);
+  rowpass_kernel<LAST><<<static_cast<unsigned>(grid), 256, 0, s>>>(p);
   return cudaGetLastError();
 }
+
+}  // namespace spn
+#include "spinner_pass.cuh"
+namespace spn {
 
 inline int ilog2_i(int64_t n) {
   int l = 0;
@@ -298,7 +353,10 @@ struct BigPlan {
   int64_t n = 0, tb = 0;
   int L = 0;
   float* dnat[3] = {nullptr, nullptr, nullptr};
-  float* drow2 = nullptr;  // D2 in the row-pass layout
+  float* drow2 = nullptr;   // D2 in the 1024-wide row-pass layout
+  float* srow1 = nullptr;   // staged schedule: D1 / D3 per row segment, D2 per column tile
+  float* srow3 = nullptr;
+  float* stile2 = nullptr;
   // sketch path (lazy)
   std::mutex mu;
   bool sk_ready = false;
@@ -321,6 +379,10 @@ struct BigPlan {
       q = nullptr;
     }
     if (drow2) cudaFree(drow2);
+    for (float** q : {&srow1, &srow3, &stile2}) {
+      if (*q) cudaFree(*q);
+      *q = nullptr;
+    }
     if (work) cudaFree(work);
     if (rowmap) cudaFree(rowmap);
     drow2 = nullptr;
@@ -341,6 +403,49 @@ struct BigPlan {
     return SPN_OK;
   }
 
+  // row-pass width for the staged schedule: C = 2^lc contiguous floats, lc = max(10, L-9)
+  // keeps the column pass at <= 9 bits (double-buffered tiles fit one SM).
+  static int staged_lc(int L) { return L - 9 > 10 ? L - 9 : 10; }
+
+  static spn_status upload_f32(const std::vector<float>& f, float** dst) {
+    cudaError_t e = cudaMalloc(dst, f.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(*dst, f.data(), f.size() * 4, cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? SPN_OK : err(e, "upload diagonals");
+  }
+
+  // D2 permuted per contiguous 2^lc segment into the layout-A float format of VCfg<lc-5, 5>.
+  static std::vector<float> row_perm(const std::vector<double>& d2, int64_t n, int64_t tb, int lc) {
+    const int64_t N = int64_t(1) << lc, R = N / 32;
+    std::vector<float> f(static_cast<size_t>(tb * n));
+    for (int64_t b = 0; b < tb; ++b)
+      for (int64_t seg = 0; seg < n / N; ++seg)
+        for (int64_t t = 0; t < 32; ++t)
+          for (int64_t j = 0; j < R; ++j) {
+            const int64_t pos = ((j / 4) * 32 + t) * 4 + (j % 4);
+            f[static_cast<size_t>(b * n + seg * N + pos)] =
+                static_cast<float>(d2[static_cast<size_t>(b * n + seg * N + t * R + j)]);
+          }
+    return f;
+  }
+
+  // D permuted per column-pass tile for the staged schedule: tile = 32-column stripe cs of
+  // the [2^lr][C] view, [cs][w][R/4][lane][4] with s = w*32 + 4q + k (layout A, R = 32).
+  static std::vector<float> tile_perm(const std::vector<double>& d, int64_t n, int64_t tb, int lc) {
+    const int64_t C = int64_t(1) << lc, S = n / C, R = S < 32 ? S : 32, W = S / R;
+    std::vector<float> f(static_cast<size_t>(tb * n));
+    for (int64_t b = 0; b < tb; ++b)
+      for (int64_t cs = 0; cs < C / 32; ++cs)
+        for (int64_t w = 0; w < W; ++w)
+          for (int64_t q = 0; q < R / 4; ++q)
+            for (int64_t lane = 0; lane < 32; ++lane)
+              for (int64_t k = 0; k < 4; ++k) {
+                const int64_t sidx = w * R + 4 * q + k;
+                const int64_t pos = (((cs * W + w) * (R / 4) + q) * 32 + lane) * 4 + k;
+                f[static_cast<size_t>(b * n + pos)] = static_cast<float>(d[static_cast<size_t>(b * n + sidx * C + cs * 32 + lane)]);
+              }
+    return f;
+  }
+
   spn_status build(int64_t n_, int64_t tb_, const std::vector<double>* d, const int*) {
     n = n_;
     tb = tb_;
@@ -348,22 +453,14 @@ struct BigPlan {
     std::vector<float> f(static_cast<size_t>(tb * n));
     for (int di = 0; di < 3; ++di) {
       for (size_t i = 0; i < f.size(); ++i) f[i] = static_cast<float>(d[di][i]);
-      cudaError_t e = cudaMalloc(&dnat[di], f.size() * 4);
-      if (e == cudaSuccess) e = cudaMemcpy(dnat[di], f.data(), f.size() * 4, cudaMemcpyHostToDevice);
-      if (e != cudaSuccess) return err(e, "upload diagonals");
+      if (spn_status st = upload_f32(f, &dnat[di])) return st;
     }
-    // D2 permuted per 1024-segment into the layout-A float format of VCfg<5,5>
-    for (int64_t b = 0; b < tb; ++b)
-      for (int64_t seg = 0; seg < n / 1024; ++seg)
-        for (int t = 0; t < 32; ++t)
-          for (int j = 0; j < 32; ++j) {
-            const int64_t pos = ((j / 4) * 32 + t) * 4 + (j % 4);
-            f[static_cast<size_t>(b * n + seg * 1024 + pos)] =
-                static_cast<float>(d[1][static_cast<size_t>(b * n + seg * 1024 + t * 32 + j)]);
-          }
-    cudaError_t e = cudaMalloc(&drow2, f.size() * 4);
-    if (e == cudaSuccess) e = cudaMemcpy(drow2, f.data(), f.size() * 4, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return err(e, "upload D2");
+    if (spn_status st = upload_f32(row_perm(d[1], n, tb, 10), &drow2)) return st;
+    // staged (row-first) schedule: D1, D3 in the row passes, D2 in the column pass
+    const int lc = staged_lc(L);
+    if (spn_status st = upload_f32(row_perm(d[0], n, tb, lc), &srow1)) return st;
+    if (spn_status st = upload_f32(row_perm(d[2], n, tb, lc), &srow3)) return st;
+    if (spn_status st = upload_f32(tile_perm(d[1], n, tb, lc), &stile2)) return st;
     return SPN_OK;
   }
 
@@ -372,21 +469,70 @@ struct BigPlan {
                    int relu, int64_t k, int64_t m, int64_t blocks, double c, int sms, cudaStream_t s) {
     if (batch == 0) return SPN_OK;
     std::lock_guard<std::mutex> lock(mu);
-    const int lc = 10, lr = L - lc;
-    const int64_t C = int64_t(1) << lc;
+    auto al16 = [](const void* q, int64_t ld) { return (reinterpret_cast<uintptr_t>(q) % 16 == 0) && (ld % 4 == 0); };
     // vectors per group: working set ~32 MB (L2-resident passes)
     const int64_t G = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t(32) << 20) / (n * 4)));
-    const bool in_place = blocks == 1 && m == n && k == n;
+    const bool in_place = blocks == 1 && m == n && k == n && al16(y, ld_y);
     if (!in_place) {
       spn_status st = ensure_work(static_cast<size_t>(G * n * 4));
       if (st) return st;
     }
+    const bool staged = al16(x, ld_x);
+    const int lc = staged ? staged_lc(L) : 10, lr = L - lc;
+    const int64_t C = int64_t(1) << lc;
     for (int64_t b = 0; b < blocks; ++b) {
       const int64_t rows_valid = std::min(m, k - b * m);
       for (int64_t v0 = 0; v0 < batch; v0 += G) {
         const int64_t nv = std::min(G, batch - v0);
         float* W = in_place ? y + v0 * ld_y : work;
         const int64_t wstride = in_place ? ld_y : n;
+        cudaError_t e;
+        if (staged) {
+          // row-first: P1 row (D1, Hc) | P2 col (Hr, D2, Hr) | P3 row (Hc, D3, Hc) | P4 col (Hr, y)
+          RowParams2 rp{};
+          rp.src = x + v0 * ld_x;
+          rp.src_vstride = ld_x;
+          rp.n_in = n_in;
+          rp.dst = W;
+          rp.dst_vstride = wstride;
+          rp.nseg = n / C;
+          rp.nvec = nv;
+          rp.d = srow1 + b * n;
+          e = launch_srow_lc(lc, RP_FIRST, rp, sms, s);
+          if (e != cudaSuccess) return err(e, "rowpass P1");
+          ColParams cp{};
+          cp.src = W;
+          cp.src_ld = C;
+          cp.src_vstride = wstride;
+          cp.src_valid = n;
+          cp.dst = W;
+          cp.dst_ld = C;
+          cp.dst_vstride = wstride;
+          cp.ncols = C;
+          cp.nstripes = C / 32;
+          cp.s0 = 0;
+          cp.nhi = 1;
+          cp.nlo = 1;
+          cp.nvec = nv;
+          cp.dd[1] = stile2 + b * n;
+          e = launch_scol_ls(lr, SC_VMID, cp, sms, s);
+          if (e != cudaSuccess) return err(e, "colpass P2");
+          rp.src = W;
+          rp.src_vstride = wstride;
+          rp.n_in = n;
+          rp.d = srow3 + b * n;
+          e = launch_srow_lc(lc, RP_MID, rp, sms, s);
+          if (e != cudaSuccess) return err(e, "rowpass P3");
+          cp.dd[1] = nullptr;
+          cp.dst = y + v0 * ld_y + b * m;
+          cp.dst_vstride = ld_y;
+          cp.rows_valid = rows_valid;
+          cp.cscale = static_cast<float>(c);
+          cp.relu = relu;
+          e = launch_scol_ls(lr, SC_VLAST, cp, sms, s);
+          if (e != cudaSuccess) return err(e, "colpass P4");
+          continue;
+        }
         ColParams cp{};
         cp.src = x + v0 * ld_x;
         cp.src_ld = C;
@@ -401,12 +547,9 @@ struct BigPlan {
         cp.nhi = 1;
         cp.nlo = 1;
         cp.nvec = nv;
-        cp.nparts = 1;
         cp.dd[0] = dnat[0] + b * n;
-        cp.dmode = DM_PER_ELEM;
         cp.d_ld = C;
-        cp.start_b = 0;
-        cudaError_t e = launch_col_ls(lr, cp, sms, s);  // P1: D1, Hr
+        e = launch_col_ls(lr, CP_FIRST, DM_PER_ELEM, cp, sms, s);  // P1: D1, Hr
         if (e != cudaSuccess) return err(e, "colpass P1");
         RowParams rp{};
         rp.buf = W;
@@ -414,25 +557,21 @@ struct BigPlan {
         rp.nseg = n / C;
         rp.nvec = nv;
         rp.d_mid = drow2 + b * n;
-        rp.last = 0;
-        e = launch_row(rp, sms, s);  // P2: Hc, D2, Hc
+        e = launch_row<false>(rp, sms, s);  // P2: Hc, D2, Hc
         if (e != cudaSuccess) return err(e, "rowpass P2");
         cp.src = W;
         cp.src_vstride = wstride;
         cp.src_valid = n;
-        cp.nparts = 2;
         cp.dd[0] = nullptr;
         cp.dd[1] = dnat[2] + b * n;
-        cp.start_b = 1;
-        e = launch_col_ls(lr, cp, sms, s);  // P3: Hr, D3, Hr
+        e = launch_col_ls(lr, CP_MID, DM_PER_ELEM, cp, sms, s);  // P3: Hr, D3, Hr
         if (e != cudaSuccess) return err(e, "colpass P3");
-        rp.last = 1;
         rp.y = y + v0 * ld_y + b * m;
         rp.ld_y = ld_y;
         rp.rows_valid = rows_valid;
         rp.c = static_cast<float>(c);
         rp.relu = relu;
-        e = launch_row(rp, sms, s);  // P4: Hc, scale, relu, store
+        e = launch_row<true>(rp, sms, s);  // P4: Hc, scale, relu, store
         if (e != cudaSuccess) return err(e, "rowpass P4");
       }
     }
@@ -496,8 +635,13 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
   if (spn_status st = bp->build_sketch(nn, d)) return st;
   if (spn_status st = bp->set_rowmap(nn, rows, m_out, s)) return st;
   const int lsa = bp->sk_lsa, lsb = bp->sk_lsb;
+  // pipelined (cp.async double-buffered) column passes when both bit ranges fit them
+  const bool staged = (reinterpret_cast<uintptr_t>(a) % 16 == 0) && (ld_a % 4 == 0) && lsa >= 2 && lsa <= 9 &&
+                      (lsb == 0 || (lsb >= 2 && lsb <= 9));
+  auto lcol = [&](int ls, int prog, const ColParams& q) {  // CP_* and SC_FIRST..SC_SINGLE share numbering
+    return staged ? launch_scol_ls(ls, prog, q, sms, s) : launch_col_ls(ls, prog, DM_PER_ROW, q, sms, s);
+  };
   ColParams cp{};
-  cp.dmode = DM_PER_ROW;
   cp.cscale = static_cast<float>(cscale);
   cp.nvec = 1;
   cp.ld_out = ld_out;
@@ -511,13 +655,12 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     cp.s0 = 0;
     cp.nhi = 1;
     cp.nlo = 1;
-    cp.nparts = 3;
     cp.dd[0] = bp->sk_d[0];
     cp.dd[1] = bp->sk_d[1];
     cp.dd[2] = bp->sk_d[2];
     cp.rowmap = bp->rowmap;
     cp.dst = out;
-    cudaError_t e = launch_col_ls(lsa, cp, sms, s);
+    cudaError_t e = lcol(lsa, CP_SINGLE, cp);
     return e == cudaSuccess ? SPN_OK : BigPlan::err(e, "sketch single pass");
   }
   // column groups of ~32 MB of workspace
@@ -544,10 +687,8 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     pa.src_valid = n_in * ld_a;
     pa.dst = W;
     pa.dst_ld = dc;
-    pa.nparts = 1;
     pa.dd[0] = bp->sk_d[0];
-    pa.start_b = 0;
-    cudaError_t e = launch_col_ls(lsa, pa, sms, s);
+    cudaError_t e = lcol(lsa, CP_FIRST, pa);
     if (e != cudaSuccess) return BigPlan::err(e, "sketch P1");
     // P2: H(high), D2, H(high)
     pb.src = W;
@@ -555,30 +696,24 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     pb.src_valid = nn * dc;
     pb.dst = W;
     pb.dst_ld = dc;
-    pb.nparts = 2;
     pb.dd[0] = nullptr;
     pb.dd[1] = bp->sk_d[1];
-    pb.start_b = 1;
-    e = launch_col_ls(lsb, pb, sms, s);
+    e = lcol(lsb, CP_MID, pb);
     if (e != cudaSuccess) return BigPlan::err(e, "sketch P2");
     // P3: H(low), D3, H(low)
     pa.src = W;
     pa.src_ld = dc;
     pa.src_valid = nn * dc;
-    pa.nparts = 2;
     pa.dd[0] = nullptr;
     pa.dd[1] = bp->sk_d[2];
-    pa.start_b = 1;
-    e = launch_col_ls(lsa, pa, sms, s);
+    e = lcol(lsa, CP_MID, pa);
     if (e != cudaSuccess) return BigPlan::err(e, "sketch P3");
     // P4: H(high), gather P rows -> out
-    pb.nparts = 1;
     pb.dd[0] = nullptr;
     pb.dd[1] = nullptr;
-    pb.start_b = 0;
     pb.rowmap = bp->rowmap;
     pb.dst = out + c0;
-    e = launch_col_ls(lsb, pb, sms, s);
+    e = lcol(lsb, CP_LAST, pb);
     if (e != cudaSuccess) return BigPlan::err(e, "sketch P4");
   }
   return SPN_OK;
