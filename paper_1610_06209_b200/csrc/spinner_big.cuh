@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <vector>
@@ -340,7 +341,18 @@ inline cudaError_t launch_row(const RowParams& p, int sms, cudaStream_t s) {
 
 }  // namespace spn
 #include "spinner_pass.cuh"
+#include "spinner_tma.cuh"
 namespace spn {
+
+// L2-resident working set per pass group (default 32 MB; SPN_GROUP_MB overrides, for tuning).
+inline int64_t group_bytes() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("SPN_GROUP_MB");
+    const int64_t mb = e ? std::atoll(e) : 32;
+    return (mb > 0 ? mb : 32) << 20;
+  }();
+  return v;
+}
 
 inline int ilog2_i(int64_t n) {
   int l = 0;
@@ -367,6 +379,11 @@ struct BigPlan {
   size_t work_bytes = 0;
   int32_t* rowmap = nullptr;
   std::vector<int64_t> rowmap_key;
+  // groups alternate between two internal streams so one group's pass tail overlaps the
+  // next group's work (each pass is a full-GPU persistent kernel; fill/drain dominate
+  // otherwise).  Forked from / joined back into the caller's stream with events.
+  cudaStream_t ss[2] = {nullptr, nullptr};
+  cudaEvent_t evf = nullptr, evj[2] = {nullptr, nullptr};
   int64_t rowmap_m = -1;
 
   void release() {
@@ -385,12 +402,37 @@ struct BigPlan {
     }
     if (work) cudaFree(work);
     if (rowmap) cudaFree(rowmap);
+    for (auto& q : ss)
+      if (q) cudaStreamDestroy(q);
+    if (evf) cudaEventDestroy(evf);
+    for (auto& q : evj)
+      if (q) cudaEventDestroy(q);
     drow2 = nullptr;
     work = nullptr;
     rowmap = nullptr;
   }
 
   static spn_status err(cudaError_t e, const char* what) { return cuda_error(e, what); }
+
+  spn_status fork(cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      if (!ss[i]) e = cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking);
+      if (e == cudaSuccess && !evj[i]) e = cudaEventCreateWithFlags(&evj[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess && !evf) e = cudaEventCreateWithFlags(&evf, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(evf, s);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(ss[i], evf, 0);
+    return e == cudaSuccess ? SPN_OK : err(e, "fork streams");
+  }
+  spn_status join(cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaEventRecord(evj[i], ss[i]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, evj[i], 0);
+    }
+    return e == cudaSuccess ? SPN_OK : err(e, "join streams");
+  }
 
   spn_status ensure_work(size_t bytes) {
     if (work_bytes >= bytes) return SPN_OK;
@@ -466,25 +508,28 @@ struct BigPlan {
 
   // y = relu?(c * first rows of (H D3 H D2 H D1 x)) for every block (tables == 1).
   spn_status apply(const float* x, int64_t batch, int64_t ld_x, int64_t n_in, float* y, int64_t ld_y,
-                   int relu, int64_t k, int64_t m, int64_t blocks, double c, int sms, cudaStream_t s) {
+                   int relu, int64_t k, int64_t m, int64_t blocks, double c, int sms, cudaStream_t s0) {
     if (batch == 0) return SPN_OK;
     std::lock_guard<std::mutex> lock(mu);
     auto al16 = [](const void* q, int64_t ld) { return (reinterpret_cast<uintptr_t>(q) % 16 == 0) && (ld % 4 == 0); };
     // vectors per group: working set ~32 MB (L2-resident passes)
-    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t(32) << 20) / (n * 4)));
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(batch, group_bytes() / (n * 4)));
     const bool in_place = blocks == 1 && m == n && k == n && al16(y, ld_y);
     if (!in_place) {
-      spn_status st = ensure_work(static_cast<size_t>(G * n * 4));
+      spn_status st = ensure_work(static_cast<size_t>(2 * G * n * 4));
       if (st) return st;
     }
+    if (spn_status st = fork(s0)) return st;
     const bool staged = al16(x, ld_x);
     const int lc = staged ? staged_lc(L) : 10, lr = L - lc;
     const int64_t C = int64_t(1) << lc;
     for (int64_t b = 0; b < blocks; ++b) {
       const int64_t rows_valid = std::min(m, k - b * m);
-      for (int64_t v0 = 0; v0 < batch; v0 += G) {
+      int64_t gi = 0;
+      for (int64_t v0 = 0; v0 < batch; v0 += G, ++gi) {
+        const cudaStream_t s = ss[gi & 1];
         const int64_t nv = std::min(G, batch - v0);
-        float* W = in_place ? y + v0 * ld_y : work;
+        float* W = in_place ? y + v0 * ld_y : work + (gi & 1) * G * n;
         const int64_t wstride = in_place ? ld_y : n;
         cudaError_t e;
         if (staged) {
@@ -515,7 +560,8 @@ struct BigPlan {
           cp.nlo = 1;
           cp.nvec = nv;
           cp.dd[1] = stile2 + b * n;
-          e = launch_scol_ls(lr, SC_VMID, cp, sms, s);
+          const bool tma = lr >= 5 && al16(y, ld_y);
+          e = tma ? launch_tcol_ls(lr, SC_VMID, cp, sms, s) : launch_scol_ls(lr, SC_VMID, cp, sms, s);
           if (e != cudaSuccess) return err(e, "colpass P2");
           rp.src = W;
           rp.src_vstride = wstride;
@@ -529,7 +575,7 @@ struct BigPlan {
           cp.rows_valid = rows_valid;
           cp.cscale = static_cast<float>(c);
           cp.relu = relu;
-          e = launch_scol_ls(lr, SC_VLAST, cp, sms, s);
+          e = tma ? launch_tcol_ls(lr, SC_VLAST, cp, sms, s) : launch_scol_ls(lr, SC_VLAST, cp, sms, s);
           if (e != cudaSuccess) return err(e, "colpass P4");
           continue;
         }
@@ -575,7 +621,7 @@ struct BigPlan {
         if (e != cudaSuccess) return err(e, "rowpass P4");
       }
     }
-    return SPN_OK;
+    return join(s0);
   }
 
   spn_status build_sketch(int64_t nn, const std::vector<double>* d) {
@@ -630,15 +676,20 @@ struct BigPlan {
 inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int* /*dsign*/,
                              const float* a, int64_t n_in, int64_t dcols, int64_t ld_a,
                              const int64_t* rows, int64_t m_out, double cscale, float* out,
-                             int64_t ld_out, int sms, cudaStream_t s, BigPlan* bp) {
+                             int64_t ld_out, int sms, cudaStream_t s0, BigPlan* bp) {
   std::lock_guard<std::mutex> lock(bp->mu);
   if (spn_status st = bp->build_sketch(nn, d)) return st;
-  if (spn_status st = bp->set_rowmap(nn, rows, m_out, s)) return st;
+  if (spn_status st = bp->set_rowmap(nn, rows, m_out, s0)) return st;
+  cudaStream_t s = s0;
   const int lsa = bp->sk_lsa, lsb = bp->sk_lsb;
   // pipelined (cp.async double-buffered) column passes when both bit ranges fit them
   const bool staged = (reinterpret_cast<uintptr_t>(a) % 16 == 0) && (ld_a % 4 == 0) && lsa >= 2 && lsa <= 9 &&
                       (lsb == 0 || (lsb >= 2 && lsb <= 9));
+  // bulk-copy (TMA) rows when every stripe is full and every row 16-B aligned
+  const bool tma = staged && dcols % 32 == 0 && ld_out % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+                   lsa >= 5 && (lsb == 0 || lsb >= 5);
   auto lcol = [&](int ls, int prog, const ColParams& q) {  // CP_* and SC_FIRST..SC_SINGLE share numbering
+    if (tma) return launch_tcol_ls(ls, prog, q, sms, s);
     return staged ? launch_scol_ls(ls, prog, q, sms, s) : launch_col_ls(ls, prog, DM_PER_ROW, q, sms, s);
   };
   ColParams cp{};
@@ -664,12 +715,15 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     return e == cudaSuccess ? SPN_OK : BigPlan::err(e, "sketch single pass");
   }
   // column groups of ~32 MB of workspace
-  int64_t dc = std::max<int64_t>(32, ((int64_t(32) << 20) / (nn * 4)) / 32 * 32);
+  int64_t dc = std::max<int64_t>(32, (group_bytes() / (nn * 4)) / 32 * 32);
   dc = std::min<int64_t>(dc, (dcols + 31) / 32 * 32);
-  if (spn_status st = bp->ensure_work(static_cast<size_t>(nn * dc * 4))) return st;
-  float* W = bp->work;
+  if (spn_status st = bp->ensure_work(static_cast<size_t>(2 * nn * dc * 4))) return st;
+  if (spn_status st = bp->fork(s0)) return st;
+  int64_t gi = 0;
   const int64_t Sa = int64_t(1) << lsa, Sb = int64_t(1) << lsb;
-  for (int64_t c0 = 0; c0 < dcols; c0 += dc) {
+  for (int64_t c0 = 0; c0 < dcols; c0 += dc, ++gi) {
+    s = bp->ss[gi & 1];
+    float* W = bp->work + (gi & 1) * nn * dc;
     const int64_t nc = std::min(dc, dcols - c0);
     ColParams pa = cp;  // low-bit passes
     pa.ncols = nc;
@@ -716,7 +770,7 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     e = lcol(lsb, CP_LAST, pb);
     if (e != cudaSuccess) return BigPlan::err(e, "sketch P4");
   }
-  return SPN_OK;
+  return bp->join(s0);
 }
 
 }  // namespace spn
