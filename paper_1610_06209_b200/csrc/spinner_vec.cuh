@@ -41,7 +41,7 @@ struct VecParams {
   DiagArrays d[3][2];  // [diagonal][layout]
   int dsign[3];        // 1: diagonal is ±1 (use sgn), 0: real (use flt)
   float c;             // scale * n^{-3/2}
-  float c2;            // OP_EMBED_GAUSS: c / (2 pi sigma)  (argument in revolutions)
+  float c2;            // OP_EMBED_GAUSS: c / sigma (folded into x once per row)
   float norm;          // OP_EMBED_GAUSS: 1/sqrt(k)
   int32_t* ids;        // OP_HASH / OP_APPLY (optional): [batch][tables]
   float* y;            // OP_APPLY / OP_EMBED_*: output rows
@@ -401,6 +401,8 @@ __device__ __forceinline__ void sincos_rev(float u, float& s, float& c) {
   c = __cosf(a);
 }
 
+// (A 16-B-store variant of this epilogue — angles re-laid through smem so each lane owns
+// four consecutive elements — measured 0.577 vs 0.458 ms on config 2 and was dropped.)
 // Embed epilogue in layout B (element i = j*T + t): coalesced 4-B streaming stores.
 template <class C, int OP, bool CHECK>
 __device__ __forceinline__ void embed_store(const float (&r)[C::R], float* __restrict__ yrow,
@@ -410,8 +412,11 @@ __device__ __forceinline__ void embed_store(const float (&r)[C::R], float* __res
     const int i = j * C::T + t;
     if (CHECK && i >= rows) continue;
     if constexpr (OP == OP_EMBED_GAUSS) {
+      // staged x was pre-scaled by scale*n^-1.5/sigma, so r[j] already is the angle t
+      // (kernels.cpp:30); the SFU reduces t itself (FMUL.RZ by 1/2pi + MUFU.SIN/COS).
+      // Measured max abs error: 2.4e-6 for |t| <= 20 (tools/microbench/sincos_acc.cu).
       float s, co;
-      sincos_rev(r[j] * p.c2, s, co);
+      __sincosf(r[j], &s, &co);
       __stcs(yrow + i, co * p.norm);
       __stcs(yrow + p.k + i, s * p.norm);
     } else {  // OP_EMBED_ANG: sign with sign(0) = +1 (kernels.cpp:23-26)
@@ -529,6 +534,24 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
     if constexpr (STAGE_X) {
       cp_async_wait_all();
       group_sync<C>();
+      if constexpr (OP == OP_EMBED_GAUSS) {
+        // fold scale*n^-1.5/sigma into x once per row (the chain is linear), so the
+        // four blocks' epilogues feed sin/cos directly; each thread rescales the chunks
+        // it staged (chunk c = t + T*u at sw(4c)).
+        if (staged) {
+#pragma unroll
+          for (int u = 0; u < C::R / 4; ++u) {
+            float4* q = reinterpret_cast<float4*>(xb + sw<C>(4 * (t + C::T * u)));
+            float4 v4 = *q;
+            v4.x *= p.c2;
+            v4.y *= p.c2;
+            v4.z *= p.c2;
+            v4.w *= p.c2;
+            *q = v4;
+          }
+          group_sync<C>();
+        }
+      }
     }
 
     ArgBest best{-1.0f, 0x7fffffff, 0.0f};
@@ -555,6 +578,10 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
         load_x_B<C>(r, xrow, p.n_in, t);
         if constexpr (END_B) {
           if constexpr (C::T > 1) xpose_B_to_A<C>(r, sm, t);
+        }
+        if constexpr (OP == OP_EMBED_GAUSS) {
+#pragma unroll
+          for (int j = 0; j < C::R; ++j) r[j] *= p.c2;
         }
       }
       const int64_t tb = tab * p.blocks + b;

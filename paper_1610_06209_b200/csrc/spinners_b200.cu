@@ -419,7 +419,7 @@ spn_status spn_embed_f32(const spn_plan* p, int32_t kind, double sigma, const fl
   v.batch = batch;
   v.y = out;
   v.ld_y = ld_out;
-  v.c2 = static_cast<float>(p->scale * std::pow(static_cast<double>(p->n), -1.5) / (sigma * 2.0 * M_PI));
+  v.c2 = static_cast<float>(p->scale * std::pow(static_cast<double>(p->n), -1.5) / sigma);
   v.norm = static_cast<float>(1.0 / std::sqrt(static_cast<double>(p->k)));
   v.x_vec_ok = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (ld_x % 4 == 0);
   return run_vec(p, kind == SPN_EMBED_GAUSSIAN ? spn::OP_EMBED_GAUSS : spn::OP_EMBED_ANG, v,
