@@ -63,8 +63,9 @@ struct VCfg {
   static constexpr bool MULTI_WARP = T > 32;
   // register budget: resident warps/SM we ask ptxas to allow (R data registers + ~50)
   static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 24 : (R == 64 ? 12 : 12));
-  // looped six-half-transform chain (smaller SASS) — measured slower on B200 for
-  // n = 1024 and n = 16384 (r4: 0.498 vs 0.475 ms, 339 vs 328 ms), so kept off.
+  // looped six-half-transform chain (one copy of the butterfly code): measured slower for
+  // n = 1024 (0.498 vs 0.475 ms) and n = 16384 (443 vs 312 ms: the loop-carried mask
+  // rotation pushes R = 128 past its 168-register budget and spills), so kept off.
   static constexpr bool LOOPED = false;
   static constexpr int MIN_CTAS = TARGET_WARPS / (THREADS / 32) > 0 ? TARGET_WARPS / (THREADS / 32) : 1;
   // per group: transpose buffer (+ an x staging buffer for the embed ops, which reuse
@@ -99,19 +100,42 @@ __device__ __forceinline__ void bfly2(float& a0, float& a1, float& b0, float& b1
       : "+f"(a0), "+f"(a1), "+f"(b0), "+f"(b1));
 }
 
+// (a, b) <- (a + b, a - b) inside one register pair as a single packed FFMA2:
+// (b, b) * (1, -1) + (a, a) — ptxas encodes the (x, x) operands as .F32 broadcasts.
+// fma(b, +-1, a) is exactly the rounded a +- b, so results equal two FADDs.
+__device__ __forceinline__ void bfly_inpair(float& a, float& b) {
+  asm("{\n\t.reg .b64 pb, pa, pc, pd;\n\t"
+      "mov.b64 pb, {%1, %1};\n\t"
+      "mov.b64 pa, {%0, %0};\n\t"
+      "mov.b64 pc, {%2, %3};\n\t"
+      "fma.rn.f32x2 pd, pb, pc, pa;\n\t"
+      "mov.b64 {%0, %1}, pd;\n\t}"
+      : "+f"(a), "+f"(b)
+      : "f"(1.0f), "f"(-1.0f));
+}
+
 // Unnormalised butterflies over register bits [BLO, BHI) (transforms.cpp:58-67 restricted
-// to the element bits this thread holds).  Register pairs (2q, 2q+1) share one FADD2.
+// to the element bits this thread holds).  Register pairs (2q, 2q+1) share one FADD2;
+// the in-pair stage (bit 0) is one FFMA2 per pair.
 template <int R, int BLO, int BHI>
 __device__ __forceinline__ void reg_fwht(float (&r)[R]) {
 #pragma unroll
   for (int b = BLO; b < BHI; ++b) {
     const int h = 1 << b;
     if (b == 0) {
+      // FFMA2 halves the issue slots but occupies the FP32 pipe longer than two FADDs:
+      // a win where issue/instruction fetch binds (R = 128, c3: 312 -> 302 ms), a loss
+      // where the FP32 pipe binds (R = 32, c2: 0.458 -> 0.479 ms).
+      if constexpr (R >= 128) {
 #pragma unroll
-      for (int j = 0; j < R; j += 2) {
-        const float u = r[j], v = r[j + 1];
-        r[j] = u + v;
-        r[j + 1] = u - v;
+        for (int j = 0; j < R; j += 2) bfly_inpair(r[j], r[j + 1]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; j += 2) {
+          const float u = r[j], v = r[j + 1];
+          r[j] = u + v;
+          r[j + 1] = u - v;
+        }
       }
     } else {
 #pragma unroll
