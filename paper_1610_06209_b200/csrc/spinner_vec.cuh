@@ -24,7 +24,7 @@
 
 namespace spn {
 
-enum Op : int { OP_HASH = 0, OP_APPLY = 1, OP_EMBED_GAUSS = 2, OP_EMBED_ANG = 3 };
+enum Op : int { OP_HASH = 0, OP_APPLY = 1, OP_EMBED_GAUSS = 2, OP_EMBED_ANG = 3, OP_EMBED_GAUSS_P = 4 };
 enum Layout : int { LAY_B = 0, LAY_A = 1 };
 
 // One diagonal position (D1/D2/D3) in one layout, for every (table, block).
@@ -70,7 +70,7 @@ struct VCfg {
   static constexpr int MIN_CTAS = TARGET_WARPS / (THREADS / 32) > 0 ? TARGET_WARPS / (THREADS / 32) : 1;
   // per group: transpose buffer (+ an x staging buffer for the embed ops, which reuse
   // x across blocks and prefetch the next row with cp.async)
-  __host__ __device__ static constexpr bool xbuf(int op) { return op == 2 || op == 3; }
+  __host__ __device__ static constexpr bool xbuf(int op) { return op == 2 || op == 3 || op == 4; }
   __host__ __device__ static constexpr int smem_floats(int op) {
     return GPC * N * (xbuf(op) ? 2 : 1) + (T > 32 ? 4 * (T / 32) : 0);
   }
@@ -427,6 +427,33 @@ __device__ __forceinline__ void sincos_rev(float u, float& s, float& c) {
 
 // (A 16-B-store variant of this epilogue — angles re-laid through smem so each lane owns
 // four consecutive elements — measured 0.577 vs 0.458 ms on config 2 and was dropped.)
+// Permuted-coordinate Gaussian embed (OP_EMBED_GAUSS_P): layout-B register j of lane t
+// holds element (j & 3) + 4t + 128 (j >> 2); each register quad is stored as one float4
+// (a warp store covers 512 contiguous bytes).
+template <class C>
+__device__ __forceinline__ void embed_store_perm(const float (&r)[C::R], float* __restrict__ yrow,
+                                                 const VecParams& p, int t) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float4 s4, c4;
+    __sincosf(r[4 * q], &s4.x, &c4.x);
+    __sincosf(r[4 * q + 1], &s4.y, &c4.y);
+    __sincosf(r[4 * q + 2], &s4.z, &c4.z);
+    __sincosf(r[4 * q + 3], &s4.w, &c4.w);
+    c4.x *= p.norm;
+    c4.y *= p.norm;
+    c4.z *= p.norm;
+    c4.w *= p.norm;
+    s4.x *= p.norm;
+    s4.y *= p.norm;
+    s4.z *= p.norm;
+    s4.w *= p.norm;
+    const int e = 4 * t + 128 * q;
+    __stcs(reinterpret_cast<float4*>(yrow + e), c4);
+    __stcs(reinterpret_cast<float4*>(yrow + p.k + e), s4);
+  }
+}
+
 // Embed epilogue in layout B (element i = j*T + t): coalesced 4-B streaming stores.
 template <class C, int OP, bool CHECK>
 __device__ __forceinline__ void embed_store(const float (&r)[C::R], float* __restrict__ yrow,
@@ -558,6 +585,35 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
     if constexpr (STAGE_X) {
       cp_async_wait_all();
       group_sync<C>();
+      if constexpr (OP == OP_EMBED_GAUSS_P) {
+        // Permuted coordinates (R = T = 32, n = 1024): the kernel runs on v' = P v with
+        // e' = P(e) = ((e >> 2) & 31) | ((e & 3) << 5) | (e & 0x380).  H_n commutes with
+        // any bit permutation of the index, so H D' H ... on v' is P (H D H ... v) with
+        // the host-permuted diagonals D' = D o P^-1.  What it buys: the final layout B in
+        // e'-space gives lane t the elements (j & 3) + 4t + 128 (j >> 2), i.e. four
+        // CONSECUTIVE outputs per register quad -> 16-B streaming stores (6.2 vs 5.5 TB/s
+        // HBM write rate, tools/microbench/wbw.cu) with no extra transpose.
+        // Here: scale x by c/sigma and scatter it from natural to e' order (chunk
+        // c = t + 32u holds e = 4c .. 4c+3 -> e' = t + 32 i + 128 u; conflict free).
+        static_assert(C::R == 32 && C::T == 32, "permuted embed is the n = 1024 kernel");
+        if (staged) {
+          float xv[C::R];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 v4 = *reinterpret_cast<const float4*>(xb + sw<C>(4 * (t + 32 * u)));
+            xv[4 * u] = v4.x * p.c2;
+            xv[4 * u + 1] = v4.y * p.c2;
+            xv[4 * u + 2] = v4.z * p.c2;
+            xv[4 * u + 3] = v4.w * p.c2;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xb[sw<C>(t + 32 * i + 128 * u)] = xv[4 * u + i];
+          __syncwarp();
+        }
+      }
       if constexpr (OP == OP_EMBED_GAUSS) {
         // fold scale*n^-1.5/sigma into x once per row (the chain is linear), so the
         // four blocks' epilogues feed sin/cos directly; each thread rescales the chunks
@@ -641,10 +697,14 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
           continue;
         }
         if (!active) continue;
-        if (rows >= C::N)
-          embed_store<C, OP, false>(r, yrow, p, t, (int)rows);
-        else
-          embed_store<C, OP, true>(r, yrow, p, t, (int)rows);
+        if constexpr (OP == OP_EMBED_GAUSS_P) {
+          embed_store_perm<C>(r, yrow, p, t);  // host guarantees full 1024-row blocks
+        } else {
+          if (rows >= C::N)
+            embed_store<C, OP, false>(r, yrow, p, t, (int)rows);
+          else
+            embed_store<C, OP, true>(r, yrow, p, t, (int)rows);
+        }
       }
     }
 

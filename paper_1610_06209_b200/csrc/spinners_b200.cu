@@ -72,6 +72,7 @@ struct spn_plan {
   // vector-kernel layouts (n <= 2^14): [diag][layout]
   uint32_t* vsgn[3][2] = {};
   float* vflt[3][2] = {};
+  uint32_t* vsgnP[3][2] = {};  // n = 1024 sign masks in permuted coordinates (OP_EMBED_GAUSS_P)
   // multi-pass layouts (n > 2^14)
   spn::BigPlan big;
 
@@ -87,6 +88,9 @@ struct spn_plan {
       for (auto* p : a)
         if (p) cudaFree(p);
     for (auto& a : vflt)
+      for (auto* p : a)
+        if (p) cudaFree(p);
+    for (auto& a : vsgnP)
       for (auto* p : a)
         if (p) cudaFree(p);
     big.release();
@@ -111,27 +115,48 @@ spn_status upload(const void* src, size_t bytes, void** dst) {
   return SPN_OK;
 }
 
+// Inverse of the n = 1024 coordinate permutation of OP_EMBED_GAUSS_P (spinner_vec.cuh):
+// e' = ((e >> 2) & 31) | ((e & 3) << 5) | (e & 0x380).
+inline int64_t perm1024_inv(int64_t ep) { return ((ep >> 5) & 3) | ((ep & 31) << 2) | (ep & 0x380); }
+
+// Bit-packed sign masks of one diagonal in one layout (optionally in permuted coordinates).
+std::vector<uint32_t> pack_signs(const double* D, int64_t TB, int64_t N, int LOG_R, int LOG_T, int lay,
+                                 bool perm) {
+  const int64_t R = int64_t(1) << LOG_R, T = int64_t(1) << LOG_T;
+  const int64_t WORDS = R >= 32 ? R / 32 : 1, BITS = R >= 32 ? 32 : R;
+  std::vector<uint32_t> w(static_cast<size_t>(TB * WORDS * T), 0u);
+  for (int64_t tb = 0; tb < TB; ++tb)
+    for (int64_t q = 0; q < WORDS; ++q)
+      for (int64_t t = 0; t < T; ++t) {
+        uint32_t word = 0;
+        for (int64_t jj = 0; jj < BITS; ++jj) {
+          int64_t e = elem(lay, LOG_R, LOG_T, t, q * 32 + jj);
+          if (perm) e = perm1024_inv(e);
+          if (D[tb * N + e] < 0.0) word |= 1u << jj;
+        }
+        w[static_cast<size_t>(tb * WORDS * T + q * T + t)] = word;
+      }
+  return w;
+}
+
 // Pack the diagonals in the exact register order each kernel layout consumes.
 spn_status build_vec_layouts(spn_plan* p) {
   const int LOG_R = (p->log_n + 1) / 2, LOG_T = p->log_n / 2;
   const int64_t R = int64_t(1) << LOG_R, T = int64_t(1) << LOG_T, N = p->n;
-  const int64_t WORDS = R >= 32 ? R / 32 : 1, BITS = R >= 32 ? 32 : R;
   const int64_t TB = p->tables * p->blocks;
+  const bool all_sign = p->dsign[0] && p->dsign[1] && p->dsign[2];
   for (int di = 0; di < 3; ++di) {
     const double* D = p->d[di].data();
     for (int lay = 0; lay < 2; ++lay) {
       if (p->dsign[di]) {
-        std::vector<uint32_t> w(static_cast<size_t>(TB * WORDS * T), 0u);
-        for (int64_t tb = 0; tb < TB; ++tb)
-          for (int64_t q = 0; q < WORDS; ++q)
-            for (int64_t t = 0; t < T; ++t) {
-              uint32_t word = 0;
-              for (int64_t jj = 0; jj < BITS; ++jj)
-                if (D[tb * N + elem(lay, LOG_R, LOG_T, t, q * 32 + jj)] < 0.0) word |= 1u << jj;
-              w[static_cast<size_t>(tb * WORDS * T + q * T + t)] = word;
-            }
+        std::vector<uint32_t> w = pack_signs(D, TB, N, LOG_R, LOG_T, lay, false);
         spn_status s = upload(w.data(), w.size() * 4, reinterpret_cast<void**>(&p->vsgn[di][lay]));
         if (s) return s;
+        if (N == 1024 && all_sign) {  // permuted-coordinate embed kernel
+          w = pack_signs(D, TB, N, LOG_R, LOG_T, lay, true);
+          s = upload(w.data(), w.size() * 4, reinterpret_cast<void**>(&p->vsgnP[di][lay]));
+          if (s) return s;
+        }
       } else {
         std::vector<float> f(static_cast<size_t>(TB * N));
         for (int64_t tb = 0; tb < TB; ++tb)
@@ -422,6 +447,17 @@ spn_status spn_embed_f32(const spn_plan* p, int32_t kind, double sigma, const fl
   v.c2 = static_cast<float>(p->scale * std::pow(static_cast<double>(p->n), -1.5) / sigma);
   v.norm = static_cast<float>(1.0 / std::sqrt(static_cast<double>(p->k)));
   v.x_vec_ok = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (ld_x % 4 == 0);
+  // n = 1024, sign diagonals, full 1024-row blocks, 16-B aligned rows: permuted-coordinate
+  // kernel with 16-B feature stores (config 2's shape)
+  if (kind == SPN_EMBED_GAUSSIAN && p->n == 1024 && p->vsgnP[0][0] && v.x_vec_ok && p->m == 1024 &&
+      p->k % 1024 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 && ld_out % 4 == 0) {
+    if (batch == 0) return SPN_OK;
+    for (int di = 0; di < 3; ++di)
+      for (int lay = 0; lay < 2; ++lay) v.d[di][lay].sgn = p->vsgnP[di][lay];
+    DeviceGuard g(p->device);
+    cudaError_t e = spn::vec_launcher_gauss_perm()(v, static_cast<cudaStream_t>(stream), p->sms, batch);
+    return e == cudaSuccess ? SPN_OK : cuda_fail(e, "spinner_vec_kernel (permuted embed) launch");
+  }
   return run_vec(p, kind == SPN_EMBED_GAUSSIAN ? spn::OP_EMBED_GAUSS : spn::OP_EMBED_ANG, v,
                  static_cast<cudaStream_t>(stream));
 }

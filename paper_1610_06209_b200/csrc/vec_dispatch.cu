@@ -16,5 +16,6 @@ LaunchFn vec_launcher_hash(int log_n, int s) { return s ? vec_launcher_hash_s(lo
 LaunchFn vec_launcher_apply(int log_n, int s) { return s ? vec_launcher_apply_s(log_n) : vec_launcher_apply_g(log_n); }
 LaunchFn vec_launcher_gauss(int log_n, int s) { return s ? vec_launcher_gauss_s(log_n) : vec_launcher_gauss_g(log_n); }
 LaunchFn vec_launcher_ang(int log_n, int s) { return s ? vec_launcher_ang_s(log_n) : vec_launcher_ang_g(log_n); }
+LaunchFn vec_launcher_gauss_perm() { return &launch_vec<10, OP_EMBED_GAUSS_P, true>; }
 
 }  // namespace spn
