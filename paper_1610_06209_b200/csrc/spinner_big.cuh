@@ -382,8 +382,9 @@ struct BigPlan {
   // groups alternate between two internal streams so one group's pass tail overlaps the
   // next group's work (each pass is a full-GPU persistent kernel; fill/drain dominate
   // otherwise).  Forked from / joined back into the caller's stream with events.
-  cudaStream_t ss[2] = {nullptr, nullptr};
-  cudaEvent_t evf = nullptr, evj[2] = {nullptr, nullptr};
+  static constexpr int kMaxStreams = 4;
+  cudaStream_t ss[kMaxStreams] = {};
+  cudaEvent_t evf = nullptr, evj[kMaxStreams] = {};
   int64_t rowmap_m = -1;
 
   void release() {
@@ -414,20 +415,30 @@ struct BigPlan {
 
   static spn_status err(cudaError_t e, const char* what) { return cuda_error(e, what); }
 
+  // number of group streams (default 2; SPN_STREAMS overrides, 1..4)
+  static int nstreams() {
+    static const int v = [] {
+      const char* e = std::getenv("SPN_STREAMS");
+      const int k = e ? std::atoi(e) : 2;
+      return k < 1 ? 1 : (k > kMaxStreams ? kMaxStreams : k);
+    }();
+    return v;
+  }
+
   spn_status fork(cudaStream_t s) {
     cudaError_t e = cudaSuccess;
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    for (int i = 0; i < nstreams() && e == cudaSuccess; ++i) {
       if (!ss[i]) e = cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking);
       if (e == cudaSuccess && !evj[i]) e = cudaEventCreateWithFlags(&evj[i], cudaEventDisableTiming);
     }
     if (e == cudaSuccess && !evf) e = cudaEventCreateWithFlags(&evf, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(evf, s);
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(ss[i], evf, 0);
+    for (int i = 0; i < nstreams() && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(ss[i], evf, 0);
     return e == cudaSuccess ? SPN_OK : err(e, "fork streams");
   }
   spn_status join(cudaStream_t s) {
     cudaError_t e = cudaSuccess;
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    for (int i = 0; i < nstreams() && e == cudaSuccess; ++i) {
       e = cudaEventRecord(evj[i], ss[i]);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(s, evj[i], 0);
     }
@@ -516,7 +527,7 @@ struct BigPlan {
     const int64_t G = std::max<int64_t>(1, std::min<int64_t>(batch, group_bytes() / (n * 4)));
     const bool in_place = blocks == 1 && m == n && k == n && al16(y, ld_y);
     if (!in_place) {
-      spn_status st = ensure_work(static_cast<size_t>(2 * G * n * 4));
+      spn_status st = ensure_work(static_cast<size_t>(nstreams() * G * n * 4));
       if (st) return st;
     }
     if (spn_status st = fork(s0)) return st;
@@ -527,9 +538,10 @@ struct BigPlan {
       const int64_t rows_valid = std::min(m, k - b * m);
       int64_t gi = 0;
       for (int64_t v0 = 0; v0 < batch; v0 += G, ++gi) {
-        const cudaStream_t s = ss[gi & 1];
+        const int si = static_cast<int>(gi % nstreams());
+        const cudaStream_t s = ss[si];
         const int64_t nv = std::min(G, batch - v0);
-        float* W = in_place ? y + v0 * ld_y : work + (gi & 1) * G * n;
+        float* W = in_place ? y + v0 * ld_y : work + si * G * n;
         const int64_t wstride = in_place ? ld_y : n;
         cudaError_t e;
         if (staged) {
@@ -717,13 +729,14 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
   // column groups of ~32 MB of workspace
   int64_t dc = std::max<int64_t>(32, (group_bytes() / (nn * 4)) / 32 * 32);
   dc = std::min<int64_t>(dc, (dcols + 31) / 32 * 32);
-  if (spn_status st = bp->ensure_work(static_cast<size_t>(2 * nn * dc * 4))) return st;
+  if (spn_status st = bp->ensure_work(static_cast<size_t>(BigPlan::nstreams() * nn * dc * 4))) return st;
   if (spn_status st = bp->fork(s0)) return st;
   int64_t gi = 0;
   const int64_t Sa = int64_t(1) << lsa, Sb = int64_t(1) << lsb;
   for (int64_t c0 = 0; c0 < dcols; c0 += dc, ++gi) {
-    s = bp->ss[gi & 1];
-    float* W = bp->work + (gi & 1) * nn * dc;
+    const int si = static_cast<int>(gi % BigPlan::nstreams());
+    s = bp->ss[si];
+    float* W = bp->work + si * nn * dc;
     const int64_t nc = std::min(dc, dcols - c0);
     ColParams pa = cp;  // low-bit passes
     pa.ncols = nc;
