@@ -73,6 +73,18 @@ def test_config2_random_features(spn, golden, torch):
     assert (fa != golden["c2_ang"]).mean() < 1e-3
 
 
+def test_config2_unaligned_output_uses_general_kernel(spn, golden, torch):
+    """ld_out not a multiple of 4 -> the non-permuted (4-B store) kernel; same results."""
+    c = cases.C2
+    sp = spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, c["n"], min(c["n"], c["k"]), c["k"], c["seed"])
+    fm = spn.FeatureMap(sp, spn.KernelKind.gaussian(c["sigma"]))
+    x = dev(torch, golden["c2_x"])
+    buf = torch.zeros((x.shape[0], 2 * c["k"] + 1), device="cuda")
+    f = spn.embed(fm, x, out=buf[:, 1:]).cpu().numpy()
+    assert row_rel(f, golden["c2_feat"]).max() <= RTOL
+    assert float(buf[:, 0].abs().max()) == 0.0  # nothing written outside the view
+
+
 def test_config3_multitable_hash(spn, oracle, golden, torch):
     c = cases.C3
     h = spn.MultiTableHasher(spn.SpinnerVariant.hd3_hd2_hd1, c["n"], c["n"], c["tables"], seed=c["seed"])
@@ -274,3 +286,16 @@ def test_structured_spinner_build_uses_spec_seed(spn, oracle, torch):
     x = oracle.gaussian_rows(300, 10, 16)
     y = sp.apply(dev(torch, x)).cpu().numpy()
     assert np.max(np.abs(y - x.astype(np.float64) @ dense.T)) < 1e-5
+
+
+@pytest.mark.parametrize("logn", [19, 20])
+def test_cooperative_big_kernel(spn, oracle, torch, logn, monkeypatch):
+    """The opt-in vector-cooperative persistent kernel (SPN_COOP=1) matches the oracle."""
+    monkeypatch.setenv("SPN_COOP", "1")
+    n = 1 << logn
+    sp = spn.StackedSpinner(spn.SpinnerVariant.gauss3, n, n, n, 31 + logn, scale=1.0)
+    d = tuple(a[0].astype(np.float32).astype(np.float64) for a in sp.plan.diagonals())
+    x = oracle.gaussian_rows(logn + 100, 19, n)  # more vectors than CTA groups
+    y = sp.apply(dev(torch, x), relu=True).cpu().numpy()
+    want = oracle.apply(*d, n, n, n, 1.0, x, relu=True)
+    assert row_rel(y, want).max() <= RTOL
