@@ -70,38 +70,52 @@ __device__ __forceinline__ void tma_stage_row(const ColParams& p, const TileIdx&
   }
 }
 
+// Buffer count: three tiles when they fit one SM (LS <= 9: 3 x 64 KB), so two tiles are
+// in flight while one is computed (the passes are bound by bytes in flight per SM).
+template <int LS>
+struct TmaCfg {
+  static constexpr size_t TILE = sizeof(float) * (size_t(1) << LS) * 32;
+  static constexpr int NBUF = 3;
+  static constexpr size_t SMEM = TILE * NBUF;
+  static constexpr int BY_SMEM = (int)((227u * 1024u) / SMEM);
+  static constexpr int BY_REGS = 512 / SColCfg<LS>::THREADS;
+  static constexpr int M0 = BY_SMEM < BY_REGS ? BY_SMEM : BY_REGS;
+  static constexpr int MIN_CTAS = M0 < 1 ? 1 : M0;
+};
+
 template <int LS, int NPARTS, int DMASK, bool START_B, int DMODE, int EPI>
-__global__ void __launch_bounds__(SColCfg<LS>::THREADS, SColCfg<LS>::MIN_CTAS) colpass_tma_kernel(const ColParams p) {
+__global__ void __launch_bounds__(SColCfg<LS>::THREADS, TmaCfg<LS>::MIN_CTAS) colpass_tma_kernel(const ColParams p) {
   using C = SColCfg<LS>;
+  constexpr int NB = TmaCfg<LS>::NBUF;  // tiles in flight: NB-1 loads ahead of the compute
   static_assert(C::THREADS == C::S, "one row per thread");
   extern __shared__ __align__(128) float smem[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[NB];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t tiles = (uint32_t)(p.nvec * p.nhi * p.nlo * p.nstripes);
   constexpr bool END_B = C::W > 1 && (START_B ^ ((NPARTS & 1) != 0));
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], C::THREADS);
-    mbar_init(&bars[1], C::THREADS);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) mbar_init(&bars[b], C::THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   uint32_t phases = 0;  // bit b = parity of bars[b]
-  int cur = 0;
-  TileIdx ti{};
-  if (blockIdx.x < tiles) {
-    ti = tile_decode(p, blockIdx.x, LS);
-    tma_stage_row<C>(p, ti, smem, &bars[0]);
+#pragma unroll
+  for (int b = 0; b < NB - 1; ++b) {
+    const uint32_t t0 = blockIdx.x + b * gridDim.x;
+    if (t0 < tiles) tma_stage_row<C>(p, tile_decode(p, t0, LS), smem + b * (C::S * 32), &bars[b]);
   }
-  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, cur ^= 1) {
-    const TileIdx cti = ti;
+  int cur = 0;
+  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, cur = (cur + 1 == NB) ? 0 : cur + 1) {
+    const TileIdx cti = tile_decode(p, tile, LS);
     float* buf = smem + cur * (C::S * 32);
     mbar_wait(&bars[cur], (phases >> cur) & 1u);
     phases ^= 1u << cur;
-    const uint32_t nxt = tile + gridDim.x;
+    const uint32_t nxt = tile + (NB - 1) * gridDim.x;
     if (nxt < tiles) {
-      ti = tile_decode(p, nxt, LS);
-      bulk_wait_read();  // my previous bulk store out of that buffer has been read
-      tma_stage_row<C>(p, ti, smem + (cur ^ 1) * (C::S * 32), &bars[cur ^ 1]);
+      const int nb = (cur + NB - 1) % NB;  // the buffer of the previous tile
+      bulk_wait_read();  // my bulk store out of that buffer has been read
+      tma_stage_row<C>(p, tile_decode(p, nxt, LS), smem + nb * (C::S * 32), &bars[nb]);
     }
 
     float r[C::R];
@@ -203,15 +217,15 @@ inline cudaError_t launch_tcol(const ColParams& p_in, int sms, cudaStream_t s) {
   auto kern = colpass_tma_kernel<LS, NPARTS, DMASK, START_B, DMODE, EPI>;
   static int occ = 0;
   if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(TmaCfg<LS>::SMEM));
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, TmaCfg<LS>::SMEM);
     if (e != cudaSuccess) return e;
     occ = occ < 1 ? 1 : occ;
   }
   const int64_t tiles = p.nvec * p.nhi * p.nlo * p.nstripes;
   const int64_t grid = tiles < int64_t(sms) * occ ? (tiles < 1 ? 1 : tiles) : int64_t(sms) * occ;
-  kern<<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, s>>>(p);
+  kern<<<static_cast<unsigned>(grid), C::THREADS, TmaCfg<LS>::SMEM, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -62,12 +62,17 @@ struct VCfg {
   static constexpr int XMASK = (R / 4 >= 8 ? 8 : (R / 4 > 0 ? R / 4 : 1)) - 1;
   static constexpr bool MULTI_WARP = T > 32;
   // register budget: resident warps/SM we ask ptxas to allow (R data registers + ~50)
-  static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 24 : (R == 64 ? 12 : 12));
+  // R = 32: 28 warps (one wave for config 1's 4096 vectors: 18.6 vs 21.1 us) for hash /
+  // apply; the embed kernels keep 24 (80 registers; at 72 they spill: 0.475 vs 0.443 ms)
+  static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 28 : (R == 64 ? 12 : 12));
+  __host__ __device__ static constexpr int min_ctas(int op) {
+    return (R == 32 && op >= 2) ? (24 / (THREADS / 32) > 0 ? 24 / (THREADS / 32) : 1) : MIN_CTAS_BASE;
+  }
   // looped six-half-transform chain (one copy of the butterfly code): measured slower for
   // n = 1024 (0.498 vs 0.475 ms) and n = 16384 (443 vs 312 ms: the loop-carried mask
   // rotation pushes R = 128 past its 168-register budget and spills), so kept off.
   static constexpr bool LOOPED = false;
-  static constexpr int MIN_CTAS = TARGET_WARPS / (THREADS / 32) > 0 ? TARGET_WARPS / (THREADS / 32) : 1;
+  static constexpr int MIN_CTAS_BASE = TARGET_WARPS / (THREADS / 32) > 0 ? TARGET_WARPS / (THREADS / 32) : 1;
   // per group: transpose buffer (+ an x staging buffer for the embed ops, which reuse
   // x across blocks and prefetch the next row with cp.async)
   __host__ __device__ static constexpr bool xbuf(int op) { return op == 2 || op == 3 || op == 4; }
@@ -546,7 +551,7 @@ __device__ __forceinline__ void stage_x(float* xb, const float* __restrict__ xro
 // ------------------------------------------------------------------- kernel
 
 template <int LOG_R, int LOG_T, int OP, bool SIGNS>
-__global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T>::MIN_CTAS)
+__global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T>::min_ctas(OP))
     spinner_vec_kernel(const VecParams p) {
   using C = VCfg<LOG_R, LOG_T>;
   extern __shared__ __align__(16) float smem[];
