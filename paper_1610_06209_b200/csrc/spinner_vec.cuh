@@ -68,10 +68,10 @@ struct VCfg {
   __host__ __device__ static constexpr int min_ctas(int op) {
     return (R == 32 && op >= 2) ? (24 / (THREADS / 32) > 0 ? 24 / (THREADS / 32) : 1) : MIN_CTAS_BASE;
   }
-  // looped six-half-transform chain (one copy of the butterfly code): measured slower for
-  // n = 1024 (0.498 vs 0.475 ms) and n = 16384 (443 vs 312 ms: the loop-carried mask
-  // rotation pushes R = 128 past its 168-register budget and spills), so kept off.
-  static constexpr bool LOOPED = false;
+  // looped chain (one copy of the D -> H body, R == T only): keeps the n = 16384 kernel
+  // (R = 128, fully unrolled ~57 KB of SASS) inside the 32 KB L1.5 instruction cache.
+  // For n = 1024 the unrolled chain fits and measured faster (0.475 vs 0.498 ms).
+  static constexpr bool LOOPED = LOG_R == LOG_T && R >= 128;
   static constexpr int MIN_CTAS_BASE = TARGET_WARPS / (THREADS / 32) > 0 ? TARGET_WARPS / (THREADS / 32) : 1;
   // per group: transpose buffer (+ an x staging buffer for the embed ops, which reuse
   // x across blocks and prefetch the next row with cp.async)
@@ -324,30 +324,20 @@ __device__ __forceinline__ void spinner_chain(float (&r)[C::R], float* sm, const
                                               int t) {
   constexpr int L0 = END_B ? LAY_A : LAY_B, L1 = END_B ? LAY_B : LAY_A;
   if constexpr (SIGNS && C::LOOPED) {
-    uint32_t w0[C::WORDS], w1[C::WORDS], w2[C::WORDS];
-    load_words<C>(w0, p.d[0][L0].sgn, tb, t);
-    load_words<C>(w1, p.d[1][L1].sgn, tb, t);
-    load_words<C>(w2, p.d[2][L0].sgn, tb, t);
-    bool a_to_b = END_B;  // direction of the next transpose
+    // R == T: layout A -> B and B -> A are the same (thread, register) swap
+    // (thread t register j <-> thread j register t), and both halves of every H cover
+    // all register bits, so D -> H is ONE loop body run three times.
+    const uint32_t* w1p = p.d[1][L1].sgn;
+    const uint32_t* w2p = p.d[2][L0].sgn;
+    uint32_t w[C::WORDS];
+    load_words<C>(w, p.d[0][L0].sgn, tb, t);
 #pragma unroll 1
-    for (int part = 0; part < 6; ++part) {
-      const bool even = (part & 1) == 0;
-      if (even) {
-        xor_signs<C>(r, w0);
-#pragma unroll
-        for (int q = 0; q < C::WORDS; ++q) {
-          w0[q] = w1[q];
-          w1[q] = w2[q];
-        }
-      }
+    for (int h = 0; h < 3; ++h) {
+      xor_signs<C>(r, w);
+      if (h < 2) load_words<C>(w, h == 0 ? w1p : w2p, tb, t);  // in flight during the butterflies
       reg_fwht<C::R, 0, C::LOG_R>(r);
-      if (even) {
-        if (a_to_b)
-          xpose_A_to_B<C>(r, sm, t);
-        else
-          xpose_B_to_A<C>(r, sm, t);
-        a_to_b = !a_to_b;
-      }
+      xpose_A_to_B<C>(r, sm, t);
+      reg_fwht<C::R, 0, C::LOG_R>(r);
     }
   } else if constexpr (SIGNS) {
     uint32_t w0[C::WORDS], w1[C::WORDS], w2[C::WORDS];

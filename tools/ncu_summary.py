@@ -9,7 +9,8 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'l1tex__throughput.avg.pct_of_peak_sustained_active', 'sm__warps_active.avg.pct_of_peak_sustained_active',
         'smsp__issue_active.avg.pct_of_peak_sustained_active', 'launch__registers_per_thread', 'launch__grid_size',
         'launch__block_size', 'launch__occupancy_limit_registers', 'launch__occupancy_limit_shared_mem',
-        'lts__t_bytes.sum', 'sm__sass_thread_inst_executed_op_fadd_pred_on.sum']
+        'lts__t_bytes.sum', 'lts__throughput.avg.pct_of_peak_sustained_elapsed',
+        'l1tex__m_xbar2l1tex_read_bytes.sum', 'sm__memory_throughput.avg.pct_of_peak_sustained_elapsed', 'sm__sass_thread_inst_executed_op_fadd_pred_on.sum']
 
 
 def summarise(rep):
