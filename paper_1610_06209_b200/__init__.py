@@ -36,7 +36,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libspinners_b200.so")
+LIB_PATH = os.environ.get("SPN_LIB") or os.path.join(_HERE, "_lib", "libspinners_b200.so")  # SPN_LIB: A/B variants
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -218,9 +218,10 @@ class _Plan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            _plan_destroy(h)
-            self._h = _vp()
+        destroy = _plan_destroy  # None once the module is torn down at interpreter exit
+        if h is not None and h.value and destroy is not None:
+            destroy(h)
+            self._h = None
 
     # ---- device / host dispatch helpers
     def _device_in(self, x):

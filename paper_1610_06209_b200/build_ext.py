@@ -42,33 +42,46 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def _compile(src: str) -> str:
-    obj = os.path.join(OBJDIR, os.path.basename(src).replace(".cu", ".o"))
+def _compile(src: str, objdir: str = OBJDIR, extra: tuple = ()) -> str:
+    obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
     hdr_t = max(os.path.getmtime(d) for d in _deps() if not d.endswith(".cu"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t):
         return obj
-    cmd = [NVCC] + FLAGS + ["-c", src, "-o", obj]
+    cmd = [NVCC] + FLAGS + list(extra) + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     return obj
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = True, variant: str = "", defines: tuple = ()) -> str:
+    """Build the library.  A named variant (A/B experiments: extra -D flags) goes to
+    _lib/variants/<name>/ and is loaded by setting SPN_LIB to its path."""
+    lib, objdir = LIB, OBJDIR
+    if variant:
+        lib = os.path.join(LIBDIR, "variants", variant, "libspinners_b200.so")
+        objdir = os.path.join(LIBDIR, "variants", variant, "obj")
+    elif not force and up_to_date():
         return LIB
-    os.makedirs(OBJDIR, exist_ok=True)
+    os.makedirs(objdir, exist_ok=True)
     srcs = _sources()
+    extra = tuple("-D" + d for d in defines)
     with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(_compile, srcs))
-    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs
+        objs = list(ex.map(lambda f: _compile(f, objdir, extra), srcs))
+    cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     if verbose:
-        print(f"built {LIB}", file=sys.stderr)
-    return LIB
+        print(f"built {lib}", file=sys.stderr)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    a = ap.parse_args()
+    build(force=a.force, variant=a.variant, defines=tuple(a.defines))

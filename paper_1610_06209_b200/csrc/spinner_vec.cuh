@@ -122,6 +122,11 @@ __device__ __forceinline__ void bfly_inpair(float& a, float& b) {
 // Unnormalised butterflies over register bits [BLO, BHI) (transforms.cpp:58-67 restricted
 // to the element bits this thread holds).  Register pairs (2q, 2q+1) share one FADD2;
 // the in-pair stage (bit 0) is one FFMA2 per pair.
+#ifndef SPN_INPAIR_FFMA2_MIN_R
+#define SPN_INPAIR_FFMA2_MIN_R 1024
+#endif
+constexpr int kInpairFfma2MinR = SPN_INPAIR_FFMA2_MIN_R;
+
 template <int R, int BLO, int BHI>
 __device__ __forceinline__ void reg_fwht(float (&r)[R]) {
 #pragma unroll
@@ -131,7 +136,7 @@ __device__ __forceinline__ void reg_fwht(float (&r)[R]) {
       // FFMA2 halves the issue slots but occupies the FP32 pipe longer than two FADDs:
       // a win where issue/instruction fetch binds (R = 128, c3: 312 -> 302 ms), a loss
       // where the FP32 pipe binds (R = 32, c2: 0.458 -> 0.479 ms).
-      if constexpr (R >= 128) {
+      if constexpr (R >= kInpairFfma2MinR) {
 #pragma unroll
         for (int j = 0; j < R; j += 2) bfly_inpair(r[j], r[j + 1]);
       } else {
