@@ -342,7 +342,6 @@ inline cudaError_t launch_row(const RowParams& p, int sms, cudaStream_t s) {
 }  // namespace spn
 #include "spinner_pass.cuh"
 #include "spinner_tma.cuh"
-#include "spinner_coop.cuh"
 namespace spn {
 
 // L2-resident working set per pass group (default 32 MB; SPN_GROUP_MB overrides, for tuning).
@@ -379,7 +378,6 @@ struct BigPlan {
   float* work = nullptr;
   size_t work_bytes = 0;
   int32_t* rowmap = nullptr;
-  unsigned* counters = nullptr;  // cooperative kernel group barriers
   std::vector<int64_t> rowmap_key;
   // groups alternate between two internal streams so one group's pass tail overlaps the
   // next group's work (each pass is a full-GPU persistent kernel; fill/drain dominate
@@ -405,8 +403,6 @@ struct BigPlan {
     }
     if (work) cudaFree(work);
     if (rowmap) cudaFree(rowmap);
-    if (counters) cudaFree(counters);
-    counters = nullptr;
     for (auto& q : ss)
       if (q) cudaStreamDestroy(q);
     if (evf) cudaEventDestroy(evf);
@@ -460,9 +456,20 @@ struct BigPlan {
     return SPN_OK;
   }
 
-  // row-pass width for the staged schedule: C = 2^lc contiguous floats, lc = max(10, L-9)
-  // keeps the column pass at <= 9 bits (double-buffered tiles fit one SM).
-  static int staged_lc(int L) { return L - 9 > 10 ? L - 9 : 10; }
+  // row-pass width for the staged schedule: C = 2^lc contiguous floats, lc = max(10, L-8)
+  // (<= 12), so the column pass covers <= 8 bits: 32 KB tiles, 256-thread CTAs, two CTAs
+  // per SM (c5: 1.464 vs 1.519 ms with lc = L-9 and 64 KB tiles).  SPN_LC_EXTRA shifts it.
+  static int staged_lc(int L) {
+    static const int extra = [] {
+      const char* e = std::getenv("SPN_LC_EXTRA");
+      return e ? std::atoi(e) : 0;
+    }();
+    int lc = (L - 8 > 10 ? L - 8 : 10) + extra;
+    if (lc > 12) lc = 12;
+    if (lc < 10) lc = 10;
+    if (L - lc > 9) lc = L - 9;
+    return lc;
+  }
 
   static spn_status upload_f32(const std::vector<float>& f, float** dst) {
     cudaError_t e = cudaMalloc(dst, f.size() * 4);
@@ -535,35 +542,6 @@ struct BigPlan {
       if (st) return st;
     }
     if (spn_status st = fork(s0)) return st;
-    // one cooperative launch for 2^19 / 2^20-point vectors computed in place (config 5).
-    // Opt-in (SPN_COOP=1): correct, but measured 2.01 vs 1.77 ms for the two-stream
-    // per-pass schedule — both run at ~30 GB/s of L2 traffic per SM, i.e. the passes are
-    // bound by bytes in flight per SM, not by launch fill/drain.
-    if (in_place && al16(x, ld_x) && (L == 19 || L == 20) && std::getenv("SPN_COOP") != nullptr) {
-      cudaError_t e = cudaSuccess;
-      if (!counters) e = cudaMalloc(&counters, 1024 * sizeof(unsigned));
-      if (e == cudaSuccess) e = cudaMemsetAsync(counters, 0, 1024 * sizeof(unsigned), s0);
-      if (e != cudaSuccess) return err(e, "coop counters");
-      CoopParams cp{};
-      cp.x = x;
-      cp.ld_x = ld_x;
-      cp.n_in = n_in;
-      cp.batch = batch;
-      cp.y = y;
-      cp.ld_y = ld_y;
-      cp.rows_valid = n;
-      cp.d1row = srow1;
-      cp.d3row = srow3;
-      cp.d2tile = stile2;
-      cp.c = static_cast<float>(c);
-      cp.relu = relu;
-      cp.gs = 8;
-      cp.counters = counters;
-      e = L == 20 ? launch_coop<11>(cp, sms, s0) : launch_coop<10>(cp, sms, s0);
-      if (e == cudaSuccess) return SPN_OK;
-      if (e != cudaErrorNotSupported && e != cudaErrorCooperativeLaunchTooLarge) return err(e, "coop launch");
-      cudaGetLastError();  // fall through to the per-pass schedule
-    }
     const bool staged = al16(x, ld_x);
     const int lc = staged ? staged_lc(L) : 10, lr = L - lc;
     const int64_t C = int64_t(1) << lc;

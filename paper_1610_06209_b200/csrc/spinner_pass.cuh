@@ -389,6 +389,11 @@ inline cudaError_t launch_srow_lc(int lc, int prog, const RowParams2& p, int sms
     if (prog == RP_MID) return launch_srow<6, RP_MID>(p, sms, s);
     return launch_srow<6, RP_LAST>(p, sms, s);
   }
+  if (lc == 12) {
+    if (prog == RP_FIRST) return launch_srow<7, RP_FIRST>(p, sms, s);
+    if (prog == RP_MID) return launch_srow<7, RP_MID>(p, sms, s);
+    return launch_srow<7, RP_LAST>(p, sms, s);
+  }
   return cudaErrorInvalidValue;
 }
 

@@ -289,13 +289,12 @@ def test_structured_spinner_build_uses_spec_seed(spn, oracle, torch):
 
 
 @pytest.mark.parametrize("logn", [19, 20])
-def test_cooperative_big_kernel(spn, oracle, torch, logn, monkeypatch):
-    """The opt-in vector-cooperative persistent kernel (SPN_COOP=1) matches the oracle."""
-    monkeypatch.setenv("SPN_COOP", "1")
+def test_big_inplace_groups(spn, oracle, torch, logn):
+    """In-place 4-pass schedule over several L2 groups on alternating streams (config-5 shape)."""
     n = 1 << logn
     sp = spn.StackedSpinner(spn.SpinnerVariant.gauss3, n, n, n, 31 + logn, scale=1.0)
     d = tuple(a[0].astype(np.float32).astype(np.float64) for a in sp.plan.diagonals())
-    x = oracle.gaussian_rows(logn + 100, 19, n)  # more vectors than CTA groups
+    x = oracle.gaussian_rows(logn + 100, 19, n)  # more vectors than one 32 MB group
     y = sp.apply(dev(torch, x), relu=True).cpu().numpy()
     want = oracle.apply(*d, n, n, n, 1.0, x, relu=True)
     assert row_rel(y, want).max() <= RTOL
