@@ -477,15 +477,16 @@ struct BigPlan {
     return e == cudaSuccess ? SPN_OK : err(e, "upload diagonals");
   }
 
-  // D2 permuted per contiguous 2^lc segment into the layout-A float format of VCfg<lc-5, 5>.
-  static std::vector<float> row_perm(const std::vector<double>& d2, int64_t n, int64_t tb, int lc) {
-    const int64_t N = int64_t(1) << lc, R = N / 32;
+  // D permuted per contiguous 2^lc segment into the layout-A float format of
+  // VCfg<lc-lt, lt> (lt = log2 threads per segment: 5, or 6 for the two-warp 2^12 rows).
+  static std::vector<float> row_perm(const std::vector<double>& d2, int64_t n, int64_t tb, int lc, int lt = 5) {
+    const int64_t N = int64_t(1) << lc, T = int64_t(1) << lt, R = N / T;
     std::vector<float> f(static_cast<size_t>(tb * n));
     for (int64_t b = 0; b < tb; ++b)
       for (int64_t seg = 0; seg < n / N; ++seg)
-        for (int64_t t = 0; t < 32; ++t)
+        for (int64_t t = 0; t < T; ++t)
           for (int64_t j = 0; j < R; ++j) {
-            const int64_t pos = ((j / 4) * 32 + t) * 4 + (j % 4);
+            const int64_t pos = ((j / 4) * T + t) * 4 + (j % 4);
             f[static_cast<size_t>(b * n + seg * N + pos)] =
                 static_cast<float>(d2[static_cast<size_t>(b * n + seg * N + t * R + j)]);
           }
@@ -522,8 +523,8 @@ struct BigPlan {
     if (spn_status st = upload_f32(row_perm(d[1], n, tb, 10), &drow2)) return st;
     // staged (row-first) schedule: D1, D3 in the row passes, D2 in the column pass
     const int lc = staged_lc(L);
-    if (spn_status st = upload_f32(row_perm(d[0], n, tb, lc), &srow1)) return st;
-    if (spn_status st = upload_f32(row_perm(d[2], n, tb, lc), &srow3)) return st;
+    if (spn_status st = upload_f32(row_perm(d[0], n, tb, lc, row_lt(lc)), &srow1)) return st;
+    if (spn_status st = upload_f32(row_perm(d[2], n, tb, lc, row_lt(lc)), &srow3)) return st;
     if (spn_status st = upload_f32(tile_perm(d[1], n, tb, lc), &stile2)) return st;
     return SPN_OK;
   }

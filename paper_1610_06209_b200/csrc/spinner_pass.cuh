@@ -214,8 +214,10 @@ __global__ void __launch_bounds__(SColCfg<LS>::THREADS, SColCfg<LS>::MIN_CTAS) c
 }
 
 // ------------------------------------------------------------------- staged row pass
-// One warp per contiguous segment of N = 2^(LR+5) floats (layouts of spinner_vec.cuh,
-// T = 32).  Diagonals in the layout-A float format of spinner_vec.cuh, per segment.
+// One CTA of T = 2^LT threads per contiguous segment of N = 2^(LR+LT) floats (layouts of
+// spinner_vec.cuh: one warp up to 2^11, R = T = 64 at 2^12 — half the registers of a
+// single-warp R = 128 segment, c5 row passes 20.5 -> see DESIGN.md).  Diagonals in the
+// layout-A float format of spinner_vec.cuh, per segment.
 //   RP_FIRST  src -> [D@A] H(A->B) -> dst    (reads the staged segment in layout A)
 //   RP_MID    buf -> H(B->A) [D@A] H(A->B) -> buf   (in place)
 //   RP_LAST   buf -> H(B->A) -> xpose -> y = relu?(c*v), truncated to rows_valid
@@ -233,9 +235,10 @@ struct RowParams2 {
   int relu;
 };
 
-template <int LR, int PROG>
-__global__ void __launch_bounds__(32) rowpass_staged_kernel(const RowParams2 p) {
-  using C = VCfg<LR, 5>;
+template <int LR, int LT, int PROG>
+__global__ void __launch_bounds__(1 << LT) rowpass_staged_kernel(const RowParams2 p) {
+  using C = VCfg<LR, LT>;
+  static_assert(C::GPC == 1, "one segment per CTA");
   extern __shared__ __align__(16) float smem[];
   float* xb = smem;          // staging buffer (swizzled 16-B chunks)
   float* sm = smem + C::N;   // transpose buffer
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(32) rowpass_staged_kernel(const RowParams2 p) 
     const int64_t v = item >> lgseg, seg = item & (p.nseg - 1);
     float r[C::R];
     cp_async_wait_all();
-    __syncwarp();
+    group_sync<C>();
     {
       const Swz<C> z(t);
       if constexpr (PROG == RP_FIRST) {
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(32) rowpass_staged_kernel(const RowParams2 p) 
         for (int j = 0; j < C::R; ++j) r[j] = xb[z.B(t, j)];
       }
     }
-    __syncwarp();
+    group_sync<C>();
     if (item + gridDim.x < items) stage(item + gridDim.x);
     cp_async_commit();
     if constexpr (PROG != RP_FIRST) fwht_B_to_A<C>(r, sm, t);
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(32) rowpass_staged_kernel(const RowParams2 p) 
       const float4* f = reinterpret_cast<const float4*>(p.d + seg * C::N);
 #pragma unroll
       for (int q = 0; q < C::R / 4; ++q) {
-        const float4 dv = __ldg(f + q * 32 + t);
+        const float4 dv = __ldg(f + q * C::T + t);
         r[4 * q] *= dv.x;
         r[4 * q + 1] *= dv.y;
         r[4 * q + 2] *= dv.z;
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(32) rowpass_staged_kernel(const RowParams2 p) 
       fwht_A_to_B<C>(r, sm, t);
       float* row = p.dst + v * p.dst_vstride + seg * C::N;
 #pragma unroll
-      for (int j = 0; j < C::R; ++j) row[j * 32 + t] = r[j];
+      for (int j = 0; j < C::R; ++j) row[j * C::T + t] = r[j];
     } else {
       xpose_A_to_B<C>(r, sm, t);
       float* yrow = p.dst + v * p.dst_vstride + seg * C::N;
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(32) rowpass_staged_kernel(const RowParams2 p) 
       for (int j = 0; j < C::R; ++j) {
         float o = r[j] * p.c;
         if (p.relu) o = fmaxf(o, 0.0f);
-        if (all || seg * C::N + j * 32 + t < p.rows_valid) __stcs(yrow + j * 32 + t, o);
+        if (all || seg * C::N + j * C::T + t < p.rows_valid) __stcs(yrow + j * C::T + t, o);
       }
     }
   }
@@ -359,40 +362,43 @@ inline cudaError_t launch_scol_ls(int ls, int prog, const ColParams& p, int sms,
   return cudaErrorInvalidValue;
 }
 
-template <int LR, int PROG>
+template <int LR, int LT, int PROG>
 inline cudaError_t launch_srow(const RowParams2& p, int sms, cudaStream_t s) {
-  using C = VCfg<LR, 5>;
-  auto kern = rowpass_staged_kernel<LR, PROG>;
+  using C = VCfg<LR, LT>;
+  auto kern = rowpass_staged_kernel<LR, LT, PROG>;
   constexpr size_t smem = sizeof(float) * 2 * C::N;
   static int occ = 0;
   if (occ == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::T, smem);
     if (e != cudaSuccess) return e;
     occ = std::max(occ, 1);
   }
   const int64_t items = p.nvec * p.nseg;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(items, int64_t(sms) * occ));
-  kern<<<static_cast<unsigned>(grid), 32, smem, s>>>(p);
+  kern<<<static_cast<unsigned>(grid), C::T, smem, s>>>(p);
   return cudaGetLastError();
 }
 
+// threads per row segment: one warp up to 2^11 floats, two warps (R = T = 64) at 2^12
+inline int row_lt(int lc) { return lc >= 12 ? 6 : 5; }
+
 inline cudaError_t launch_srow_lc(int lc, int prog, const RowParams2& p, int sms, cudaStream_t s) {
   if (lc == 10) {
-    if (prog == RP_FIRST) return launch_srow<5, RP_FIRST>(p, sms, s);
-    if (prog == RP_MID) return launch_srow<5, RP_MID>(p, sms, s);
-    return launch_srow<5, RP_LAST>(p, sms, s);
+    if (prog == RP_FIRST) return launch_srow<5, 5, RP_FIRST>(p, sms, s);
+    if (prog == RP_MID) return launch_srow<5, 5, RP_MID>(p, sms, s);
+    return launch_srow<5, 5, RP_LAST>(p, sms, s);
   }
   if (lc == 11) {
-    if (prog == RP_FIRST) return launch_srow<6, RP_FIRST>(p, sms, s);
-    if (prog == RP_MID) return launch_srow<6, RP_MID>(p, sms, s);
-    return launch_srow<6, RP_LAST>(p, sms, s);
+    if (prog == RP_FIRST) return launch_srow<6, 5, RP_FIRST>(p, sms, s);
+    if (prog == RP_MID) return launch_srow<6, 5, RP_MID>(p, sms, s);
+    return launch_srow<6, 5, RP_LAST>(p, sms, s);
   }
   if (lc == 12) {
-    if (prog == RP_FIRST) return launch_srow<7, RP_FIRST>(p, sms, s);
-    if (prog == RP_MID) return launch_srow<7, RP_MID>(p, sms, s);
-    return launch_srow<7, RP_LAST>(p, sms, s);
+    if (prog == RP_FIRST) return launch_srow<6, 6, RP_FIRST>(p, sms, s);
+    if (prog == RP_MID) return launch_srow<6, 6, RP_MID>(p, sms, s);
+    return launch_srow<6, 6, RP_LAST>(p, sms, s);
   }
   return cudaErrorInvalidValue;
 }
