@@ -2,7 +2,7 @@
 
 * ``Oracle``   : the plain-C fp64 restatement (oracle/spinner_oracle.c).
 * ``Reference``: the reference's own sources compiled into oracle/_ref
-  (oracle/ref_api.cpp binds proj/src/{transforms,spinner,lsh,kernels}.cpp).
+  (oracle/ref_api.cpp binds proj/src/{transforms,spinner,lsh,kernels,newton_sketch}.cpp).
 
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu-baseline /
 ``--impl reference`` legs import this module, and only as the checker or the
@@ -176,6 +176,47 @@ class Oracle:
         self.lib.orc_sample_rows(N, m, seed, out)
         return out
 
+    # ---- sketched Newton (newton_sketch.cpp)
+    def ar1_problem(self, n, d, seed):
+        a, y = np.zeros((n, d)), np.zeros(n)
+        self.lib.orc_ar1_problem(i64(n), i64(d), u64(seed), a.ctypes.data_as(C.c_void_p),
+                                 y.ctypes.data_as(C.c_void_p))
+        return a, y
+
+    def _ay(self, a, y):
+        return np.ascontiguousarray(a, dtype=np.float64), np.ascontiguousarray(y, dtype=np.float64)
+
+    def logistic(self, a, y, x):
+        """(loss, gradient, hessian_sqrt) at x."""
+        a, y = self._ay(a, y)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, d = a.shape
+        L = self.lib
+        L.orc_logistic_loss.restype = dbl
+        vp = lambda v: v.ctypes.data_as(C.c_void_p)  # noqa: E731
+        f = L.orc_logistic_loss(vp(a), vp(y), i64(n), i64(d), vp(x))
+        g = np.zeros(d)
+        L.orc_logistic_gradient(vp(a), vp(y), i64(n), i64(d), vp(x), vp(g))
+        h = np.zeros((n, d))
+        L.orc_hessian_sqrt(vp(a), i64(n), i64(d), vp(x), vp(h))
+        return float(f), g, h
+
+    def sketched_step(self, a, y, x, N=None, m=None, scale=None, norm=None, diags=None):
+        """Exact step when diags is None, else first-m of one block (d1, d2, d3) over N."""
+        a, y = self._ay(a, y)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, d = a.shape
+        step = np.zeros(d)
+        vp = lambda v: v.ctypes.data_as(C.c_void_p) if v is not None else None  # noqa: E731
+        if diags is None:
+            rc = self.lib.orc_sketched_step(vp(a), vp(y), i64(n), i64(d), vp(x), i64(0), i64(0), dbl(0), dbl(0),
+                                            None, None, None, vp(step))
+        else:
+            d1, d2, d3 = (np.ascontiguousarray(v, dtype=np.float64).reshape(-1) for v in diags)
+            rc = self.lib.orc_sketched_step(vp(a), vp(y), i64(n), i64(d), vp(x), i64(N), i64(m), dbl(scale),
+                                            dbl(norm), vp(d1), vp(d2), vp(d3), vp(step))
+        return int(rc), step
+
 
 class ReferenceError_(RuntimeError):
     def __init__(self, code, msg):
@@ -273,6 +314,48 @@ class Reference:
         self._check(self.lib.ref_sketch(variant, a.shape[0], rows, seed, a, a.shape[1], a.shape[1], rl, out,
                                         threads))
         return out
+
+    # ---- sketched Newton: the reference's own newton_sketch.cpp
+    def ar1_problem(self, n, d, seed):
+        a, y = np.zeros((n, d)), np.zeros(n)
+        self._check(self.lib.ref_ar1_problem(i64(n), i64(d), u64(seed), a.ctypes.data_as(C.c_void_p),
+                                             y.ctypes.data_as(C.c_void_p)))
+        return a, y
+
+    def logistic(self, a, y, x):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, d = a.shape
+        f, g, h = C.c_double(), np.zeros(d), np.zeros((n, d))
+        vp = lambda v: v.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._check(self.lib.ref_logistic(vp(a), vp(y), i64(n), i64(d), vp(x), C.byref(f), vp(g), vp(h)))
+        return f.value, g, h
+
+    def sketched_step(self, a, y, x, variant=-1, rows=0, seed=0):
+        """variant < 0: exact step; else SketchOperator(variant, n, rows, seed) (first-m rows)."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, d = a.shape
+        step = np.zeros(d)
+        vp = lambda v: v.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._check(self.lib.ref_sketched_step(vp(a), vp(y), i64(n), i64(d), vp(x), cint(variant), i64(rows),
+                                               u64(seed), vp(step)))
+        return step
+
+    def solve(self, a, y, variant=-1, rows=0, max_iters=50, gap_tol=1e-10, line_search=True, seed=0):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        n, d = a.shape
+        it, fs, cv = i64(), C.c_double(), cint()
+        losses, gaps, xf = np.zeros(max_iters), np.zeros(max_iters), np.zeros(d)
+        vp = lambda v: v.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._check(self.lib.ref_solve(vp(a), vp(y), i64(n), i64(d), cint(variant), i64(rows), i64(max_iters),
+                                       dbl(gap_tol), cint(int(line_search)), u64(seed), C.byref(it), vp(losses),
+                                       vp(gaps), vp(xf), C.byref(fs), C.byref(cv)))
+        k = it.value
+        return {"losses": losses[:k], "gaps": gaps[:k], "x": xf, "f_star": fs.value, "converged": bool(cv.value)}
 
     def chain(self, d1, d2, d3, scale, x, relu=False, threads=1):
         x = _f32rows(x)

@@ -7,11 +7,15 @@
 // uses it as the CPU baseline ("kind": "reference") and as the --impl reference arm.
 // Nothing in the product links it.
 //
-// SketchOperator (proj/src/newton_sketch.cpp:74-101) is restated here over the
-// real StackedSpinner because newton_sketch.cpp needs Eigen's LLT.
+// newton_sketch.cpp compiles against the shim's LLT, so the sketched-Newton
+// entry points below (loss, gradient, hessian_sqrt, sketched_step, solve,
+// generate_ar1_problem) call the reference itself.  ref_sketch keeps its
+// restatement of SketchOperator::apply because it also serves the builder-defined
+// random-P mode.
 #include <spinners/common.hpp>
 #include <spinners/kernels.hpp>
 #include <spinners/lsh.hpp>
+#include <spinners/newton_sketch.hpp>
 #include <spinners/spinner.hpp>
 #include <spinners/transforms.hpp>
 
@@ -34,6 +38,7 @@ int fail(const std::exception& e) {
   g_err = e.what();
   if (dynamic_cast<const DimensionError*>(&e)) return 1;
   if (dynamic_cast<const DomainError*>(&e)) return 2;
+  if (dynamic_cast<const SingularSystemError*>(&e)) return 7;
   return 3;
 }
 
@@ -256,6 +261,107 @@ int ref_batch_chain(std::int64_t n, const double* d1, const double* d2, const do
         y[r * n + i] = (relu && t < 0.0) ? 0.0 : t;
       }
     });
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// ------------------------------------------------------------ sketched Newton
+// (newton_sketch.cpp, the reference's own functions).  Features are row-major
+// fp64 [n][d]; variant < 0 selects the exact (identity) sketch.
+
+namespace {
+LogisticProblem problem_of(const double* a, const double* labels, std::int64_t n, std::int64_t d) {
+  LogisticProblem p;
+  p.features.resize(n, d);
+  for (std::int64_t i = 0; i < n; ++i)
+    for (std::int64_t j = 0; j < d; ++j) p.features(i, j) = a[i * d + j];
+  p.labels.resize(n);
+  for (std::int64_t i = 0; i < n; ++i) p.labels(i) = labels[i];
+  return p;
+}
+Eigen::VectorXd vec_of(const double* x, std::int64_t d) {
+  Eigen::VectorXd v(d);
+  for (std::int64_t j = 0; j < d; ++j) v(j) = x[j];
+  return v;
+}
+SketchOperator sketch_of(int variant, std::int64_t n, std::int64_t rows, std::uint64_t seed) {
+  if (variant < 0) return SketchOperator();
+  return SketchOperator(variant_of(variant), static_cast<std::size_t>(n), static_cast<std::size_t>(rows), seed);
+}
+}  // namespace
+
+int ref_ar1_problem(std::int64_t n, std::int64_t d, std::uint64_t seed, double* features, double* labels) {
+  try {
+    LogisticProblem p = generate_ar1_problem(static_cast<std::size_t>(n), static_cast<std::size_t>(d), seed);
+    for (std::int64_t i = 0; i < n; ++i) {
+      for (std::int64_t j = 0; j < d; ++j) features[i * d + j] = p.features(i, j);
+      labels[i] = p.labels(i);
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_logistic(const double* a, const double* labels, std::int64_t n, std::int64_t d, const double* x,
+                 double* loss_out, double* grad_out, double* hsqrt_out) {
+  try {
+    LogisticProblem p = problem_of(a, labels, n, d);
+    Eigen::VectorXd xv = vec_of(x, d);
+    if (loss_out) *loss_out = loss(p, xv);
+    if (grad_out) {
+      Eigen::VectorXd g = gradient(p, xv);
+      for (std::int64_t j = 0; j < d; ++j) grad_out[j] = g(j);
+    }
+    if (hsqrt_out) {
+      Eigen::MatrixXd h = hessian_sqrt(p, xv);
+      for (std::int64_t i = 0; i < n; ++i)
+        for (std::int64_t j = 0; j < d; ++j) hsqrt_out[i * d + j] = h(i, j);
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_sketched_step(const double* a, const double* labels, std::int64_t n, std::int64_t d, const double* x,
+                      int variant, std::int64_t rows, std::uint64_t seed, double* step_out) {
+  try {
+    LogisticProblem p = problem_of(a, labels, n, d);
+    Eigen::VectorXd s = sketched_step(p, vec_of(x, d), sketch_of(variant, n, rows, seed));
+    for (std::int64_t j = 0; j < d; ++j) step_out[j] = s(j);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// solve(): iterations run, per-iteration losses / gaps, final iterate, f_star, converged.
+int ref_solve(const double* a, const double* labels, std::int64_t n, std::int64_t d, int variant,
+              std::int64_t rows, std::int64_t max_iters, double gap_tol, int line_search, std::uint64_t seed,
+              std::int64_t* iters, double* losses, double* gaps, double* x_final, double* f_star,
+              int* converged) {
+  try {
+    LogisticProblem p = problem_of(a, labels, n, d);
+    SketchConfig cfg;
+    if (variant >= 0) cfg.sketch_variant = variant_of(variant);
+    cfg.sketch_rows = static_cast<std::size_t>(rows);
+    cfg.max_iters = static_cast<std::size_t>(max_iters);
+    cfg.gap_tolerance = gap_tol;
+    cfg.line_search = line_search != 0;
+    cfg.seed = seed;
+    NewtonTrace t = solve(p, cfg);
+    *iters = static_cast<std::int64_t>(t.losses.size());
+    for (std::size_t i = 0; i < t.losses.size(); ++i) {
+      losses[i] = t.losses[i];
+      gaps[i] = t.gaps[i];
+    }
+    const Eigen::VectorXd& xf = t.iterates.back();
+    for (std::int64_t j = 0; j < d; ++j) x_final[j] = xf(j);
+    *f_star = t.f_star;
+    *converged = t.converged ? 1 : 0;
+    return 0;
   } catch (const std::exception& e) {
     return fail(e);
   }

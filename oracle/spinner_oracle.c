@@ -302,3 +302,162 @@ void orc_rng_fill(uint64_t seed, int kind, int64_t count, double* out) {
   for (int64_t i = 0; i < count; ++i)
     out[i] = kind == 1 ? orc_rng_uniform01(&r) : kind == 2 ? orc_rng_gaussian(&r) : orc_rng_rademacher(&r);
 }
+
+/* ------------------------------------------------------------ sketched Newton */
+
+/* newton_sketch.cpp:10-15 */
+static double log1p_exp(double t) {
+  if (t > 35.0) return t;
+  if (t < -35.0) return exp(t);
+  return log1p(exp(t));
+}
+
+/* newton_sketch.cpp:17-24 */
+static double sigmoid(double t) {
+  if (t >= 0.0) {
+    const double e = exp(-t);
+    return 1.0 / (1.0 + e);
+  }
+  const double e = exp(t);
+  return e / (1.0 + e);
+}
+
+/* newton_sketch.cpp:185-204: AR(1) rows (rho = 0.99) from Rng(mix_seed(seed, 7)),
+ * then the labels from the same stream. */
+void orc_ar1_problem(int64_t n, int64_t d, uint64_t seed, double* a, double* labels) {
+  const double rho = 0.99, noise = sqrt(1.0 - rho * rho);
+  orc_rng r;
+  orc_rng_init(&r, orc_mix_seed(seed, 7));
+  for (int64_t i = 0; i < n; ++i) {
+    double prev = orc_rng_gaussian(&r);
+    a[i * d] = prev;
+    for (int64_t j = 1; j < d; ++j) {
+      prev = rho * prev + noise * orc_rng_gaussian(&r);
+      a[i * d + j] = prev;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) labels[i] = orc_rng_rademacher(&r);
+}
+
+static double margin(const double* a, int64_t d, int64_t i, const double* x) {
+  double m = 0.0;
+  for (int64_t k = 0; k < d; ++k) m += a[i * d + k] * x[k];
+  return m;
+}
+
+/* newton_sketch.cpp:45-52 */
+double orc_logistic_loss(const double* a, const double* y, int64_t n, int64_t d, const double* x) {
+  double total = 0.0;
+  for (int64_t i = 0; i < n; ++i) total += log1p_exp(-y[i] * margin(a, d, i, x));
+  return total;
+}
+
+/* newton_sketch.cpp:54-61: A^T w, w_i = (sigmoid(y_i m_i) - 1) y_i */
+void orc_logistic_gradient(const double* a, const double* y, int64_t n, int64_t d, const double* x,
+                           double* g) {
+  double* w = (double*)malloc(sizeof(double) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) w[i] = (sigmoid(y[i] * margin(a, d, i, x)) - 1.0) * y[i];
+  for (int64_t j = 0; j < d; ++j) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += a[i * d + j] * w[i];
+    g[j] = s;
+  }
+  free(w);
+}
+
+/* newton_sketch.cpp:63-72: rows scaled by sqrt(s (1 - s)), s = sigmoid(a_i . x) */
+void orc_hessian_sqrt(const double* a, int64_t n, int64_t d, const double* x, double* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    const double s = sigmoid(margin(a, d, i, x));
+    const double h = sqrt(s * (1.0 - s));
+    for (int64_t j = 0; j < d; ++j) out[i * d + j] = a[i * d + j] * h;
+  }
+}
+
+/* Lower Cholesky (a non-positive pivot fails, as Eigen's LLT) + two triangular solves. */
+static int llt(const double* A, int64_t d, double* L) {
+  memset(L, 0, sizeof(double) * (size_t)(d * d));
+  for (int64_t j = 0; j < d; ++j) {
+    double p = A[j * d + j];
+    for (int64_t k = 0; k < j; ++k) p -= L[j * d + k] * L[j * d + k];
+    if (!(p > 0.0)) return 7;
+    const double ljj = sqrt(p);
+    L[j * d + j] = ljj;
+    for (int64_t i = j + 1; i < d; ++i) {
+      double s = A[i * d + j];
+      for (int64_t k = 0; k < j; ++k) s -= L[i * d + k] * L[j * d + k];
+      L[i * d + j] = s / ljj;
+    }
+  }
+  return 0;
+}
+
+/* newton_sketch.cpp:112-121: LLT; on failure add 1e-10 * trace to the diagonal and
+ * retry once; a second failure is SingularSystemError. */
+int orc_llt_solve(double* normal, int64_t d, const double* rhs, double* x) {
+  double* L = (double*)malloc(sizeof(double) * (size_t)(d * d));
+  int rc = llt(normal, d, L);
+  if (rc) {
+    double tr = 0.0;
+    for (int64_t j = 0; j < d; ++j) tr += normal[j * d + j];
+    for (int64_t j = 0; j < d; ++j) normal[j * d + j] += 1e-10 * tr;
+    rc = llt(normal, d, L);
+  }
+  if (!rc) {
+    double* t = (double*)malloc(sizeof(double) * (size_t)d);
+    for (int64_t i = 0; i < d; ++i) {
+      double s = rhs[i];
+      for (int64_t k = 0; k < i; ++k) s -= L[i * d + k] * t[k];
+      t[i] = s / L[i * d + i];
+    }
+    for (int64_t i = d - 1; i >= 0; --i) {
+      double s = t[i];
+      for (int64_t k = i + 1; k < d; ++k) s -= L[k * d + i] * x[k];
+      x[i] = s / L[i * d + i];
+    }
+    free(t);
+  }
+  free(L);
+  return rc;
+}
+
+/* newton_sketch.cpp:103-122: S B with B = hessian_sqrt, normal = (SB)^T SB,
+ * solve normal * step = -gradient. */
+int orc_sketched_step(const double* a, const double* y, int64_t n, int64_t d, const double* x, int64_t N,
+                      int64_t m, double scale, double norm, const double* d1, const double* d2,
+                      const double* d3, double* step) {
+  double* B = (double*)malloc(sizeof(double) * (size_t)(n * d));
+  orc_hessian_sqrt(a, n, d, x, B);
+  const int64_t rows = d1 ? m : n;
+  double* SB = B;
+  if (d1) {
+    SB = (double*)malloc(sizeof(double) * (size_t)(m * d));
+    double* v = (double*)malloc(sizeof(double) * (size_t)N);
+    for (int64_t c = 0; c < d; ++c) {
+      for (int64_t i = 0; i < N; ++i) v[i] = i < n ? B[i * d + c] : 0.0;
+      chain(N, d1, d2, d3, v);
+      for (int64_t r = 0; r < m; ++r) SB[r * d + c] = norm * (scale * v[r]);
+    }
+    free(v);
+  }
+  int rc = 0;
+  if (rows < d) rc = 1;
+  if (!rc) {
+    double* normal = (double*)malloc(sizeof(double) * (size_t)(d * d));
+    for (int64_t j = 0; j < d; ++j)
+      for (int64_t k = 0; k < d; ++k) {
+        double s = 0.0;
+        for (int64_t r = 0; r < rows; ++r) s += SB[r * d + j] * SB[r * d + k];
+        normal[j * d + k] = s;
+      }
+    double* rhs = (double*)malloc(sizeof(double) * (size_t)d);
+    orc_logistic_gradient(a, y, n, d, x, rhs);
+    for (int64_t j = 0; j < d; ++j) rhs[j] = -rhs[j];
+    rc = orc_llt_solve(normal, d, rhs, step);
+    free(rhs);
+    free(normal);
+  }
+  if (SB != B) free(SB);
+  free(B);
+  return rc;
+}

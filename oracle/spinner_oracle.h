@@ -94,6 +94,20 @@ void orc_sketch(int64_t n, double scale, double norm, const double* d1, const do
  * rejection sampling; returned sorted ascending. */
 void orc_sample_rows(int64_t N, int64_t m, uint64_t seed, int64_t* out);
 
+/* ---- sketched Newton for logistic regression (newton_sketch.cpp) ----------
+ * Features row-major fp64 [n][d], labels +-1.  Sketch = first-m rows of one
+ * spinner block over N = next_pow2(n) (d1..d3, scale) times norm, or exact when
+ * d1 == NULL.  Status: 0 ok, 1 dimension, 7 singular (SingularSystemError). */
+void orc_ar1_problem(int64_t n, int64_t d, uint64_t seed, double* a, double* labels); /* :185-204 */
+double orc_logistic_loss(const double* a, const double* y, int64_t n, int64_t d, const double* x); /* :45-52 */
+void orc_logistic_gradient(const double* a, const double* y, int64_t n, int64_t d, const double* x,
+                           double* g);                                                     /* :54-61 */
+void orc_hessian_sqrt(const double* a, int64_t n, int64_t d, const double* x, double* out); /* :63-72 */
+int orc_llt_solve(double* normal, int64_t d, const double* rhs, double* x);               /* :112-121 */
+int orc_sketched_step(const double* a, const double* y, int64_t n, int64_t d, const double* x, int64_t N,
+                      int64_t m, double scale, double norm, const double* d1, const double* d2,
+                      const double* d3, double* step);                                      /* :103-122 */
+
 #ifdef __cplusplus
 }
 #endif
