@@ -18,6 +18,9 @@
  *                               newton_sketch.cpp:74-101)
  *   spn_*_host               <- the same calls on host buffers (the reference's
  *                               value-semantics API), with the H2D/D2H copies inside.
+ *   spn_newton_*, spn_logistic_*, spn_sketched_step_f32, spn_ar1_problem
+ *                            <- the sketched Newton method that calls SketchOperator
+ *                               (newton_sketch.hpp:63-86; newton_sketch.cpp:45-72,103-204)
  *
  * Conventions: plain pointers and sizes; all sizes/strides in elements;
  * device entry points are stream-ordered and asynchronous (stream = a
@@ -49,7 +52,8 @@ typedef enum spn_status {
   SPN_ECUDA = 3,        /* CUDA runtime failure */
   SPN_ENOMEM = 4,       /* device / pinned allocation failed */
   SPN_EUNSUPPORTED = 5, /* valid request this build does not implement */
-  SPN_EINVAL = 6        /* null pointer / bad argument */
+  SPN_EINVAL = 6,       /* null pointer / bad argument */
+  SPN_ESINGULAR = 7     /* SingularSystemError (common.hpp:25): sketched Hessian indefinite */
 } spn_status;
 
 typedef enum spn_variant {
@@ -145,6 +149,44 @@ SPN_API uint64_t spn_mix_seed(uint64_t base, uint64_t stream);
  * non-finite entry, bit1 = all zero (what hash/embed reject, lsh.cpp:24-28). */
 SPN_API spn_status spn_check_rows_f32(const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
                                       int32_t* flags, void* stream);
+
+/* ------------------------------------------------------------------ sketched Newton
+ * Logistic regression with spinner-sketched Hessians (newton_sketch.hpp:13-86).
+ * Problem data on the device: A row-major fp32 [n][ld_a], labels fp32 (+-1) [n];
+ * iterates, steps and gradients fp64 [d] device vectors; losses fp64 device scalars.
+ * A workspace holds the per-problem scratch (margins, Hessian row scales, the
+ * sketched matrix S*B, the d x d normal matrix and its Cholesky factor).  d <= 1024.
+ * Calls on one workspace must be serialised by the caller. */
+typedef struct spn_newton spn_newton;
+SPN_API spn_status spn_newton_create(spn_newton** out, int64_t n, int64_t d, int64_t max_sketch_rows,
+                                     int device);
+SPN_API spn_status spn_newton_destroy(spn_newton* w);
+/* loss(p, x) (newton_sketch.cpp:45-52) and gradient(p, x) (:54-61) in one pass over A;
+ * either output may be NULL. */
+SPN_API spn_status spn_logistic_eval_f32(spn_newton* w, const float* a, int64_t ld_a, const float* labels,
+                                         const double* x, double* loss, double* grad, void* stream);
+/* hessian_sqrt(p, x) (:63-72): out[i][:] = sqrt(s_i (1 - s_i)) a_i, s_i = sigmoid(a_i . x). */
+SPN_API spn_status spn_hessian_sqrt_f32(spn_newton* w, const float* a, int64_t ld_a, const double* x,
+                                        float* out, int64_t ld_out, void* stream);
+/* sketched_step(p, x, sketch) (:103-122).  sketch = a plan made like
+ * SketchOperator(variant, n, rows, seed) (:74-81: n' = next_pow2(n), m = min(rows, n'),
+ * k = rows), applied with norm 1/sqrt(rows) to B = hessian_sqrt(p, x) (first `rows`
+ * rows, :87-101); sketch = NULL is the exact (identity) operator.  Solves
+ * ((S B)^T (S B)) step = -gradient by Cholesky with the reference's ridge retry
+ * (1e-10 * trace); SPN_ESINGULAR if that fails too; SPN_EDIM if rows < d.
+ * grad / loss (optional) receive gradient(p, x) / loss(p, x).  Synchronises `stream`
+ * (the status depends on the factorisation). */
+SPN_API spn_status spn_sketched_step_f32(spn_newton* w, const spn_plan* sketch, int64_t rows, const float* a,
+                                         int64_t ld_a, const float* labels, const double* x, double* step,
+                                         double* grad, double* loss, void* stream);
+/* The backtracking candidates of solve() (:140-143, :160-165):
+ * losses[k] = loss(p, x + (s0 * 2^-k) * step) for k < count (count <= 64). */
+SPN_API spn_status spn_logistic_line_f32(spn_newton* w, const float* a, int64_t ld_a, const float* labels,
+                                         const double* x, const double* step, double s0, int64_t count,
+                                         double* losses, void* stream);
+/* generate_ar1_problem(n, d, seed) (:185-204) on the host (reference generator, bit-exact
+ * in fp64), rounded to fp32: features [n][d], labels [n]. */
+SPN_API spn_status spn_ar1_problem(int64_t n, int64_t d, uint64_t seed, float* features, float* labels);
 
 #ifdef __cplusplus
 }

@@ -81,12 +81,14 @@ _sample_rows = _sig("spn_sample_rows", C.c_int, [_i64, _i64, _u64, _vp])
 _mix_seed = _sig("spn_mix_seed", _u64, [_u64, _u64])
 _check_rows = _sig("spn_check_rows_f32", C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp])
 
-SPN_OK, SPN_EDIM, SPN_EDOMAIN, SPN_ECUDA, SPN_ENOMEM, SPN_EUNSUPPORTED, SPN_EINVAL = range(7)
+SPN_OK, SPN_EDIM, SPN_EDOMAIN, SPN_ECUDA, SPN_ENOMEM, SPN_EUNSUPPORTED, SPN_EINVAL, SPN_ESINGULAR = range(8)
 ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_create",
                "spn_plan_create_explicit", "spn_plan_destroy", "spn_plan_query", "spn_plan_diagonals",
                "spn_apply_f32", "spn_hash_f32", "spn_embed_f32", "spn_sketch_f32", "spn_apply_f32_host",
                "spn_hash_f32_host", "spn_embed_f32_host", "spn_sample_rows", "spn_mix_seed",
-               "spn_check_rows_f32", "spn_realize_block")
+               "spn_check_rows_f32", "spn_realize_block", "spn_newton_create", "spn_newton_destroy",
+               "spn_logistic_eval_f32", "spn_hessian_sqrt_f32", "spn_sketched_step_f32", "spn_logistic_line_f32",
+               "spn_ar1_problem")
 
 
 # ----------------------------------------------------------------------- errors
@@ -102,6 +104,10 @@ class DomainError(ValueError):
     """Mirrors spinners::DomainError (common.hpp:19-21)."""
 
 
+class SingularSystemError(RuntimeError):
+    """Mirrors spinners::SingularSystemError (common.hpp:25-27)."""
+
+
 def _check(status: int) -> None:
     if status == SPN_OK:
         return
@@ -110,6 +116,8 @@ def _check(status: int) -> None:
         raise DimensionError(msg)
     if status == SPN_EDOMAIN:
         raise DomainError(msg)
+    if status == SPN_ESINGULAR:
+        raise SingularSystemError(msg)
     raise SpinnerError(msg)
 
 
@@ -517,7 +525,12 @@ class SketchOperator:
     StackedSpinner); mode "random" is the builder-defined P = sample_rows(...)
     of BASELINE config 4.  Output = sqrt(padded)/sqrt(rows) * P H D3 H D2 H D1 a_c."""
 
-    def __init__(self, variant, input_dim, rows, seed, mode="first", p_seed=None, device=0):
+    def __init__(self, variant=None, input_dim=None, rows=None, seed=0, mode="first", p_seed=None, device=0):
+        self._p = None
+        if variant is None:  # SketchOperator() = the exact (identity) operator (newton_sketch.hpp:55-56)
+            self.input_dim = self.padded = self.m = None
+            self.norm, self.row_list = 1.0, None
+            return
         padded = 1 << max(0, (input_dim - 1).bit_length())
         if rows > padded:
             raise SpinnerError("SketchOperator: rows > padded dimension (multi-block sketch) not supported")
@@ -534,11 +547,16 @@ class SketchOperator:
     def plan(self):
         return self._p
 
+    def is_exact(self) -> bool:
+        return self._p is None
+
     def rows(self, input_dim=None):
-        return self.m
+        return input_dim if self.is_exact() else self.m
 
     def apply(self, columns, out=None, stream=None):
         """columns: [input_dim, d] (row-major; the sketch runs along axis 0)."""
+        if self.is_exact():
+            return columns
         if columns.shape[0] != self.input_dim:
             raise DimensionError("SketchOperator::apply: row count mismatch")
         return self._p.sketch(columns, self.m, self.norm, rows=self.row_list, out=out, stream=stream)
@@ -548,5 +566,10 @@ __all__ = [
     "SpinnerVariant", "SpinnerSpec", "StructuredSpinner", "StackedSpinner", "CrossPolytopeHasher",
     "MultiTableHasher", "make_hasher_factory", "signed_argmax", "decode_id", "KernelKind", "FeatureMap",
     "embed", "SketchOperator", "mix_seed", "sample_rows", "realize_block", "check_rows", "DimensionError", "DomainError",
-    "SpinnerError", "variant_from_string", "version", "LIB_PATH", "ABI_SYMBOLS",
+    "SpinnerError", "SingularSystemError", "variant_from_string", "version", "LIB_PATH", "ABI_SYMBOLS",
+    "LogisticProblem", "SketchConfig", "NewtonTrace", "loss", "gradient", "hessian_sqrt", "sketched_step", "solve",
+    "generate_ar1_problem",
 ]
+
+from .newton import (LogisticProblem, NewtonTrace, SketchConfig, generate_ar1_problem, gradient,  # noqa: E402
+                     hessian_sqrt, loss, sketched_step, solve)

@@ -1,0 +1,673 @@
+// Sketched Newton for logistic regression on the device — the caller of
+// SketchOperator in the reference (proj/src/newton_sketch.cpp:45-122,
+// proj/include/spinners/newton_sketch.hpp:63-86).
+//
+// One Newton step = one pass over A (margins, loss, gradient, Hessian row scales
+// sqrt(s(1-s)) — loss/gradient/hessian_sqrt of the reference fused), the spinner
+// sketch of B = diag(h) A with h folded into D1 of the sketch's first pass (B is never
+// materialised), the d x d normal matrix (S B)^T (S B) in fp64, a blocked fp64
+// Cholesky with the reference's ridge retry, and two triangular solves.  All sums that
+// the reference does in fp64 are fp64 here; every reduction has a fixed order
+// (per-CTA partials + an ordered final sum), so results are run-to-run deterministic.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "../../include/spinners_b200.h"
+#include "errors.hpp"
+#include "host_params.hpp"
+#include "internal.hpp"
+
+namespace {
+
+constexpr int kMaxD = 1024;
+constexpr int kPassThreads = 256;  // 8 warps, one row per warp at a time
+constexpr int kNB = 32;            // Cholesky panel width
+constexpr int kST = 64;            // SYRK output tile (4 x 4 per thread)
+
+__device__ __forceinline__ double log1p_exp(double t) {  // newton_sketch.cpp:10-15
+  if (t > 35.0) return t;
+  if (t < -35.0) return exp(t);
+  return log1p(exp(t));
+}
+
+__device__ __forceinline__ double sigmoid(double t) {  // newton_sketch.cpp:17-24
+  if (t >= 0.0) {
+    const double e = exp(-t);
+    return 1.0 / (1.0 + e);
+  }
+  const double e = exp(t);
+  return e / (1.0 + e);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------- pass over A
+// Warp-per-row: lane l holds columns l, l+32, ... (DCH chunks).  Per row:
+// m = a.x (fp64), loss += log1p_exp(-y m), g += (sigmoid(y m) - 1) y a,
+// h = sqrt(s (1 - s)) with s = sigmoid(m).  Per-CTA partials [grid][d+1] (loss last).
+template <int DCH>
+__global__ void __launch_bounds__(kPassThreads) logistic_pass_kernel(const float* __restrict__ a, int64_t ld,
+                                                                     const float* __restrict__ labels,
+                                                                     const double* __restrict__ x, int64_t n, int d,
+                                                                     double* __restrict__ part,
+                                                                     double* __restrict__ margins,
+                                                                     float* __restrict__ h32,
+                                                                     double* __restrict__ h64) {
+  extern __shared__ double red[];  // d + 1
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t nw = (int64_t)gridDim.x * (kPassThreads / 32);
+  double xr[DCH], g[DCH];
+#pragma unroll
+  for (int c = 0; c < DCH; ++c) {
+    const int col = c * 32 + lane;
+    xr[c] = col < d ? x[col] : 0.0;
+    g[c] = 0.0;
+  }
+  double lsum = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * (kPassThreads / 32) + wid; r < n; r += nw) {
+    const float* row = a + r * ld;
+    float av[DCH];
+#pragma unroll
+    for (int c = 0; c < DCH; ++c) {
+      const int col = c * 32 + lane;
+      av[c] = col < d ? __ldg(row + col) : 0.0f;
+    }
+    double dot = 0.0;
+#pragma unroll
+    for (int c = 0; c < DCH; ++c) dot = fma((double)av[c], xr[c], dot);
+    const double m = warp_sum(dot);
+    if (labels) {
+      const double y = (double)__ldg(labels + r);
+      lsum += log1p_exp(-y * m);
+      const double w = (sigmoid(y * m) - 1.0) * y;
+#pragma unroll
+      for (int c = 0; c < DCH; ++c) g[c] = fma(w, (double)av[c], g[c]);
+    }
+    if (lane == 0) {
+      if (margins) margins[r] = m;
+      const double s = sigmoid(m);
+      const double h = sqrt(s * (1.0 - s));
+      if (h32) h32[r] = (float)h;
+      if (h64) h64[r] = h;
+    }
+  }
+  if (!part) return;
+  // ordered block reduction: warp 0, then 1, ... into smem
+  for (int i = threadIdx.x; i <= d; i += kPassThreads) red[i] = 0.0;
+  __syncthreads();
+  for (int w = 0; w < kPassThreads / 32; ++w) {
+    if (wid == w) {
+#pragma unroll
+      for (int c = 0; c < DCH; ++c) {
+        const int col = c * 32 + lane;
+        if (col < d) red[col] += g[c];
+      }
+      if (lane == 0) red[d] += lsum;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i <= d; i += kPassThreads) part[(int64_t)blockIdx.x * (d + 1) + i] = red[i];
+}
+
+// out[j] = sum_b part[b][j] (fixed order); j == d is the loss.
+__global__ void reduce_parts_kernel(const double* __restrict__ part, int nparts, int width,
+                                    double* __restrict__ grad, double* __restrict__ loss, int d) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= width) return;
+  double s = 0.0;
+  for (int b = 0; b < nparts; ++b) s += part[(int64_t)b * width + j];
+  if (j < d) {
+    if (grad) grad[j] = s;
+  } else if (loss) {
+    *loss = s;
+  }
+}
+
+__global__ void scale_rows_f32_kernel(const float* __restrict__ a, int64_t ld, const double* __restrict__ h,
+                                      int64_t n, int d, float* __restrict__ out, int64_t ld_out) {
+  const int64_t total = n * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / d;
+    const int j = (int)(e - i * d);
+    out[i * ld_out + j] = (float)((double)a[i * ld + j] * h[i]);
+  }
+}
+
+// ------------------------------------------------------------- normal matrix
+// part[s][i][j] = sum over rows r of slice s of (w_r x_ri)(w_r x_rj) for the lower
+// 64 x 64 tiles (bi >= bj); 256 threads, 4 x 4 outputs each, rows staged as fp64.
+__global__ void __launch_bounds__(256) syrk_partial_kernel(const float* __restrict__ X, int64_t ldx,
+                                                           const double* __restrict__ w, int64_t rows, int d,
+                                                           int64_t rows_per_split, double* __restrict__ part) {
+  __shared__ double Xi[32][kST + 1];
+  __shared__ double Xj[32][kST + 1];
+  const int t = blockIdx.x;
+  int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+  while (bi * (bi + 1) / 2 > t) --bi;
+  const int bj = t - bi * (bi + 1) / 2;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t r1 = min(rows, r0 + rows_per_split);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int64_t rc = r0; rc < r1; rc += 32) {
+    for (int e = threadIdx.x; e < 32 * kST; e += 256) {
+      const int rr = e / kST, cc = e - rr * kST;
+      const int64_t r = rc + rr;
+      const int ci = bi * kST + cc, cj = bj * kST + cc;
+      double wi = 0.0, wj = 0.0;
+      if (r < r1) {
+        const double ww = w ? w[r] : 1.0;
+        if (ci < d) wi = (double)X[r * ldx + ci] * ww;
+        if (cj < d) wj = (double)X[r * ldx + cj] * ww;
+      }
+      Xi[rr][cc] = wi;
+      Xj[rr][cc] = wj;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {
+      double u[4], v[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) u[a] = Xi[rr][ty * 4 + a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) v[b] = Xj[rr][tx * 4 + b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(u[a], v[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+  double* out = part + (int64_t)blockIdx.y * d * d;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = bi * kST + ty * 4 + a, j = bj * kST + tx * 4 + b;
+      if (i < d && j < d) out[(int64_t)i * d + j] = acc[a][b];
+    }
+}
+
+// normal[i][j] = normal[j][i] = sum_s part[s][i][j] for i >= j (fixed order).
+__global__ void syrk_reduce_kernel(const double* __restrict__ part, int nsplit, int d, double* __restrict__ normal) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)d * d) return;
+  const int i = (int)(e / d), j = (int)(e - (int64_t)i * d);
+  if (j > i) return;
+  double s = 0.0;
+  for (int k = 0; k < nsplit; ++k) s += part[(int64_t)k * d * d + e];
+  normal[e] = s;
+  normal[(int64_t)j * d + i] = s;
+}
+
+// ------------------------------------------------------------- Cholesky (lower, in place)
+// Panel j0: factor the nb x nb diagonal block in smem (right-looking inside the panel,
+// so every element sees its subtractions in column order, like the unblocked LLT),
+// then each thread solves one row of the sub-diagonal panel L21 = A21 L11^{-T}.
+// A non-positive pivot sets *flag (Eigen's LLT NumericalIssue).
+__global__ void __launch_bounds__(1024) chol_panel_kernel(double* __restrict__ A, int d, int j0,
+                                                          int* __restrict__ flag) {
+  __shared__ double L[kNB][kNB + 1];
+  __shared__ int bad;
+  if (*flag) return;
+  const int nb = min(kNB, d - j0);
+  const int tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e - i * nb;
+    L[i][j] = i >= j ? A[(int64_t)(j0 + i) * d + j0 + j] : 0.0;
+  }
+  __syncthreads();
+  for (int k = 0; k < nb; ++k) {
+    if (tid == 0) {
+      const double p = L[k][k];
+      if (!(p > 0.0))
+        bad = 1;
+      else
+        L[k][k] = sqrt(p);
+    }
+    __syncthreads();
+    if (bad) {
+      if (tid == 0) *flag = 1;
+      return;
+    }
+    if (tid > k && tid < nb) L[tid][k] /= L[k][k];
+    __syncthreads();
+    for (int e = tid; e < nb * nb; e += blockDim.x) {
+      const int i = e / nb, j = e - i * nb;
+      if (j > k && i >= j) L[i][j] -= L[i][k] * L[j][k];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e - i * nb;
+    if (i >= j) A[(int64_t)(j0 + i) * d + j0 + j] = L[i][j];
+  }
+  // rows below the panel
+  for (int i = j0 + nb + tid; i < d; i += blockDim.x) {
+    double* row = A + (int64_t)i * d + j0;
+    double l[kNB];
+#pragma unroll
+    for (int k = 0; k < kNB; ++k) {
+      if (k < nb) {
+        double s = row[k];
+        for (int m = 0; m < k; ++m) s -= l[m] * L[k][m];
+        l[k] = s / L[k][k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kNB; ++k)
+      if (k < nb) row[k] = l[k];
+  }
+}
+
+// Trailing update A22 -= L21 L21^T on the lower 32 x 32 tiles below/right of panel j0.
+__global__ void __launch_bounds__(256) chol_update_kernel(double* __restrict__ A, int d, int j0,
+                                                          const int* __restrict__ flag) {
+  __shared__ double Li[kNB][kNB + 1];
+  __shared__ double Lj[kNB][kNB + 1];
+  if (*flag) return;
+  const int t = blockIdx.x;
+  int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+  while (bi * (bi + 1) / 2 > t) --bi;
+  const int bj = t - bi * (bi + 1) / 2;
+  const int base = j0 + kNB;
+  const int i0 = base + bi * kNB, jj0 = base + bj * kNB;
+  for (int e = threadIdx.x; e < kNB * kNB; e += 256) {
+    const int r = e / kNB, k = e - r * kNB;
+    Li[r][k] = (i0 + r < d) ? A[(int64_t)(i0 + r) * d + j0 + k] : 0.0;
+    Lj[r][k] = (jj0 + r < d) ? A[(int64_t)(jj0 + r) * d + j0 + k] : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kNB * kNB; e += 256) {
+    const int r = e / kNB, c = e - r * kNB;
+    const int i = i0 + r, j = jj0 + c;
+    if (i < d && j < d && j <= i) {
+      double s = A[(int64_t)i * d + j];
+#pragma unroll 8
+      for (int k = 0; k < kNB; ++k) s -= Li[r][k] * Lj[c][k];
+      A[(int64_t)i * d + j] = s;
+    }
+  }
+}
+
+// step = -(L L^T)^{-1} grad: forward then backward substitution (one CTA).
+__global__ void __launch_bounds__(1024) chol_solve_kernel(const double* __restrict__ L, int d,
+                                                          const double* __restrict__ grad, double* __restrict__ step,
+                                                          const int* __restrict__ flag) {
+  extern __shared__ double b[];
+  if (*flag) return;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) b[i] = -grad[i];
+  __syncthreads();
+  for (int k = 0; k < d; ++k) {
+    const double yk = b[k] / L[(int64_t)k * d + k];
+    __syncthreads();
+    if (threadIdx.x == 0) b[k] = yk;
+    for (int i = k + 1 + threadIdx.x; i < d; i += blockDim.x) b[i] -= L[(int64_t)i * d + k] * yk;
+    __syncthreads();
+  }
+  for (int i = d - 1; i >= 0; --i) {
+    const double xi = b[i] / L[(int64_t)i * d + i];
+    __syncthreads();
+    if (threadIdx.x == 0) b[i] = xi;
+    for (int k = threadIdx.x; k < i; k += blockDim.x) b[k] -= L[(int64_t)i * d + k] * xi;
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < d; i += blockDim.x) step[i] = b[i];
+}
+
+// normal_jj += 1e-10 * trace(normal)   (newton_sketch.cpp:114-115)
+__global__ void ridge_kernel(double* __restrict__ normal, int d) {
+  __shared__ double tr;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int j = 0; j < d; ++j) t += normal[(int64_t)j * d + j];
+    tr = t;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < d; j += blockDim.x) normal[(int64_t)j * d + j] += 1e-10 * tr;
+}
+
+// ------------------------------------------------------------- line search
+// losses[k] = sum_r log1p_exp(-y_r (a_r.x + s_k a_r.step)), s_k = s0 * 2^-k; lanes own candidates.
+template <int DCH>
+__global__ void __launch_bounds__(kPassThreads) line_kernel(const float* __restrict__ a, int64_t ld,
+                                                            const float* __restrict__ labels,
+                                                            const double* __restrict__ x,
+                                                            const double* __restrict__ step, int64_t n, int d,
+                                                            double s0, int count, double* __restrict__ part) {
+  __shared__ double red[64];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t nw = (int64_t)gridDim.x * (kPassThreads / 32);
+  double xr[DCH], pr[DCH];
+#pragma unroll
+  for (int c = 0; c < DCH; ++c) {
+    const int col = c * 32 + lane;
+    xr[c] = col < d ? x[col] : 0.0;
+    pr[c] = col < d ? step[col] : 0.0;
+  }
+  const double sA = s0 * exp2(-(double)lane), sB = s0 * exp2(-(double)(lane + 32));
+  double accA = 0.0, accB = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * (kPassThreads / 32) + wid; r < n; r += nw) {
+    const float* row = a + r * ld;
+    double dm = 0.0, dq = 0.0;
+#pragma unroll
+    for (int c = 0; c < DCH; ++c) {
+      const int col = c * 32 + lane;
+      const double v = col < d ? (double)__ldg(row + col) : 0.0;
+      dm = fma(v, xr[c], dm);
+      dq = fma(v, pr[c], dq);
+    }
+    const double m = warp_sum(dm), q = warp_sum(dq);
+    const double y = (double)__ldg(labels + r);
+    if (lane < count) accA += log1p_exp(-y * (m + sA * q));
+    if (lane + 32 < count) accB += log1p_exp(-y * (m + sB * q));
+  }
+  if (threadIdx.x < 64) red[threadIdx.x] = 0.0;
+  __syncthreads();
+  for (int w = 0; w < kPassThreads / 32; ++w) {
+    if (wid == w) {
+      red[lane] += accA;
+      red[lane + 32] += accB;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < count) part[(int64_t)blockIdx.x * count + threadIdx.x] = red[threadIdx.x];
+}
+
+int sm_count(int dev) {
+  int s = 0;
+  if (cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || s < 1) s = 148;
+  return s;
+}
+
+spn_status fail(spn_status s, const char* msg) { return spn::set_error(s, msg); }
+
+#define NWT_CUDA(call)                                                 \
+  do {                                                                 \
+    cudaError_t e_ = (call);                                           \
+    if (e_ != cudaSuccess) return spn::cuda_error(e_, #call);          \
+  } while (0)
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct spn_newton {
+  int64_t n = 0, d = 0, max_rows = 0;
+  int device = 0, sms = 148, grid = 296, nsplit_max = 1;
+  double* part = nullptr;     // [grid][d+1] pass partials (also line-search partials)
+  double* margins = nullptr;  // [n]
+  float* h32 = nullptr;       // [n] Hessian row scales (sketch D1 scaling)
+  double* h64 = nullptr;      // [n] the same in fp64 (exact normal matrix, hessian_sqrt)
+  float* sb = nullptr;        // [max_rows][d] sketched S B
+  double* spart = nullptr;    // [nsplit_max][d][d]
+  double* normal = nullptr;   // [d][d]
+  double* fact = nullptr;     // [d][d] Cholesky factor (lower)
+  double* grad = nullptr;     // [d]
+  double* loss = nullptr;     // [1]
+  int* flag = nullptr;        // device pivot-failure flag
+  int* flag_h = nullptr;      // pinned
+};
+
+namespace {
+
+void newton_free(spn_newton* w) {
+  for (void* p : {(void*)w->part, (void*)w->margins, (void*)w->h32, (void*)w->h64, (void*)w->sb, (void*)w->spart,
+                  (void*)w->normal, (void*)w->fact, (void*)w->grad, (void*)w->loss, (void*)w->flag})
+    if (p) cudaFree(p);
+  if (w->flag_h) cudaFreeHost(w->flag_h);
+}
+
+template <int DCH>
+cudaError_t launch_pass_t(const spn_newton* w, const float* a, int64_t ld, const float* labels, const double* x,
+                          bool want_part, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (size_t)(w->d + 1);
+  logistic_pass_kernel<DCH><<<w->grid, kPassThreads, smem, s>>>(a, ld, labels, x, w->n, (int)w->d,
+                                                                 want_part ? w->part : nullptr, w->margins, w->h32,
+                                                                 w->h64);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pass(const spn_newton* w, const float* a, int64_t ld, const float* labels, const double* x,
+                        bool want_part, cudaStream_t s) {
+  const int dch = (int)((w->d + 31) / 32);
+  if (dch <= 2) return launch_pass_t<2>(w, a, ld, labels, x, want_part, s);
+  if (dch <= 4) return launch_pass_t<4>(w, a, ld, labels, x, want_part, s);
+  if (dch <= 8) return launch_pass_t<8>(w, a, ld, labels, x, want_part, s);
+  if (dch <= 16) return launch_pass_t<16>(w, a, ld, labels, x, want_part, s);
+  return launch_pass_t<32>(w, a, ld, labels, x, want_part, s);
+}
+
+template <int DCH>
+cudaError_t launch_line_t(const spn_newton* w, const float* a, int64_t ld, const float* labels, const double* x,
+                          const double* step, double s0, int count, cudaStream_t s) {
+  line_kernel<DCH><<<w->grid, kPassThreads, 0, s>>>(a, ld, labels, x, step, w->n, (int)w->d, s0, count, w->part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_line(const spn_newton* w, const float* a, int64_t ld, const float* labels, const double* x,
+                        const double* step, double s0, int count, cudaStream_t s) {
+  const int dch = (int)((w->d + 31) / 32);
+  if (dch <= 2) return launch_line_t<2>(w, a, ld, labels, x, step, s0, count, s);
+  if (dch <= 4) return launch_line_t<4>(w, a, ld, labels, x, step, s0, count, s);
+  if (dch <= 8) return launch_line_t<8>(w, a, ld, labels, x, step, s0, count, s);
+  if (dch <= 16) return launch_line_t<16>(w, a, ld, labels, x, step, s0, count, s);
+  return launch_line_t<32>(w, a, ld, labels, x, step, s0, count, s);
+}
+
+// normal = X^T diag(w)^2 X over `rows` rows (w may be NULL).
+spn_status normal_matrix(spn_newton* w, const float* X, int64_t ldx, const double* wt, int64_t rows, cudaStream_t s) {
+  const int d = (int)w->d;
+  const int T = (d + kST - 1) / kST, tiles = T * (T + 1) / 2;
+  int nsplit = std::max(1, std::min<int>(w->nsplit_max, (2 * w->sms + tiles - 1) / tiles));
+  nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, (rows + 255) / 256));
+  const int64_t per = ((rows + nsplit - 1) / nsplit + 31) / 32 * 32;
+  nsplit = (int)std::max<int64_t>(1, (rows + per - 1) / per);
+  syrk_partial_kernel<<<dim3(tiles, nsplit), 256, 0, s>>>(X, ldx, wt, rows, d, per, w->spart);
+  NWT_CUDA(cudaGetLastError());
+  const int64_t e = (int64_t)d * d;
+  syrk_reduce_kernel<<<(unsigned)((e + 255) / 256), 256, 0, s>>>(w->spart, nsplit, d, w->normal);
+  NWT_CUDA(cudaGetLastError());
+  return SPN_OK;
+}
+
+// fact = chol(normal); step = -(fact fact^T)^{-1} grad; returns the pivot flag (syncs s).
+spn_status factor_solve(spn_newton* w, const double* grad, double* step, cudaStream_t s, int* failed) {
+  const int d = (int)w->d;
+  NWT_CUDA(cudaMemcpyAsync(w->fact, w->normal, sizeof(double) * (size_t)d * d, cudaMemcpyDeviceToDevice, s));
+  NWT_CUDA(cudaMemsetAsync(w->flag, 0, sizeof(int), s));
+  for (int j0 = 0; j0 < d; j0 += kNB) {
+    chol_panel_kernel<<<1, 1024, 0, s>>>(w->fact, d, j0, w->flag);
+    NWT_CUDA(cudaGetLastError());
+    const int rest = d - j0 - kNB;
+    if (rest > 0) {
+      const int T = (rest + kNB - 1) / kNB;
+      chol_update_kernel<<<T * (T + 1) / 2, 256, 0, s>>>(w->fact, d, j0, w->flag);
+      NWT_CUDA(cudaGetLastError());
+    }
+  }
+  chol_solve_kernel<<<1, 1024, sizeof(double) * (size_t)d, s>>>(w->fact, d, grad, step, w->flag);
+  NWT_CUDA(cudaGetLastError());
+  NWT_CUDA(cudaMemcpyAsync(w->flag_h, w->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NWT_CUDA(cudaStreamSynchronize(s));
+  *failed = *w->flag_h;
+  return SPN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+spn_status spn_newton_create(spn_newton** out, int64_t n, int64_t d, int64_t max_sketch_rows, int device) {
+  if (!out) return fail(SPN_EINVAL, "null output");
+  *out = nullptr;
+  if (n < 1 || d < 1) return fail(SPN_EDIM, "LogisticProblem: empty data");
+  if (d > kMaxD) return fail(SPN_EUNSUPPORTED, "sketched Newton: d > 1024");
+  if (max_sketch_rows < 0) return fail(SPN_EDIM, "bad sketch row count");
+  DevGuard g(device);
+  auto* w = new spn_newton();
+  w->n = n;
+  w->d = d;
+  w->max_rows = max_sketch_rows;
+  w->device = device;
+  w->sms = sm_count(device);
+  w->grid = 2 * w->sms;
+  const int T = (int)((d + kST - 1) / kST), tiles = T * (T + 1) / 2;
+  w->nsplit_max = std::max(1, std::min<int>((2 * w->sms + tiles - 1) / tiles,
+                                            (int)((int64_t(256) << 20) / (8 * d * d))));
+  cudaError_t e = cudaSuccess;
+  auto al = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess && bytes) e = cudaMalloc(p, bytes);
+  };
+  al((void**)&w->part, sizeof(double) * (size_t)w->grid * (size_t)std::max<int64_t>(d + 1, 64));
+  al((void**)&w->margins, sizeof(double) * (size_t)n);
+  al((void**)&w->h32, sizeof(float) * (size_t)n);
+  al((void**)&w->h64, sizeof(double) * (size_t)n);
+  al((void**)&w->sb, sizeof(float) * (size_t)(max_sketch_rows * d));
+  al((void**)&w->spart, sizeof(double) * (size_t)w->nsplit_max * (size_t)(d * d));
+  al((void**)&w->normal, sizeof(double) * (size_t)(d * d));
+  al((void**)&w->fact, sizeof(double) * (size_t)(d * d));
+  al((void**)&w->grad, sizeof(double) * (size_t)d);
+  al((void**)&w->loss, sizeof(double));
+  al((void**)&w->flag, sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&w->flag_h, sizeof(int));
+  if (e != cudaSuccess) {
+    newton_free(w);
+    delete w;
+    return spn::cuda_error(e, "spn_newton_create");
+  }
+  *out = w;
+  return SPN_OK;
+}
+
+spn_status spn_newton_destroy(spn_newton* w) {
+  if (!w) return SPN_OK;
+  DevGuard g(w->device);
+  newton_free(w);
+  delete w;
+  return SPN_OK;
+}
+
+spn_status spn_logistic_eval_f32(spn_newton* w, const float* a, int64_t ld_a, const float* labels,
+                                 const double* x, double* loss, double* grad, void* stream) {
+  if (!w || !a || !labels || !x) return fail(SPN_EINVAL, "null pointer");
+  if (ld_a < w->d) return fail(SPN_EINVAL, "bad leading dimension");
+  DevGuard g(w->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  NWT_CUDA(launch_pass(w, a, ld_a, labels, x, true, s));
+  const int width = (int)w->d + 1;
+  reduce_parts_kernel<<<(width + 255) / 256, 256, 0, s>>>(w->part, w->grid, width, grad, loss, (int)w->d);
+  NWT_CUDA(cudaGetLastError());
+  return SPN_OK;
+}
+
+spn_status spn_hessian_sqrt_f32(spn_newton* w, const float* a, int64_t ld_a, const double* x, float* out,
+                                int64_t ld_out, void* stream) {
+  if (!w || !a || !x || !out) return fail(SPN_EINVAL, "null pointer");
+  if (ld_a < w->d || ld_out < w->d) return fail(SPN_EINVAL, "bad leading dimension");
+  DevGuard g(w->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  NWT_CUDA(launch_pass(w, a, ld_a, nullptr, x, false, s));
+  const int64_t total = w->n * w->d;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, int64_t(w->sms) * 16);
+  scale_rows_f32_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, ld_a, w->h64, w->n, (int)w->d, out, ld_out);
+  NWT_CUDA(cudaGetLastError());
+  return SPN_OK;
+}
+
+spn_status spn_sketched_step_f32(spn_newton* w, const spn_plan* sketch, int64_t rows, const float* a, int64_t ld_a,
+                                 const float* labels, const double* x, double* step, double* grad, double* loss,
+                                 void* stream) {
+  if (!w || !a || !labels || !x || !step) return fail(SPN_EINVAL, "null pointer");
+  if (ld_a < w->d) return fail(SPN_EINVAL, "bad leading dimension");
+  const int64_t m = sketch ? rows : w->n;
+  if (m < w->d) return fail(SPN_EDIM, "sketched_step: sketch dimension below d");
+  if (sketch && rows > w->max_rows) return fail(SPN_EDIM, "sketch rows exceed the workspace");
+  DevGuard g(w->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // gradient, loss, Hessian row scales at x (newton_sketch.cpp:105,110)
+  NWT_CUDA(launch_pass(w, a, ld_a, labels, x, true, s));
+  const int width = (int)w->d + 1;
+  reduce_parts_kernel<<<(width + 255) / 256, 256, 0, s>>>(w->part, w->grid, width, w->grad, w->loss, (int)w->d);
+  NWT_CUDA(cudaGetLastError());
+  if (grad) NWT_CUDA(cudaMemcpyAsync(grad, w->grad, sizeof(double) * (size_t)w->d, cudaMemcpyDeviceToDevice, s));
+  if (loss) NWT_CUDA(cudaMemcpyAsync(loss, w->loss, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  // normal matrix (S B)^T (S B)   (:106,109)
+  if (sketch) {
+    if (spn::plan_device(sketch) != w->device) return fail(SPN_EINVAL, "sketch plan on another device");
+    spn_status st = spn::plan_sketch_scaled(sketch, a, w->n, w->d, ld_a, rows, 1.0 / std::sqrt((double)rows),
+                                            w->h32, w->sb, w->d, s);
+    if (st) return st;
+    if (spn_status st2 = normal_matrix(w, w->sb, w->d, nullptr, rows, s)) return st2;
+  } else {
+    if (spn_status st2 = normal_matrix(w, a, ld_a, w->h64, w->n, s)) return st2;
+  }
+  // LLT, ridge retry, solve   (:112-121)
+  int failed = 0;
+  if (spn_status st = factor_solve(w, w->grad, step, s, &failed)) return st;
+  if (failed) {
+    ridge_kernel<<<1, 256, 0, s>>>(w->normal, (int)w->d);
+    NWT_CUDA(cudaGetLastError());
+    if (spn_status st = factor_solve(w, w->grad, step, s, &failed)) return st;
+    if (failed) return fail(SPN_ESINGULAR, "sketched_step: sketched Hessian is indefinite; sketch dimension too small");
+  }
+  return SPN_OK;
+}
+
+spn_status spn_logistic_line_f32(spn_newton* w, const float* a, int64_t ld_a, const float* labels, const double* x,
+                                 const double* step, double s0, int64_t count, double* losses, void* stream) {
+  if (!w || !a || !labels || !x || !step || !losses) return fail(SPN_EINVAL, "null pointer");
+  if (count < 1 || count > 64) return fail(SPN_EINVAL, "line search: 1 <= count <= 64");
+  if (ld_a < w->d) return fail(SPN_EINVAL, "bad leading dimension");
+  DevGuard g(w->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  NWT_CUDA(launch_line(w, a, ld_a, labels, x, step, s0, (int)count, s));
+  reduce_parts_kernel<<<1, 64, 0, s>>>(w->part, w->grid, (int)count, losses, nullptr, (int)count);
+  NWT_CUDA(cudaGetLastError());
+  return SPN_OK;
+}
+
+spn_status spn_ar1_problem(int64_t n, int64_t d, uint64_t seed, float* features, float* labels) {
+  if (n < 1 || d < 1) return fail(SPN_EDIM, "generate_ar1_problem: n, d must be >= 1");
+  if (!features || !labels) return fail(SPN_EINVAL, "null pointer");
+  // newton_sketch.cpp:185-204 with the reference generator (host_params.hpp HostRng)
+  const double rho = 0.99, noise = std::sqrt(1.0 - rho * rho);
+  spn::HostRng rng(spn::mix_seed(seed, 7));
+  for (int64_t i = 0; i < n; ++i) {
+    double prev = rng.gaussian();
+    features[i * d] = (float)prev;
+    for (int64_t j = 1; j < d; ++j) {
+      prev = rho * prev + noise * rng.gaussian();
+      features[i * d + j] = (float)prev;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) labels[i] = (float)rng.rademacher();
+  return SPN_OK;
+}
+
+}  // extern "C"

@@ -374,6 +374,7 @@ struct BigPlan {
   bool sk_ready = false;
   int sk_lsa = 0, sk_lsb = 0;
   float* sk_d[3] = {nullptr, nullptr, nullptr};
+  float* sk_d1s = nullptr;  // D1 * row scale (Newton step), lazily allocated
   // scratch
   float* work = nullptr;
   size_t work_bytes = 0;
@@ -396,6 +397,8 @@ struct BigPlan {
       if (q) cudaFree(q);
       q = nullptr;
     }
+    if (sk_d1s) cudaFree(sk_d1s);
+    sk_d1s = nullptr;
     if (drow2) cudaFree(drow2);
     for (float** q : {&srow1, &srow3, &stile2}) {
       if (*q) cudaFree(*q);
@@ -697,13 +700,33 @@ struct BigPlan {
   }
 };
 
+// D1 with a per-row scale folded in (the Newton step's B = diag(h) A, newton_sketch.cpp:63-72,
+// sketched in the first pass without materialising B).
+__global__ void scale_rows_kernel(const float* __restrict__ d1, const float* __restrict__ h, int64_t n_in,
+                                  int64_t nn, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i < n_in ? d1[i] * h[i] : 0.0f;
+}
+
 inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int* /*dsign*/,
                              const float* a, int64_t n_in, int64_t dcols, int64_t ld_a,
                              const int64_t* rows, int64_t m_out, double cscale, float* out,
-                             int64_t ld_out, int sms, cudaStream_t s0, BigPlan* bp) {
+                             int64_t ld_out, int sms, cudaStream_t s0, BigPlan* bp,
+                             const float* row_scale = nullptr) {
   std::lock_guard<std::mutex> lock(bp->mu);
   if (spn_status st = bp->build_sketch(nn, d)) return st;
   if (spn_status st = bp->set_rowmap(nn, rows, m_out, s0)) return st;
+  const float* d1 = bp->sk_d[0];
+  if (row_scale) {
+    cudaError_t e = cudaSuccess;
+    if (!bp->sk_d1s) e = cudaMalloc(&bp->sk_d1s, static_cast<size_t>(nn) * 4);
+    if (e != cudaSuccess) return BigPlan::err(e, "scaled D1");
+    const int64_t blocks = std::min<int64_t>((nn + 255) / 256, int64_t(sms) * 8);
+    scale_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, s0>>>(bp->sk_d[0], row_scale, n_in, nn, bp->sk_d1s);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return BigPlan::err(e, "scaled D1");
+    d1 = bp->sk_d1s;
+  }
   cudaStream_t s = s0;
   const int lsa = bp->sk_lsa, lsb = bp->sk_lsb;
   // pipelined (cp.async double-buffered) column passes when both bit ranges fit them
@@ -730,7 +753,7 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     cp.s0 = 0;
     cp.nhi = 1;
     cp.nlo = 1;
-    cp.dd[0] = bp->sk_d[0];
+    cp.dd[0] = d1;
     cp.dd[1] = bp->sk_d[1];
     cp.dd[2] = bp->sk_d[2];
     cp.rowmap = bp->rowmap;
@@ -766,7 +789,7 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     pa.src_valid = n_in * ld_a;
     pa.dst = W;
     pa.dst_ld = dc;
-    pa.dd[0] = bp->sk_d[0];
+    pa.dd[0] = d1;
     cudaError_t e = lcol(lsa, CP_FIRST, pa);
     if (e != cudaSuccess) return BigPlan::err(e, "sketch P1");
     // P2: H(high), D2, H(high)

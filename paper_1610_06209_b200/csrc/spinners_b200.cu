@@ -17,6 +17,7 @@
 
 #include "errors.hpp"
 #include "host_params.hpp"
+#include "internal.hpp"
 #include "spinner_big.cuh"
 #include "spinner_vec.cuh"
 #include "vec_launch.cuh"
@@ -263,6 +264,7 @@ const char* spn_status_string(spn_status s) {
     case SPN_ENOMEM: return "out of memory";
     case SPN_EUNSUPPORTED: return "unsupported";
     case SPN_EINVAL: return "invalid argument";
+    case SPN_ESINGULAR: return "singular system";
   }
   return "unknown status";
 }
@@ -485,6 +487,25 @@ spn_status spn_sketch_f32(const spn_plan* p, const float* a, int64_t n_in, int64
 // --------------------------------------------------------------------- host-buffer API
 
 }  // extern "C"
+
+namespace spn {
+
+int plan_device(const spn_plan* p) { return p->device; }
+
+// First-m sketch of diag(row_scale) A (the Newton step's S * hessian_sqrt, newton_sketch.cpp:87-106).
+spn_status plan_sketch_scaled(const spn_plan* p, const float* a, int64_t n_in, int64_t d, int64_t ld_a,
+                              int64_t m_out, double norm, const float* row_scale, float* out, int64_t ld_out,
+                              cudaStream_t s) {
+  if (p->tables != 1 || p->blocks != 1) return fail(SPN_EUNSUPPORTED, "sketch needs one table of one block");
+  if (n_in < 1 || n_in > p->n) return fail(SPN_EDIM, "SketchOperator::apply: row count mismatch");
+  if (m_out > p->k || m_out > p->n) return fail(SPN_EDIM, "sketch rows exceed the plan");
+  DeviceGuard g(p->device);
+  return sketch_run(p->n, p->d, p->dsign, a, n_in, d, ld_a, nullptr, m_out,
+                    p->scale * std::pow(static_cast<double>(p->n), -1.5) * norm, out, ld_out, p->sms, s,
+                    const_cast<BigPlan*>(&p->big), row_scale);
+}
+
+}  // namespace spn
 
 namespace {
 
