@@ -45,6 +45,9 @@ CONFIGS = {
                         "random rows", N=1 << 17, d=256, m=2048, bytes_per_vec=(1 << 17) * 4 + 2048 * 4, flush=True),
     "c5": dict(workload="BASELINE configs[4]: ReLU(H D3 H D2 H D1 x), Gaussian D's, 256 x n=2^20",
                n=1 << 20, batch=256, bytes_per_vec=(1 << 20) * 8, flush=False),
+    "c6": dict(workload="SURVEY 8(f) rank 1: one sketched Newton iteration of solve() (fresh HD3 SketchOperator, "
+                        "sketched_step, Armijo line search) for logistic regression on A = 131072 x 256, m = 2048",
+               N=1 << 17, d=256, m=2048, bytes_per_vec=(1 << 17) * 4 * 6, flush=False),
 }
 
 
@@ -187,6 +190,18 @@ class Workload:
             groups = math.ceil(cfg["d"] / max(32, ((32 << 20) // (cfg["N"] * 4)) // 32 * 32))
             self.launches_per_step = 4 * groups
             del lsa
+        elif name == "c6":
+            from paper_1610_06209_b200 import newton
+            self.newton = newton
+            f = torch.randn((cfg["N"], cfg["d"]), device="cuda", generator=g)
+            y = torch.where(torch.rand(cfg["N"], device="cuda", generator=g) < 0.5, -1.0, 1.0)
+            self.prob = spn.LogisticProblem(f, y)
+            self.prob.workspace(cfg["m"])
+            self.xk = torch.full((cfg["d"],), 0.01, dtype=torch.float64, device="cuda")
+            self.vectors = cfg["d"]  # columns sketched per iteration
+            self.t = 0
+            # pass over A + 4 sketch passes + line-search pass per iteration (launch count is a lower bound)
+            self.launches_per_step = 16
         elif name == "c5":
             self.sp = spn.StackedSpinner(V.gauss3, cfg["n"], cfg["n"], cfg["n"], 13 + rank, scale=1.0)
             self.x = torch.randn((cfg["batch"], cfg["n"]), device="cuda", generator=g)
@@ -205,6 +220,16 @@ class Workload:
             return self.h.plan.hash(self.x, stream=stream)
         if self.name == "c4":
             return self.sk.apply(self.x, out=self.out, stream=stream)
+        if self.name == "c6":  # newton_sketch.cpp:155-170, one iteration
+            cfg, nt = self.cfg, self.newton
+            sk = self.spn.SketchOperator(self.spn.SpinnerVariant.hd3_hd2_hd1, cfg["N"], cfg["m"],
+                                         self.spn.mix_seed(3, self.t))
+            self.t += 1
+            step, g, f = nt._step_dev(self.prob, self.xk, sk, stream)
+            slope = float(self.torch.dot(g, step).item())
+            s, _ = nt._backtrack(self.prob, self.xk, step, float(f.item()), slope, stream)
+            self.xk = self.xk + s * step
+            return self.xk
         return self.sp.apply(self.x, relu=True, out=self.y, stream=stream)
 
 
@@ -352,6 +377,14 @@ def cpu_reference(config, budget_s=20.0, threads=None):
                                 threads=threads)
         total = cfg["d"]
         what = "SketchOperator::apply restated over the reference StackedSpinner, random P"
+    elif config == "c6":  # one reference sketched_step (newton_sketch.cpp:103-122, single-threaded code)
+        a = rng.standard_normal((cfg["N"], cfg["d"])).astype(np.float32).astype(np.float64)
+        y = np.where(rng.random(cfg["N"]) < 0.5, -1.0, 1.0)
+        x = np.full(cfg["d"], 0.01)
+        dt = timed(lambda c: r.sketched_step(a, y, x, HD3, cfg["m"], o.mix_seed(3, 0)), 1)
+        return cfg["d"] / dt, {"kind": "reference", "cores": 1,
+                               "sample": "1 sketched_step (131072 x 256, m = 2048, HD3) of c6 = 256 sketched "
+                                         "columns; the reference's newton_sketch.cpp, single-threaded"}
     else:
         n = cfg["n"]
         d = [a[0].astype(np.float32).astype(np.float64) for a in o.realize(100, n, n, n, 13)]

@@ -43,6 +43,17 @@ __device__ __forceinline__ double sigmoid(double t) {  // newton_sketch.cpp:17-2
   return e / (1.0 + e);
 }
 
+// Streaming loads that stay batched: ptxas otherwise places each F2F.F64.F32 right after
+// its load, and the warp then waits out every load's latency in turn.  The loads are
+// volatile asm (kept in order), and a second volatile "touch" of every loaded register
+// pins all conversions after the last load has been issued.
+__device__ __forceinline__ float ldg_stream(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void pin(float& v) { asm volatile("" : "+f"(v)); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -50,9 +61,23 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ------------------------------------------------------------- pass over A
-// Warp-per-row: lane l holds columns l, l+32, ... (DCH chunks).  Per row:
-// m = a.x (fp64), loss += log1p_exp(-y m), g += (sigmoid(y m) - 1) y a,
-// h = sqrt(s (1 - s)) with s = sigmoid(m).  Per-CTA partials [grid][d+1] (loss last).
+// A warp takes RPI = 8 rows per iteration (all loads issued before any math, 8 KB in
+// flight per warp at d = 256); lane l holds columns l, l+32, ... (DCH chunks).  The
+// per-row scalars run one row per lane (lane q < 8): with e = exp(-|m|) shared by
+// sigmoid(m) and sigmoid(y m) (bit-identical to evaluating both, y = +-1),
+//   loss += log1p_exp(-y m), w = (sigmoid(y m) - 1) y, h = sqrt(s (1 - s)), s = sigmoid(m),
+// then g += w a (lane-parallel over columns).  Per-CTA partials [grid][d+1] (loss last).
+constexpr int kRPI = 8;
+
+__device__ __forceinline__ double sigmoid_e(double t, double e) {  // e = exp(-|t|)
+  return t >= 0.0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
+}
+
+template <int DCH>
+struct PassCfg {  // rows per warp iteration: 8 KB of loads in flight, <= 64 data registers
+  static constexpr int RPI = DCH <= 8 ? kRPI : 64 / DCH;
+};
+
 template <int DCH>
 __global__ void __launch_bounds__(kPassThreads) logistic_pass_kernel(const float* __restrict__ a, int64_t ld,
                                                                      const float* __restrict__ labels,
@@ -71,35 +96,60 @@ __global__ void __launch_bounds__(kPassThreads) logistic_pass_kernel(const float
     xr[c] = col < d ? x[col] : 0.0;
     g[c] = 0.0;
   }
+  constexpr int RPI = PassCfg<DCH>::RPI;
   double lsum = 0.0;
-  for (int64_t r = (int64_t)blockIdx.x * (kPassThreads / 32) + wid; r < n; r += nw) {
-    const float* row = a + r * ld;
-    float av[DCH];
+  for (int64_t r0 = ((int64_t)blockIdx.x * (kPassThreads / 32) + wid) * RPI; r0 < n; r0 += nw * RPI) {
+    float av[RPI][DCH];
 #pragma unroll
-    for (int c = 0; c < DCH; ++c) {
-      const int col = c * 32 + lane;
-      av[c] = col < d ? __ldg(row + col) : 0.0f;
+    for (int q = 0; q < RPI; ++q) {
+      const float* row = a + (r0 + q) * ld;
+#pragma unroll
+      for (int c = 0; c < DCH; ++c) {
+        const int col = c * 32 + lane;
+        av[q][c] = (r0 + q < n && col < d) ? ldg_stream(row + col) : 0.0f;
+      }
     }
-    double dot = 0.0;
 #pragma unroll
-    for (int c = 0; c < DCH; ++c) dot = fma((double)av[c], xr[c], dot);
-    const double m = warp_sum(dot);
-    if (labels) {
-      const double y = (double)__ldg(labels + r);
-      lsum += log1p_exp(-y * m);
-      const double w = (sigmoid(y * m) - 1.0) * y;
+    for (int q = 0; q < RPI; ++q)
 #pragma unroll
-      for (int c = 0; c < DCH; ++c) g[c] = fma(w, (double)av[c], g[c]);
+      for (int c = 0; c < DCH; ++c) pin(av[q][c]);
+    double mine = 0.0;  // lane q < RPI: margin of row r0 + q
+#pragma unroll
+    for (int q = 0; q < RPI; ++q) {
+      double dot = 0.0;
+#pragma unroll
+      for (int c = 0; c < DCH; ++c) dot = fma((double)av[q][c], xr[c], dot);
+      const double m = warp_sum(dot);
+      if (lane == q) mine = m;
     }
-    if (lane == 0) {
+    const int64_t r = r0 + lane;
+    double w = 0.0;
+    if (lane < RPI && r < n) {
+      const double m = mine;
+      const double e = exp(-fabs(m));
+      if (labels) {
+        const double y = (double)__ldg(labels + r);
+        const double t = -y * m;
+        lsum += log1p_exp(t);
+        w = (sigmoid_e(y * m, e) - 1.0) * y;
+      }
+      const double sg = sigmoid_e(m, e);
+      const double h = sqrt(sg * (1.0 - sg));
       if (margins) margins[r] = m;
-      const double s = sigmoid(m);
-      const double h = sqrt(s * (1.0 - s));
       if (h32) h32[r] = (float)h;
       if (h64) h64[r] = h;
     }
+    if (labels) {
+#pragma unroll
+      for (int q = 0; q < RPI; ++q) {
+        const double wq = __shfl_sync(0xffffffffu, w, q);
+#pragma unroll
+        for (int c = 0; c < DCH; ++c) g[c] = fma(wq, (double)av[q][c], g[c]);
+      }
+    }
   }
   if (!part) return;
+  lsum = warp_sum(lsum);
   // ordered block reduction: warp 0, then 1, ... into smem
   for (int i = threadIdx.x; i <= d; i += kPassThreads) red[i] = 0.0;
   __syncthreads();
@@ -117,17 +167,26 @@ __global__ void __launch_bounds__(kPassThreads) logistic_pass_kernel(const float
   for (int i = threadIdx.x; i <= d; i += kPassThreads) part[(int64_t)blockIdx.x * (d + 1) + i] = red[i];
 }
 
-// out[j] = sum_b part[b][j] (fixed order); j == d is the loss.
-__global__ void reduce_parts_kernel(const double* __restrict__ part, int nparts, int width,
-                                    double* __restrict__ grad, double* __restrict__ loss, int d) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= width) return;
+// out[j] = sum_b part[b][j]: one CTA per column, strided partial sums + a fixed tree.
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const double* __restrict__ part, int nparts, int width,
+                                                           double* __restrict__ grad, double* __restrict__ loss,
+                                                           int d) {
+  __shared__ double sh[256];
+  const int j = blockIdx.x;
   double s = 0.0;
-  for (int b = 0; b < nparts; ++b) s += part[(int64_t)b * width + j];
-  if (j < d) {
-    if (grad) grad[j] = s;
-  } else if (loss) {
-    *loss = s;
+  for (int b = threadIdx.x; b < nparts; b += 256) s += part[(int64_t)b * width + j];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (j < d) {
+      if (grad) grad[j] = sh[0];
+    } else if (loss) {
+      *loss = sh[0];
+    }
   }
 }
 
@@ -214,63 +273,88 @@ __global__ void syrk_reduce_kernel(const double* __restrict__ part, int nsplit, 
 }
 
 // ------------------------------------------------------------- Cholesky (lower, in place)
-// Panel j0: factor the nb x nb diagonal block in smem (right-looking inside the panel,
-// so every element sees its subtractions in column order, like the unblocked LLT),
-// then each thread solves one row of the sub-diagonal panel L21 = A21 L11^{-T}.
-// A non-positive pivot sets *flag (Eigen's LLT NumericalIssue).
-__global__ void __launch_bounds__(1024) chol_panel_kernel(double* __restrict__ A, int d, int j0,
-                                                          int* __restrict__ flag) {
-  __shared__ double L[kNB][kNB + 1];
+// Panel j0: warp 0 factors the nb x nb diagonal block in registers (lane r = row r,
+// right-looking with shuffles, so every element sees its subtractions in column order,
+// like the unblocked LLT); every other thread meanwhile holds one sub-diagonal row and
+// then solves L21 = A21 L11^{-T} against L11 in smem.  A non-positive pivot sets *flag
+// (Eigen's LLT NumericalIssue).
+constexpr int kPanelThreads = 256;
+
+// Compact code on purpose: the factorisation is a chain of nb dependent pivots, and an
+// unrolled version (shuffles, 32 x 32 registers) measured 80 us per panel in instruction
+// fetch (one warp streams ~48 KB of SASS once per panel).  Here every step is one
+// barrier-separated parallel update over the (r, j) pairs of the 32 x 32 block (four
+// pairs per thread); the sub-diagonal rows (one per thread per round) are solved after.
+__global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __restrict__ A, int d, int j0,
+                                                                   int* __restrict__ flag) {
+  __shared__ double L11[kNB][kNB + 1];
+  __shared__ double lkk_s;
   __shared__ int bad;
   if (*flag) return;
   const int nb = min(kNB, d - j0);
   const int tid = threadIdx.x;
+  const int rq = tid >> 5, j = tid & 31;  // (row rq + 8 q, column j) pairs of the diagonal block
   if (tid == 0) bad = 0;
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    const int i = e / nb, j = e - i * nb;
-    L[i][j] = i >= j ? A[(int64_t)(j0 + i) * d + j0 + j] : 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = rq + 8 * q;
+    if (r < nb && j <= r) L11[r][j] = A[(int64_t)(j0 + r) * d + j0 + j];
   }
   __syncthreads();
   for (int k = 0; k < nb; ++k) {
     if (tid == 0) {
-      const double p = L[k][k];
-      if (!(p > 0.0))
+      const double p = L11[k][k];
+      if (!(p > 0.0)) {
         bad = 1;
-      else
-        L[k][k] = sqrt(p);
+      } else {
+        lkk_s = sqrt(p);
+        L11[k][k] = lkk_s;
+      }
     }
     __syncthreads();
-    if (bad) {
-      if (tid == 0) *flag = 1;
-      return;
+    if (bad) break;
+    if (j == k) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = rq + 8 * q;
+        if (r > k && r < nb) L11[r][k] /= lkk_s;
+      }
     }
-    if (tid > k && tid < nb) L[tid][k] /= L[k][k];
     __syncthreads();
-    for (int e = tid; e < nb * nb; e += blockDim.x) {
-      const int i = e / nb, j = e - i * nb;
-      if (j > k && i >= j) L[i][j] -= L[i][k] * L[j][k];
+    if (j > k) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = rq + 8 * q;
+        if (r >= j && r < nb) L11[r][j] -= L11[r][k] * L11[j][k];
+      }
     }
     __syncthreads();
   }
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    const int i = e / nb, j = e - i * nb;
-    if (i >= j) A[(int64_t)(j0 + i) * d + j0 + j] = L[i][j];
+  if (bad) {
+    if (tid == 0) *flag = 1;
+    return;
   }
-  // rows below the panel
-  for (int i = j0 + nb + tid; i < d; i += blockDim.x) {
-    double* row = A + (int64_t)i * d + j0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = rq + 8 * q;
+    if (r < nb && j <= r) A[(int64_t)(j0 + r) * d + j0 + j] = L11[r][j];
+  }
+  for (int i = j0 + nb + tid; i < d; i += kPanelThreads) {
     double l[kNB];
+#pragma unroll
+    for (int k = 0; k < kNB; ++k) l[k] = k < nb ? A[(int64_t)i * d + j0 + k] : 0.0;
 #pragma unroll
     for (int k = 0; k < kNB; ++k) {
       if (k < nb) {
-        double s = row[k];
-        for (int m = 0; m < k; ++m) s -= l[m] * L[k][m];
-        l[k] = s / L[k][k];
+        double sum = l[k];
+#pragma unroll
+        for (int m = 0; m < k; ++m) sum -= l[m] * L11[k][m];
+        l[k] = sum / L11[k][k];
       }
     }
 #pragma unroll
     for (int k = 0; k < kNB; ++k)
-      if (k < nb) row[k] = l[k];
+      if (k < nb) A[(int64_t)i * d + j0 + k] = l[k];
   }
 }
 
@@ -305,29 +389,80 @@ __global__ void __launch_bounds__(256) chol_update_kernel(double* __restrict__ A
   }
 }
 
-// step = -(L L^T)^{-1} grad: forward then backward substitution (one CTA).
-__global__ void __launch_bounds__(1024) chol_solve_kernel(const double* __restrict__ L, int d,
-                                                          const double* __restrict__ grad, double* __restrict__ step,
-                                                          const int* __restrict__ flag) {
-  extern __shared__ double b[];
+// step = -(L L^T)^{-1} grad, blocked by 32: each 32 x 32 diagonal block is staged in smem
+// and solved by warp 0 (a shuffle per row, compact loop), then all threads apply the block
+// to the remaining entries (one barrier pair per block instead of per row).
+__global__ void __launch_bounds__(256) chol_solve_kernel(const double* __restrict__ L, int d,
+                                                         const double* __restrict__ grad, double* __restrict__ step,
+                                                         const int* __restrict__ flag) {
+  extern __shared__ double b[];  // [d]
+  __shared__ double T[32][33];
   if (*flag) return;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) b[i] = -grad[i];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < d; i += blockDim.x) b[i] = -grad[i];
   __syncthreads();
-  for (int k = 0; k < d; ++k) {
-    const double yk = b[k] / L[(int64_t)k * d + k];
+  // forward: L y = b
+  for (int kb = 0; kb < d; kb += 32) {
+    const int nb = min(32, d - kb);
+    for (int e = tid; e < 32 * 32; e += blockDim.x) {
+      const int rr = e >> 5, cc = e & 31;
+      T[rr][cc] = (rr < nb && cc <= rr) ? L[(int64_t)(kb + rr) * d + kb + cc] : 0.0;
+    }
     __syncthreads();
-    if (threadIdx.x == 0) b[k] = yk;
-    for (int i = k + 1 + threadIdx.x; i < d; i += blockDim.x) b[i] -= L[(int64_t)i * d + k] * yk;
+    if (tid < 32) {
+      double y = lane < nb ? b[kb + lane] : 0.0;
+      for (int k = 0; k < nb; ++k) {
+        if (lane == k) y = y / T[k][k];
+        const double yk = __shfl_sync(0xffffffffu, y, k);
+        if (lane > k) y -= T[lane][k] * yk;
+      }
+      if (lane < nb) b[kb + lane] = y;
+    }
+    __syncthreads();
+    for (int i = kb + nb + tid; i < d; i += blockDim.x) {
+      const double* li = L + (int64_t)i * d + kb;
+      double lv[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) lv[c] = c < nb ? li[c] : 0.0;  // all 32 loads in flight
+      double sum = b[i];
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (c < nb) sum -= lv[c] * b[kb + c];
+      b[i] = sum;
+    }
     __syncthreads();
   }
-  for (int i = d - 1; i >= 0; --i) {
-    const double xi = b[i] / L[(int64_t)i * d + i];
+  // backward: L^T x = y
+  for (int ke = d; ke > 0; ke -= 32) {
+    const int kb = max(0, ke - 32), nb = ke - kb;
+    for (int e = tid; e < 32 * 32; e += blockDim.x) {
+      const int rr = e >> 5, cc = e & 31;
+      T[rr][cc] = (rr < nb && cc <= rr) ? L[(int64_t)(kb + rr) * d + kb + cc] : 0.0;
+    }
     __syncthreads();
-    if (threadIdx.x == 0) b[i] = xi;
-    for (int k = threadIdx.x; k < i; k += blockDim.x) b[k] -= L[(int64_t)i * d + k] * xi;
+    if (tid < 32) {
+      double xv = lane < nb ? b[kb + lane] : 0.0;
+      for (int k = nb - 1; k >= 0; --k) {
+        if (lane == k) xv = xv / T[k][k];
+        const double xk = __shfl_sync(0xffffffffu, xv, k);
+        if (lane < k) xv -= T[k][lane] * xk;
+      }
+      if (lane < nb) b[kb + lane] = xv;
+    }
+    __syncthreads();
+    for (int i = tid; i < kb; i += blockDim.x) {
+      double lv[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) lv[c] = c < nb ? L[(int64_t)(kb + c) * d + i] : 0.0;
+      double sum = b[i];
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (c < nb) sum -= lv[c] * b[kb + c];
+      b[i] = sum;
+    }
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < d; i += blockDim.x) step[i] = b[i];
+  for (int i = tid; i < d; i += blockDim.x) step[i] = b[i];
 }
 
 // normal_jj += 1e-10 * trace(normal)   (newton_sketch.cpp:114-115)
@@ -343,14 +478,16 @@ __global__ void ridge_kernel(double* __restrict__ normal, int d) {
 }
 
 // ------------------------------------------------------------- line search
-// losses[k] = sum_r log1p_exp(-y_r (a_r.x + s_k a_r.step)), s_k = s0 * 2^-k; lanes own candidates.
+// losses[k] = sum_r log1p_exp(-y_r (a_r.x + s_k a_r.step)), s_k = s0 * 2^-k.  Rows are read
+// 8 per warp iteration; lane (q, k) = row q, candidate k when count <= 4 (one transcendental
+// per lane per 8 rows), otherwise lane k (and k + 32) for every row.
 template <int DCH>
 __global__ void __launch_bounds__(kPassThreads) line_kernel(const float* __restrict__ a, int64_t ld,
                                                             const float* __restrict__ labels,
                                                             const double* __restrict__ x,
                                                             const double* __restrict__ step, int64_t n, int d,
                                                             double s0, int count, double* __restrict__ part) {
-  __shared__ double red[64];
+  __shared__ double red[kPassThreads / 32][64];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t nw = (int64_t)gridDim.x * (kPassThreads / 32);
   double xr[DCH], pr[DCH];
@@ -360,33 +497,74 @@ __global__ void __launch_bounds__(kPassThreads) line_kernel(const float* __restr
     xr[c] = col < d ? x[col] : 0.0;
     pr[c] = col < d ? step[col] : 0.0;
   }
-  const double sA = s0 * exp2(-(double)lane), sB = s0 * exp2(-(double)(lane + 32));
+  const bool pairs = count <= 4;
+  const int kA = pairs ? (lane & 3) : lane;
+  const double sA = s0 * exp2(-(double)kA), sB = s0 * exp2(-(double)(lane + 32));
   double accA = 0.0, accB = 0.0;
-  for (int64_t r = (int64_t)blockIdx.x * (kPassThreads / 32) + wid; r < n; r += nw) {
-    const float* row = a + r * ld;
-    double dm = 0.0, dq = 0.0;
+  for (int64_t r0 = ((int64_t)blockIdx.x * (kPassThreads / 32) + wid) * kRPI; r0 < n; r0 += nw * kRPI) {
+    double mq = 0.0, qq = 0.0;  // pairs mode: this lane's row (lane >> 2)
+    double mm[kRPI], qv[kRPI];
+    float av[kRPI][DCH];
 #pragma unroll
-    for (int c = 0; c < DCH; ++c) {
-      const int col = c * 32 + lane;
-      const double v = col < d ? (double)__ldg(row + col) : 0.0;
-      dm = fma(v, xr[c], dm);
-      dq = fma(v, pr[c], dq);
+    for (int q = 0; q < kRPI; ++q) {
+      const float* row = a + (r0 + q) * ld;
+#pragma unroll
+      for (int c = 0; c < DCH; ++c) {
+        const int col = c * 32 + lane;
+        av[q][c] = (r0 + q < n && col < d) ? ldg_stream(row + col) : 0.0f;
+      }
     }
-    const double m = warp_sum(dm), q = warp_sum(dq);
-    const double y = (double)__ldg(labels + r);
-    if (lane < count) accA += log1p_exp(-y * (m + sA * q));
-    if (lane + 32 < count) accB += log1p_exp(-y * (m + sB * q));
+#pragma unroll
+    for (int q = 0; q < kRPI; ++q)
+#pragma unroll
+      for (int c = 0; c < DCH; ++c) pin(av[q][c]);
+#pragma unroll
+    for (int q = 0; q < kRPI; ++q) {
+      double dm = 0.0, dq = 0.0;
+#pragma unroll
+      for (int c = 0; c < DCH; ++c) {
+        const double v = (double)av[q][c];
+        dm = fma(v, xr[c], dm);
+        dq = fma(v, pr[c], dq);
+      }
+      mm[q] = warp_sum(dm);
+      qv[q] = warp_sum(dq);
+      if ((lane >> 2) == q) {
+        mq = mm[q];
+        qq = qv[q];
+      }
+    }
+    if (pairs) {
+      const int64_t r = r0 + (lane >> 2);
+      if (kA < count && r < n) {
+        const double y = (double)__ldg(labels + r);
+        accA += log1p_exp(-y * (mq + sA * qq));
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kRPI; ++q) {
+        if (r0 + q >= n) break;
+        const double y = (double)__ldg(labels + r0 + q);
+        if (lane < count) accA += log1p_exp(-y * (mm[q] + sA * qv[q]));
+        if (lane + 32 < count) accB += log1p_exp(-y * (mm[q] + sB * qv[q]));
+      }
+    }
   }
-  if (threadIdx.x < 64) red[threadIdx.x] = 0.0;
+  red[wid][lane] = accA;
+  red[wid][lane + 32] = accB;
   __syncthreads();
-  for (int w = 0; w < kPassThreads / 32; ++w) {
-    if (wid == w) {
-      red[lane] += accA;
-      red[lane + 32] += accB;
+  if (threadIdx.x < count) {
+    const int k = threadIdx.x;
+    double s = 0.0;
+    for (int w = 0; w < kPassThreads / 32; ++w) {
+      if (pairs) {
+        for (int q = 0; q < kRPI; ++q) s += red[w][q * 4 + k];
+      } else {
+        s += red[w][k];
+      }
     }
-    __syncthreads();
+    part[(int64_t)blockIdx.x * count + k] = s;
   }
-  if (threadIdx.x < count) part[(int64_t)blockIdx.x * count + threadIdx.x] = red[threadIdx.x];
 }
 
 int sm_count(int dev) {
@@ -502,7 +680,7 @@ spn_status factor_solve(spn_newton* w, const double* grad, double* step, cudaStr
   NWT_CUDA(cudaMemcpyAsync(w->fact, w->normal, sizeof(double) * (size_t)d * d, cudaMemcpyDeviceToDevice, s));
   NWT_CUDA(cudaMemsetAsync(w->flag, 0, sizeof(int), s));
   for (int j0 = 0; j0 < d; j0 += kNB) {
-    chol_panel_kernel<<<1, 1024, 0, s>>>(w->fact, d, j0, w->flag);
+    chol_panel_kernel<<<1, kPanelThreads, 0, s>>>(w->fact, d, j0, w->flag);
     NWT_CUDA(cudaGetLastError());
     const int rest = d - j0 - kNB;
     if (rest > 0) {
@@ -511,7 +689,7 @@ spn_status factor_solve(spn_newton* w, const double* grad, double* step, cudaStr
       NWT_CUDA(cudaGetLastError());
     }
   }
-  chol_solve_kernel<<<1, 1024, sizeof(double) * (size_t)d, s>>>(w->fact, d, grad, step, w->flag);
+  chol_solve_kernel<<<1, 256, sizeof(double) * (size_t)d, s>>>(w->fact, d, grad, step, w->flag);
   NWT_CUDA(cudaGetLastError());
   NWT_CUDA(cudaMemcpyAsync(w->flag_h, w->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   NWT_CUDA(cudaStreamSynchronize(s));
@@ -581,7 +759,7 @@ spn_status spn_logistic_eval_f32(spn_newton* w, const float* a, int64_t ld_a, co
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   NWT_CUDA(launch_pass(w, a, ld_a, labels, x, true, s));
   const int width = (int)w->d + 1;
-  reduce_parts_kernel<<<(width + 255) / 256, 256, 0, s>>>(w->part, w->grid, width, grad, loss, (int)w->d);
+  reduce_parts_kernel<<<width, 256, 0, s>>>(w->part, w->grid, width, grad, loss, (int)w->d);
   NWT_CUDA(cudaGetLastError());
   return SPN_OK;
 }
@@ -613,7 +791,7 @@ spn_status spn_sketched_step_f32(spn_newton* w, const spn_plan* sketch, int64_t 
   // gradient, loss, Hessian row scales at x (newton_sketch.cpp:105,110)
   NWT_CUDA(launch_pass(w, a, ld_a, labels, x, true, s));
   const int width = (int)w->d + 1;
-  reduce_parts_kernel<<<(width + 255) / 256, 256, 0, s>>>(w->part, w->grid, width, w->grad, w->loss, (int)w->d);
+  reduce_parts_kernel<<<width, 256, 0, s>>>(w->part, w->grid, width, w->grad, w->loss, (int)w->d);
   NWT_CUDA(cudaGetLastError());
   if (grad) NWT_CUDA(cudaMemcpyAsync(grad, w->grad, sizeof(double) * (size_t)w->d, cudaMemcpyDeviceToDevice, s));
   if (loss) NWT_CUDA(cudaMemcpyAsync(loss, w->loss, sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -647,7 +825,7 @@ spn_status spn_logistic_line_f32(spn_newton* w, const float* a, int64_t ld_a, co
   DevGuard g(w->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   NWT_CUDA(launch_line(w, a, ld_a, labels, x, step, s0, (int)count, s));
-  reduce_parts_kernel<<<1, 64, 0, s>>>(w->part, w->grid, (int)count, losses, nullptr, (int)count);
+  reduce_parts_kernel<<<(unsigned)count, 256, 0, s>>>(w->part, w->grid, (int)count, losses, nullptr, (int)count);
   NWT_CUDA(cudaGetLastError());
   return SPN_OK;
 }

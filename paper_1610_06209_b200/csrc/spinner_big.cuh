@@ -354,6 +354,45 @@ inline int64_t group_bytes() {
   return v;
 }
 
+// Stream-ordered scratch (cudaMallocFromPoolAsync / cudaFreeAsync) from one pool per device
+// that keeps its memory (release threshold = max): per-call workspaces cost no cudaMalloc /
+// device-synchronising cudaFree, which matters when plans are short-lived (a fresh sketch
+// per Newton iteration).
+inline cudaMemPool_t scratch_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    uint64_t keep = ~uint64_t(0);
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  return pools[dev];
+}
+
+struct Scratch {  // freed (stream-ordered) on `s` when the scope ends
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t alloc(size_t bytes, cudaStream_t st) {
+    s = st;
+    cudaMemPool_t pool = scratch_pool();
+    if (!pool) return cudaErrorMemoryAllocation;
+    return cudaMallocFromPoolAsync(&p, bytes, pool, st);
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
 inline int ilog2_i(int64_t n) {
   int l = 0;
   while ((int64_t(1) << l) < n) ++l;
@@ -514,10 +553,20 @@ struct BigPlan {
     return f;
   }
 
+  // The apply layouts are built on first use: sketch-only plans (a fresh SketchOperator per
+  // Newton iteration, newton_sketch.cpp:155-157) never pay for them.
+  const std::vector<double>* dsrc = nullptr;
+  bool built = false;
   spn_status build(int64_t n_, int64_t tb_, const std::vector<double>* d, const int*) {
     n = n_;
     tb = tb_;
     L = ilog2_i(n);
+    dsrc = d;
+    return SPN_OK;
+  }
+  spn_status build_now() {
+    if (built) return SPN_OK;
+    const std::vector<double>* d = dsrc;
     std::vector<float> f(static_cast<size_t>(tb * n));
     for (int di = 0; di < 3; ++di) {
       for (size_t i = 0; i < f.size(); ++i) f[i] = static_cast<float>(d[di][i]);
@@ -529,6 +578,7 @@ struct BigPlan {
     if (spn_status st = upload_f32(row_perm(d[0], n, tb, lc, row_lt(lc)), &srow1)) return st;
     if (spn_status st = upload_f32(row_perm(d[2], n, tb, lc, row_lt(lc)), &srow3)) return st;
     if (spn_status st = upload_f32(tile_perm(d[1], n, tb, lc), &stile2)) return st;
+    built = true;
     return SPN_OK;
   }
 
@@ -537,6 +587,7 @@ struct BigPlan {
                    int relu, int64_t k, int64_t m, int64_t blocks, double c, int sms, cudaStream_t s0) {
     if (batch == 0) return SPN_OK;
     std::lock_guard<std::mutex> lock(mu);
+    if (spn_status st = build_now()) return st;
     auto al16 = [](const void* q, int64_t ld) { return (reinterpret_cast<uintptr_t>(q) % 16 == 0) && (ld % 4 == 0); };
     // vectors per group: working set ~32 MB (L2-resident passes)
     const int64_t G = std::max<int64_t>(1, std::min<int64_t>(batch, group_bytes() / (n * 4)));
@@ -764,14 +815,17 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
   // column groups of ~32 MB of workspace
   int64_t dc = std::max<int64_t>(32, (group_bytes() / (nn * 4)) / 32 * 32);
   dc = std::min<int64_t>(dc, (dcols + 31) / 32 * 32);
-  if (spn_status st = bp->ensure_work(static_cast<size_t>(BigPlan::nstreams() * nn * dc * 4))) return st;
+  Scratch scratch;
+  if (cudaError_t e = scratch.alloc(static_cast<size_t>(BigPlan::nstreams() * nn * dc * 4), s0))
+    return BigPlan::err(e, "sketch workspace");
+  float* const work = static_cast<float*>(scratch.p);
   if (spn_status st = bp->fork(s0)) return st;
   int64_t gi = 0;
   const int64_t Sa = int64_t(1) << lsa, Sb = int64_t(1) << lsb;
   for (int64_t c0 = 0; c0 < dcols; c0 += dc, ++gi) {
     const int si = static_cast<int>(gi % BigPlan::nstreams());
     s = bp->ss[si];
-    float* W = bp->work + si * nn * dc;
+    float* W = work + si * nn * dc;
     const int64_t nc = std::min(dc, dcols - c0);
     ColParams pa = cp;  // low-bit passes
     pa.ncols = nc;

@@ -202,8 +202,11 @@ def _line_losses(p, x, step, s0, count, stream=None):
 
 def _backtrack(p, x, step, f0, slope, stream=None):
     """Backtracking Armijo (alpha 0.1, beta 0.5) of newton_sketch.cpp:140-142 / 163-164:
-    returns (s, loss(x + s step)).  Candidates s = 2^-k are evaluated in one pass over A."""
-    losses = _line_losses(p, x, step, 1.0, _MAX_BACKTRACK, stream)
+    returns (s, loss(x + s step)).  The first 4 candidates s = 2^-k come from one pass over
+    A (one transcendental per lane per 8 rows); deeper backtracking evaluates all 41."""
+    losses = _line_losses(p, x, step, 1.0, 4, stream)
+    if not any(losses[k] <= f0 + 0.1 * 2.0 ** -k * slope for k in range(4)):
+        losses = _line_losses(p, x, step, 1.0, _MAX_BACKTRACK, stream)
     s = 1.0
     for k in range(_MAX_BACKTRACK):
         if not (s > 1e-12):
