@@ -184,6 +184,16 @@ SPN_API spn_status spn_sketched_step_f32(spn_newton* w, const spn_plan* sketch, 
 SPN_API spn_status spn_logistic_line_f32(spn_newton* w, const float* a, int64_t ld_a, const float* labels,
                                          const double* x, const double* step, double s0, int64_t count,
                                          double* losses, void* stream);
+/* Host-buffer forms (the reference's value semantics; synchronous).  The problem is
+ * uploaded once into the workspace (fp32 features [n][ld], +-1 labels); the calls then
+ * move only d-vectors and scalars. */
+SPN_API spn_status spn_newton_set_problem(spn_newton* w, const float* features, int64_t ld, const float* labels);
+SPN_API spn_status spn_logistic_eval_host(spn_newton* w, const double* x, double* loss, double* grad);
+SPN_API spn_status spn_hessian_sqrt_host(spn_newton* w, const double* x, float* out, int64_t ld_out);
+SPN_API spn_status spn_sketched_step_host(spn_newton* w, const spn_plan* sketch, int64_t rows, const double* x,
+                                          double* step, double* grad, double* loss);
+SPN_API spn_status spn_logistic_line_host(spn_newton* w, const double* x, const double* step, double s0,
+                                          int64_t count, double* losses);
 /* generate_ar1_problem(n, d, seed) (:185-204) on the host (reference generator, bit-exact
  * in fp64), rounded to fp32: features [n][d], labels [n]. */
 SPN_API spn_status spn_ar1_problem(int64_t n, int64_t d, uint64_t seed, float* features, float* labels);

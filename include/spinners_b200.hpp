@@ -12,8 +12,11 @@
 //   * Eigen is not required: SketchOperator::apply takes a row-major n x d buffer.
 #pragma once
 
+#include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <tuple>
+#include <utility>
 #include <functional>
 #include <memory>
 #include <stdexcept>
@@ -35,12 +38,16 @@ struct DomainError : std::domain_error {  // common.hpp:19-21
 struct DeviceError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct SingularSystemError : std::runtime_error {  // common.hpp:25-27
+  using std::runtime_error::runtime_error;
+};
 
 inline void check(spn_status s) {
   if (s == SPN_OK) return;
   std::string msg = std::string(spn_status_string(s)) + ": " + spn_last_error();
   if (s == SPN_EDIM) throw DimensionError(msg);
   if (s == SPN_EDOMAIN) throw DomainError(msg);
+  if (s == SPN_ESINGULAR) throw SingularSystemError(msg);
   throw DeviceError(msg);
 }
 
@@ -277,6 +284,9 @@ inline void embed_batch(const FeatureMap& fm, const float* x, std::size_t batch,
 // Spinner sketch on n-row matrices (newton_sketch.hpp:50-71, newton_sketch.cpp:74-101).
 class SketchOperator {
  public:
+  SketchOperator() = default;  // the exact (identity) operator, newton_sketch.hpp:55-56
+  bool is_exact() const { return !projector_; }
+  const spn_plan* plan() const { return projector_ ? projector_->plan() : nullptr; }
   SketchOperator(SpinnerVariant v, std::size_t input_dim, std::size_t rows, std::uint64_t seed, int device = 0)
       : input_dim_(input_dim), rows_(rows) {
     padded_ = 1;
@@ -285,7 +295,7 @@ class SketchOperator {
     projector_ = std::make_unique<StackedSpinner>(v, padded_, std::min(rows, padded_), rows, seed, 0.0, device);
     norm_ = 1.0 / std::sqrt(static_cast<double>(rows));
   }
-  std::size_t rows(std::size_t) const { return rows_; }
+  std::size_t rows(std::size_t input_dim) const { return is_exact() ? input_dim : rows_; }
   // columns: row-major [input_dim][d] on the DEVICE; out: [rows][d] on the device.
   void apply_device(const float* columns, std::size_t d, float* out, void* stream,
                     const std::vector<int64_t>* row_list = nullptr) const {
@@ -295,15 +305,203 @@ class SketchOperator {
   }
 
  private:
-  std::size_t input_dim_, rows_, padded_ = 1;
+  std::size_t input_dim_ = 0, rows_ = 0, padded_ = 1;
   double norm_ = 1.0;
-  std::unique_ptr<StackedSpinner> projector_;
+  std::shared_ptr<StackedSpinner> projector_;
 };
 
 inline std::vector<int64_t> sample_rows(std::int64_t N, std::int64_t m, std::uint64_t seed) {
   std::vector<int64_t> out(static_cast<std::size_t>(m));
   check(spn_sample_rows(N, m, seed, out.data()));
   return out;
+}
+
+// ------------------------------------------------------------------ sketched Newton
+// newton_sketch.hpp:13-86 / newton_sketch.cpp:28-204.  Features are a row-major
+// n x d host matrix (no Eigen); the problem is uploaded once (fp32) to a device
+// workspace, every numeric step runs on the GPU, vectors come back as fp64.
+struct LogisticProblem {
+  std::size_t n = 0, d = 0;
+  std::vector<double> features;  // row-major n x d
+  Vec64 labels;                  // +-1
+  int device = 0;
+
+  void validate() const {  // newton_sketch.cpp:28-37
+    if (n < 1 || d < 1) throw DimensionError("LogisticProblem: empty data");
+    if (labels.size() != n) throw DimensionError("LogisticProblem: label count mismatch");
+    for (double v : features)
+      if (!std::isfinite(v)) throw DomainError("LogisticProblem: non-finite features");
+    for (double y : labels)
+      if (y != 1.0 && y != -1.0) throw DomainError("LogisticProblem: labels must be +-1");
+  }
+  std::size_t observations() const { return n; }
+  std::size_t dim() const { return d; }
+
+  // device workspace with the problem resident (created on first use, grown for larger sketches)
+  spn_newton* workspace(std::size_t rows = 0) const {
+    if (!ws_ || ws_rows_ < rows) {
+      spn_newton* w = nullptr;
+      check(spn_newton_create(&w, static_cast<int64_t>(n), static_cast<int64_t>(d), static_cast<int64_t>(rows),
+                              device));
+      ws_.reset(w, [](spn_newton* q) { spn_newton_destroy(q); });
+      ws_rows_ = rows;
+      std::vector<float> f(features.begin(), features.end()), y(labels.begin(), labels.end());
+      check(spn_newton_set_problem(w, f.data(), static_cast<int64_t>(d), y.data()));
+    }
+    return ws_.get();
+  }
+
+ private:
+  mutable std::shared_ptr<spn_newton> ws_;
+  mutable std::size_t ws_rows_ = 0;
+};
+
+struct SketchConfig {  // newton_sketch.hpp:23-33
+  bool sketched = false;  // std::optional<SpinnerVariant> in the reference
+  SpinnerVariant sketch_variant = SpinnerVariant::hd3_hd2_hd1;
+  std::size_t sketch_rows = 0;
+  std::size_t max_iters = 50;
+  double gap_tolerance = 1e-10;
+  bool line_search = true;
+  std::uint64_t seed = 0;
+
+  void validate(const LogisticProblem& p) const {  // newton_sketch.cpp:39-43
+    if (sketched && sketch_rows < p.dim()) throw DimensionError("SketchConfig: sketch_rows must be >= d");
+    if (max_iters < 1) throw DimensionError("SketchConfig: max_iters must be >= 1");
+  }
+};
+
+struct NewtonTrace {  // newton_sketch.hpp:35-42
+  std::vector<Vec64> iterates;
+  std::vector<double> losses, gaps, seconds;
+  double f_star = 0.0;
+  bool converged = false;
+};
+
+inline double loss(const LogisticProblem& p, const Vec64& x) {  // newton_sketch.cpp:45-52
+  if (x.size() != p.d) throw DimensionError("loss: dimension mismatch");
+  double f = 0.0;
+  check(spn_logistic_eval_host(p.workspace(), x.data(), &f, nullptr));
+  return f;
+}
+
+inline Vec64 gradient(const LogisticProblem& p, const Vec64& x) {  // newton_sketch.cpp:54-61
+  if (x.size() != p.d) throw DimensionError("gradient: dimension mismatch");
+  Vec64 g(p.d);
+  check(spn_logistic_eval_host(p.workspace(), x.data(), nullptr, g.data()));
+  return g;
+}
+
+// newton_sketch.cpp:63-72, row-major n x d
+inline std::vector<double> hessian_sqrt(const LogisticProblem& p, const Vec64& x) {
+  if (x.size() != p.d) throw DimensionError("hessian_sqrt: dimension mismatch");
+  std::vector<float> h(p.n * p.d);
+  check(spn_hessian_sqrt_host(p.workspace(), x.data(), h.data(), static_cast<int64_t>(p.d)));
+  return std::vector<double>(h.begin(), h.end());
+}
+
+namespace detail {
+inline Vec64 step_at(const LogisticProblem& p, const Vec64& x, const SketchOperator& sketch, Vec64* grad,
+                     double* f) {
+  if (x.size() != p.d) throw DimensionError("sketched_step: dimension mismatch");
+  const std::size_t rows = sketch.rows(p.n);
+  Vec64 step(p.d);
+  check(spn_sketched_step_host(p.workspace(sketch.is_exact() ? 0 : rows), sketch.plan(), static_cast<int64_t>(rows),
+                               x.data(), step.data(), grad ? grad->data() : nullptr, f));
+  return step;
+}
+
+// Backtracking Armijo, alpha 0.1, beta 0.5 (newton_sketch.cpp:140-142,163-164): returns
+// (s, loss(x + s step)); the 2^-k candidates come from one pass over A on the device.
+inline std::pair<double, double> backtrack(const LogisticProblem& p, const Vec64& x, const Vec64& step, double f0,
+                                           double slope) {
+  constexpr int kMax = 41;
+  double losses[kMax];
+  spn_newton* w = p.workspace();
+  check(spn_logistic_line_host(w, x.data(), step.data(), 1.0, 4, losses));
+  bool found = false;
+  for (int k = 0; k < 4 && !found; ++k) found = !(losses[k] > f0 + 0.1 * std::ldexp(1.0, -k) * slope);
+  if (!found) check(spn_logistic_line_host(w, x.data(), step.data(), 1.0, kMax, losses));
+  double s = 1.0;
+  for (int k = 0; k < kMax; ++k) {
+    if (!(s > 1e-12) || !(losses[k] > f0 + 0.1 * s * slope)) return {s, losses[k]};
+    s *= 0.5;
+  }
+  return {s, loss(p, x)};
+}
+}  // namespace detail
+
+// newton_sketch.cpp:103-122
+inline Vec64 sketched_step(const LogisticProblem& p, const Vec64& x, const SketchOperator& sketch) {
+  return detail::step_at(p, x, sketch, nullptr, nullptr);
+}
+
+// newton_sketch.cpp:124-183
+inline NewtonTrace solve(const LogisticProblem& p, const SketchConfig& cfg) {
+  p.validate();
+  cfg.validate(p);
+  const std::size_t d = p.dim(), n = p.observations();
+  double f_star;
+  {
+    Vec64 x(d, 0.0), g(d);
+    const SketchOperator exact;
+    for (int it = 0; it < 200; ++it) {
+      double f0 = 0.0;
+      const Vec64 step = detail::step_at(p, x, exact, &g, &f0);
+      double decrement = 0.0;
+      for (std::size_t j = 0; j < d; ++j) decrement -= g[j] * step[j];
+      const double s = detail::backtrack(p, x, step, f0, -decrement).first;
+      for (std::size_t j = 0; j < d; ++j) x[j] += s * step[j];
+      if (decrement / 2.0 < 1e-13) break;
+    }
+    f_star = loss(p, x);
+  }
+  NewtonTrace trace;
+  trace.f_star = f_star;
+  Vec64 x(d, 0.0), g(d);
+  for (std::size_t t = 0; t < cfg.max_iters; ++t) {
+    const auto tic = std::chrono::steady_clock::now();
+    SketchOperator sketch;  // fresh sketch every iteration
+    if (cfg.sketched) sketch = SketchOperator(cfg.sketch_variant, n, cfg.sketch_rows, mix_seed(cfg.seed, t), p.device);
+    double f0 = 0.0;
+    const Vec64 step = detail::step_at(p, x, sketch, &g, &f0);
+    double s = 1.0, f_next;
+    if (cfg.line_search) {
+      double slope = 0.0;
+      for (std::size_t j = 0; j < d; ++j) slope += g[j] * step[j];
+      std::tie(s, f_next) = detail::backtrack(p, x, step, f0, slope);
+    } else {
+      double l1 = 0.0;
+      check(spn_logistic_line_host(p.workspace(), x.data(), step.data(), 1.0, 1, &l1));
+      f_next = l1;
+    }
+    if (!cfg.line_search && f_next > f0)
+      throw SingularSystemError("solve: loss increased under a full step (divergence)");
+    for (std::size_t j = 0; j < d; ++j) x[j] += s * step[j];
+    const auto toc = std::chrono::steady_clock::now();
+    trace.iterates.push_back(x);
+    trace.losses.push_back(f_next);
+    trace.gaps.push_back(f_next - f_star);
+    trace.seconds.push_back(std::chrono::duration<double>(toc - tic).count());
+    if (f_next - f_star <= cfg.gap_tolerance) {
+      trace.converged = true;
+      break;
+    }
+  }
+  return trace;
+}
+
+// newton_sketch.cpp:185-204 (the reference generator; features rounded to fp32 like the device copy)
+inline LogisticProblem generate_ar1_problem(std::size_t n, std::size_t d, std::uint64_t seed, int device = 0) {
+  std::vector<float> f(n * d), y(n);
+  check(spn_ar1_problem(static_cast<int64_t>(n), static_cast<int64_t>(d), seed, f.data(), y.data()));
+  LogisticProblem p;
+  p.n = n;
+  p.d = d;
+  p.features.assign(f.begin(), f.end());
+  p.labels.assign(y.begin(), y.end());
+  p.device = device;
+  return p;
 }
 
 }  // namespace spinners_b200

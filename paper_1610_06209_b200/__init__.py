@@ -88,7 +88,8 @@ ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_c
                "spn_hash_f32_host", "spn_embed_f32_host", "spn_sample_rows", "spn_mix_seed",
                "spn_check_rows_f32", "spn_realize_block", "spn_newton_create", "spn_newton_destroy",
                "spn_logistic_eval_f32", "spn_hessian_sqrt_f32", "spn_sketched_step_f32", "spn_logistic_line_f32",
-               "spn_ar1_problem")
+               "spn_ar1_problem", "spn_newton_set_problem", "spn_logistic_eval_host", "spn_hessian_sqrt_host",
+               "spn_sketched_step_host", "spn_logistic_line_host")
 
 
 # ----------------------------------------------------------------------- errors

@@ -610,15 +610,22 @@ struct spn_newton {
   double* loss = nullptr;     // [1]
   int* flag = nullptr;        // device pivot-failure flag
   int* flag_h = nullptr;      // pinned
+  // resident problem for the host-buffer entry points
+  float* a = nullptr;         // [n][d]
+  float* labels = nullptr;    // [n]
+  double* hx = nullptr;       // [3][d] x, step, scratch (+ scalars)
+  cudaStream_t s = nullptr;
 };
 
 namespace {
 
 void newton_free(spn_newton* w) {
   for (void* p : {(void*)w->part, (void*)w->margins, (void*)w->h32, (void*)w->h64, (void*)w->sb, (void*)w->spart,
-                  (void*)w->normal, (void*)w->fact, (void*)w->grad, (void*)w->loss, (void*)w->flag})
+                  (void*)w->normal, (void*)w->fact, (void*)w->grad, (void*)w->loss, (void*)w->flag, (void*)w->a,
+                  (void*)w->labels, (void*)w->hx})
     if (p) cudaFree(p);
   if (w->flag_h) cudaFreeHost(w->flag_h);
+  if (w->s) cudaStreamDestroy(w->s);
 }
 
 template <int DCH>
@@ -827,6 +834,102 @@ spn_status spn_logistic_line_f32(spn_newton* w, const float* a, int64_t ld_a, co
   NWT_CUDA(launch_line(w, a, ld_a, labels, x, step, s0, (int)count, s));
   reduce_parts_kernel<<<(unsigned)count, 256, 0, s>>>(w->part, w->grid, (int)count, losses, nullptr, (int)count);
   NWT_CUDA(cudaGetLastError());
+  return SPN_OK;
+}
+
+// ------------------------------------------------------------- host-buffer forms
+spn_status spn_newton_set_problem(spn_newton* w, const float* features, int64_t ld, const float* labels) {
+  if (!w || !features || !labels) return fail(SPN_EINVAL, "null pointer");
+  if (ld < w->d) return fail(SPN_EINVAL, "bad leading dimension");
+  DevGuard g(w->device);
+  if (!w->a) NWT_CUDA(cudaMalloc(&w->a, sizeof(float) * (size_t)(w->n * w->d)));
+  if (!w->labels) NWT_CUDA(cudaMalloc(&w->labels, sizeof(float) * (size_t)w->n));
+  if (!w->hx) NWT_CUDA(cudaMalloc(&w->hx, sizeof(double) * (size_t)(4 * w->d + 128)));
+  if (!w->s) NWT_CUDA(cudaStreamCreateWithFlags(&w->s, cudaStreamNonBlocking));
+  NWT_CUDA(cudaMemcpy2D(w->a, sizeof(float) * (size_t)w->d, features, sizeof(float) * (size_t)ld,
+                        sizeof(float) * (size_t)w->d, (size_t)w->n, cudaMemcpyHostToDevice));
+  NWT_CUDA(cudaMemcpy(w->labels, labels, sizeof(float) * (size_t)w->n, cudaMemcpyHostToDevice));
+  return SPN_OK;
+}
+
+namespace {
+spn_status need_problem(const spn_newton* w) {
+  if (!w) return fail(SPN_EINVAL, "null workspace");
+  if (!w->a) return fail(SPN_EINVAL, "spn_newton_set_problem was not called");
+  return SPN_OK;
+}
+}  // namespace
+
+spn_status spn_logistic_eval_host(spn_newton* w, const double* x, double* loss, double* grad) {
+  if (spn_status st = need_problem(w)) return st;
+  if (!x) return fail(SPN_EINVAL, "null pointer");
+  DevGuard g(w->device);
+  const size_t db = sizeof(double) * (size_t)w->d;
+  double* dx = w->hx;
+  double* dg = w->hx + w->d;
+  double* df = w->hx + 4 * w->d;
+  NWT_CUDA(cudaMemcpyAsync(dx, x, db, cudaMemcpyHostToDevice, w->s));
+  if (spn_status st = spn_logistic_eval_f32(w, w->a, w->d, w->labels, dx, df, dg, w->s)) return st;
+  if (grad) NWT_CUDA(cudaMemcpyAsync(grad, dg, db, cudaMemcpyDeviceToHost, w->s));
+  if (loss) NWT_CUDA(cudaMemcpyAsync(loss, df, sizeof(double), cudaMemcpyDeviceToHost, w->s));
+  NWT_CUDA(cudaStreamSynchronize(w->s));
+  return SPN_OK;
+}
+
+spn_status spn_hessian_sqrt_host(spn_newton* w, const double* x, float* out, int64_t ld_out) {
+  if (spn_status st = need_problem(w)) return st;
+  if (!x || !out) return fail(SPN_EINVAL, "null pointer");
+  if (ld_out < w->d) return fail(SPN_EINVAL, "bad leading dimension");
+  DevGuard g(w->device);
+  float* dout = nullptr;
+  NWT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dout), sizeof(float) * (size_t)(w->n * w->d), w->s));
+  NWT_CUDA(cudaMemcpyAsync(w->hx, x, sizeof(double) * (size_t)w->d, cudaMemcpyHostToDevice, w->s));
+  spn_status st = spn_hessian_sqrt_f32(w, w->a, w->d, w->hx, dout, w->d, w->s);
+  cudaError_t e = cudaSuccess;
+  if (!st)
+    e = cudaMemcpy2DAsync(out, sizeof(float) * (size_t)ld_out, dout, sizeof(float) * (size_t)w->d,
+                          sizeof(float) * (size_t)w->d, (size_t)w->n, cudaMemcpyDeviceToHost, w->s);
+  cudaFreeAsync(dout, w->s);
+  if (st) return st;
+  if (e != cudaSuccess) return spn::cuda_error(e, "hessian_sqrt copy");
+  NWT_CUDA(cudaStreamSynchronize(w->s));
+  return SPN_OK;
+}
+
+spn_status spn_sketched_step_host(spn_newton* w, const spn_plan* sketch, int64_t rows, const double* x, double* step,
+                                  double* grad, double* loss) {
+  if (spn_status st = need_problem(w)) return st;
+  if (!x || !step) return fail(SPN_EINVAL, "null pointer");
+  DevGuard g(w->device);
+  const size_t db = sizeof(double) * (size_t)w->d;
+  double* dx = w->hx;
+  double* ds = w->hx + w->d;
+  double* dg = w->hx + 2 * w->d;
+  double* df = w->hx + 4 * w->d;
+  NWT_CUDA(cudaMemcpyAsync(dx, x, db, cudaMemcpyHostToDevice, w->s));
+  if (spn_status st = spn_sketched_step_f32(w, sketch, rows, w->a, w->d, w->labels, dx, ds, dg, df, w->s)) return st;
+  NWT_CUDA(cudaMemcpyAsync(step, ds, db, cudaMemcpyDeviceToHost, w->s));
+  if (grad) NWT_CUDA(cudaMemcpyAsync(grad, dg, db, cudaMemcpyDeviceToHost, w->s));
+  if (loss) NWT_CUDA(cudaMemcpyAsync(loss, df, sizeof(double), cudaMemcpyDeviceToHost, w->s));
+  NWT_CUDA(cudaStreamSynchronize(w->s));
+  return SPN_OK;
+}
+
+spn_status spn_logistic_line_host(spn_newton* w, const double* x, const double* step, double s0, int64_t count,
+                                  double* losses) {
+  if (spn_status st = need_problem(w)) return st;
+  if (!x || !step || !losses) return fail(SPN_EINVAL, "null pointer");
+  if (count < 1 || count > 64) return fail(SPN_EINVAL, "line search: 1 <= count <= 64");
+  DevGuard g(w->device);
+  const size_t db = sizeof(double) * (size_t)w->d;
+  double* dx = w->hx;
+  double* ds = w->hx + w->d;
+  double* dl = w->hx + 4 * w->d + 1;
+  NWT_CUDA(cudaMemcpyAsync(dx, x, db, cudaMemcpyHostToDevice, w->s));
+  NWT_CUDA(cudaMemcpyAsync(ds, step, db, cudaMemcpyHostToDevice, w->s));
+  if (spn_status st = spn_logistic_line_f32(w, w->a, w->d, w->labels, dx, ds, s0, count, dl, w->s)) return st;
+  NWT_CUDA(cudaMemcpyAsync(losses, dl, sizeof(double) * (size_t)count, cudaMemcpyDeviceToHost, w->s));
+  NWT_CUDA(cudaStreamSynchronize(w->s));
   return SPN_OK;
 }
 

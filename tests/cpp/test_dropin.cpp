@@ -173,6 +173,54 @@ int main() {
     CHECK(ok && r.front() >= 0 && r.back() < 1000);
   });
 
+  // newton_sketch.cpp via the drop-in: loss / gradient / steps against the C oracle,
+  // solve() convergence (proj/tests/test_newton.cpp-style properties)
+  test_case("sketched Newton: loss, gradient, exact and sketched steps match the oracle", [] {
+    const std::size_t n = 300, d = 12;
+    LogisticProblem p = generate_ar1_problem(n, d, 5);
+    std::vector<double> a(n * d), y(n);
+    orc_ar1_problem(n, d, 5, a.data(), y.data());
+    for (std::size_t i = 0; i < n * d; ++i) a[i] = static_cast<double>(static_cast<float>(a[i]));
+    CHECK(p.labels == y);
+    Vec64 x(d);
+    for (std::size_t j = 0; j < d; ++j) x[j] = -0.1 + 0.2 * j / (d - 1);
+    const double f = orc_logistic_loss(a.data(), y.data(), n, d, x.data());
+    CHECK(std::abs(loss(p, x) - f) <= 1e-9 * std::abs(f));
+    Vec64 g(d);
+    orc_logistic_gradient(a.data(), y.data(), n, d, x.data(), g.data());
+    CHECK(max_abs_diff(gradient(p, x), g) <= 1e-9);
+    Vec64 s(d);
+    CHECK(orc_sketched_step(a.data(), y.data(), n, d, x.data(), 0, 0, 0, 0, nullptr, nullptr, nullptr, s.data()) == 0);
+    CHECK(max_abs_diff(sketched_step(p, x, SketchOperator()), s) <= 1e-8);
+    const std::size_t N = 512, m = 64;
+    std::vector<double> d1(N), d2(N), d3(N);
+    orc_realize_stacked(0, N, m, m, 99, d1.data(), d2.data(), d3.data());
+    CHECK(orc_sketched_step(a.data(), y.data(), n, d, x.data(), N, m, std::sqrt(double(N)), 1 / std::sqrt(double(m)),
+                            d1.data(), d2.data(), d3.data(), s.data()) == 0);
+    SketchOperator sk(SpinnerVariant::hd3_hd2_hd1, n, m, 99);
+    CHECK(max_abs_diff(sketched_step(p, x, sk), s) <= 1e-5);
+    CHECK(throws<DimensionError>([&] { sketched_step(p, x, SketchOperator(SpinnerVariant::hd3_hd2_hd1, n, 8, 1)); }));
+  });
+
+  test_case("sketched Newton: solve converges (exact and HD3 sketch) to the same optimum", [] {
+    LogisticProblem p = generate_ar1_problem(300, 12, 5);
+    SketchConfig ex;
+    ex.max_iters = 30;
+    NewtonTrace te = solve(p, ex);
+    CHECK(te.converged && te.gaps.back() <= 1e-10);
+    SketchConfig sk;
+    sk.sketched = true;
+    sk.sketch_rows = 64;
+    sk.max_iters = 30;
+    sk.seed = 7;
+    NewtonTrace ts = solve(p, sk);
+    CHECK(ts.converged && ts.gaps.back() <= 1e-10);
+    CHECK(std::abs(ts.f_star - te.f_star) <= 1e-12 * std::abs(te.f_star));
+    LogisticProblem z = generate_ar1_problem(300, 12, 5);
+    for (double& v : z.features) v = 0.0;
+    CHECK(throws<SingularSystemError>([&] { sketched_step(z, Vec64(12, 0.0), SketchOperator()); }));
+  });
+
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ALL PASSED", g_fail);
   return g_fail ? 1 : 0;
 }
