@@ -45,6 +45,9 @@ CONFIGS = {
                         "random rows", N=1 << 17, d=256, m=2048, bytes_per_vec=(1 << 17) * 4 + 2048 * 4, flush=True),
     "c5": dict(workload="BASELINE configs[4]: ReLU(H D3 H D2 H D1 x), Gaussian D's, 256 x n=2^20",
                n=1 << 20, batch=256, bytes_per_vec=(1 << 20) * 8, flush=False),
+    "c7": dict(workload="SURVEY 8(f) rank 2: collision_curve of the HD3 family, n=256, m=64, 20000 pairs x 100 "
+                        "trials (acceptance criterion 5 scale); units = hashed vectors (2 x pairs x trials)",
+               n=256, m=64, pairs=20000, trials=100, bytes_per_vec=256 * 4, flush=False),
     "c6": dict(workload="SURVEY 8(f) rank 1: one sketched Newton iteration of solve() (fresh HD3 SketchOperator, "
                         "sketched_step, Armijo line search) for logistic regression on A = 131072 x 256, m = 2048",
                N=1 << 17, d=256, m=2048, bytes_per_vec=(1 << 17) * 4 * 6, flush=False),
@@ -202,6 +205,23 @@ class Workload:
             self.t = 0
             # pass over A + 4 sketch passes + line-search pass per iteration (launch count is a lower bound)
             self.launches_per_step = 16
+        elif name == "c7":
+            import numpy as np
+            rng = np.random.default_rng(88 + rank)
+            P, n = cfg["pairs"], cfg["n"]
+            ang = np.pi * (np.arange(P) + 0.5) / P
+            x = rng.standard_normal((P, n))
+            u = rng.standard_normal((P, n))
+            x /= np.linalg.norm(x, axis=1, keepdims=True)
+            u -= np.sum(u * x, axis=1, keepdims=True) * x
+            u /= np.linalg.norm(u, axis=1, keepdims=True)
+            y = np.cos(ang)[:, None] * x + np.sin(ang)[:, None] * u
+            self.cx = torch.from_numpy(x.astype(np.float32)).cuda()
+            self.cy = torch.from_numpy(y.astype(np.float32)).cuda()
+            self.cd = 2.0 * np.sin(ang / 2.0)
+            self.fac = spn.make_hasher_factory(V.hd3_hd2_hd1, n, cfg["m"])
+            self.vectors = 2 * P * cfg["trials"]
+            self.t = 0
         elif name == "c5":
             self.sp = spn.StackedSpinner(V.gauss3, cfg["n"], cfg["n"], cfg["n"], 13 + rank, scale=1.0)
             self.x = torch.randn((cfg["batch"], cfg["n"]), device="cuda", generator=g)
@@ -220,6 +240,10 @@ class Workload:
             return self.h.plan.hash(self.x, stream=stream)
         if self.name == "c4":
             return self.sk.apply(self.x, out=self.out, stream=stream)
+        if self.name == "c7":  # lsh.cpp:38-74, fresh trial seeds every step
+            self.t += 1
+            return self.spn.collision_curve((self.cx, self.cy, self.cd), self.fac, self.cfg["trials"], 90 + self.t,
+                                            stream=stream)
         if self.name == "c6":  # newton_sketch.cpp:155-170, one iteration
             cfg, nt = self.cfg, self.newton
             sk = self.spn.SketchOperator(self.spn.SpinnerVariant.hd3_hd2_hd1, cfg["N"], cfg["m"],
@@ -377,6 +401,20 @@ def cpu_reference(config, budget_s=20.0, threads=None):
                                 threads=threads)
         total = cfg["d"]
         what = "SketchOperator::apply restated over the reference StackedSpinner, random P"
+    elif config == "c7":  # the reference's collision_curve on 2 of the 100 trials (single-threaded driver)
+        P, n = cfg["pairs"], cfg["n"]
+        ang = np.pi * (np.arange(P) + 0.5) / P
+        x = rng.standard_normal((P, n))
+        u = rng.standard_normal((P, n))
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        u -= np.sum(u * x, axis=1, keepdims=True) * x
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        y = np.cos(ang)[:, None] * x + np.sin(ang)[:, None] * u
+        d = 2.0 * np.sin(ang / 2.0)
+        dt = timed(lambda c: r.collision_curve(HD3, n, cfg["m"], x, y, d, 2, 91), 1)
+        return 2 * P * 2 / dt, {"kind": "reference", "cores": 1,
+                                "sample": "collision_curve over all 20000 pairs x 2 trials (80000 hashed vectors); "
+                                          "the reference's lsh.cpp driver, single-threaded"}
     elif config == "c6":  # one reference sketched_step (newton_sketch.cpp:103-122, single-threaded code)
         a = rng.standard_normal((cfg["N"], cfg["d"])).astype(np.float32).astype(np.float64)
         y = np.where(rng.random(cfg["N"]) < 0.5, -1.0, 1.0)

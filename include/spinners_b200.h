@@ -18,6 +18,7 @@
  *                               newton_sketch.cpp:74-101)
  *   spn_*_host               <- the same calls on host buffers (the reference's
  *                               value-semantics API), with the H2D/D2H copies inside.
+ *   spn_collision_hits_f32   <- collision_curve / compare_families (lsh.hpp:38-75; lsh.cpp:38-96)
  *   spn_newton_*, spn_logistic_*, spn_sketched_step_f32, spn_ar1_problem
  *                            <- the sketched Newton method that calls SketchOperator
  *                               (newton_sketch.hpp:63-86; newton_sketch.cpp:45-72,103-204)
@@ -149,6 +150,15 @@ SPN_API uint64_t spn_mix_seed(uint64_t base, uint64_t stream);
  * non-finite entry, bit1 = all zero (what hash/embed reject, lsh.cpp:24-28). */
 SPN_API spn_status spn_check_rows_f32(const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
                                       int32_t* flags, void* stream);
+
+/* collision_curve / compare_families (lsh.cpp:38-96; lsh.hpp:38-75), the counting core.
+ * plan: `trials` tables of make_hasher_factory(v, n, m) with table seeds mix_seed(seed, t)
+ * (lsh.cpp:56).  xy: 2*pairs device rows, row 2p = x_p, row 2p+1 = y_p.  bucket_of: device
+ * int32 [pairs] (< buckets).  hits: device int64 [buckets], accumulated with the number of
+ * (pair, trial) events where hash_t(x_p) == hash_t(y_p) (same index and sign). */
+SPN_API spn_status spn_collision_hits_f32(const spn_plan* plan, const float* xy, int64_t pairs, int64_t ld,
+                                          int64_t n_in, const int32_t* bucket_of, int64_t buckets, int64_t* hits,
+                                          void* stream);
 
 /* ------------------------------------------------------------------ sketched Newton
  * Logistic regression with spinner-sketched Hessians (newton_sketch.hpp:13-86).

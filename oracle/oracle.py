@@ -315,6 +315,19 @@ class Reference:
                                         threads))
         return out
 
+    def collision_curve(self, variant, n, m, xs, ys, dist, trials, seed, buckets=25, max_distance=2.0):
+        """lsh.cpp:38-74 (the reference's own collision_curve + make_hasher_factory)."""
+        xs = np.ascontiguousarray(xs, dtype=np.float32)
+        ys = np.ascontiguousarray(ys, dtype=np.float32)
+        dist = np.ascontiguousarray(dist, dtype=np.float64)
+        edges, probs = np.zeros(buckets + 1), np.zeros(buckets)
+        counts = np.zeros(buckets, dtype=np.uint64)
+        vp = lambda v: v.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._check(self.lib.ref_collision_curve(cint(variant), i64(n), i64(m), vp(xs), vp(ys), vp(dist),
+                                                 i64(xs.shape[0]), i64(trials), u64(seed), i64(buckets),
+                                                 dbl(max_distance), vp(edges), vp(probs), vp(counts)))
+        return {"bucket_edges": edges, "probabilities": probs, "counts": counts}
+
     # ---- sketched Newton: the reference's own newton_sketch.cpp
     def ar1_problem(self, n, d, seed):
         a, y = np.zeros((n, d)), np.zeros(n)

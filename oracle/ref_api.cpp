@@ -266,6 +266,34 @@ int ref_batch_chain(std::int64_t n, const double* d1, const double* d2, const do
   }
 }
 
+// collision_curve(pairs, make_hasher_factory(v, n, m), trials, seed, buckets, max_distance)
+// (lsh.cpp:38-74), the reference's own driver.  xs / ys: [pairs][n] fp32 rows.
+int ref_collision_curve(int variant, std::int64_t n, std::int64_t m, const float* xs, const float* ys,
+                        const double* dist, std::int64_t pairs, std::int64_t trials, std::uint64_t seed,
+                        std::int64_t buckets, double max_distance, double* edges, double* probs,
+                        std::uint64_t* counts) {
+  try {
+    std::vector<HashedPair> hp(static_cast<std::size_t>(pairs));
+    for (std::int64_t p = 0; p < pairs; ++p) {
+      hp[p].x = row_of(xs, n, p, n, n);
+      hp[p].y = row_of(ys, n, p, n, n);
+      hp[p].distance = dist[p];
+    }
+    CollisionCurve c = collision_curve(hp, make_hasher_factory(variant_of(variant), static_cast<std::size_t>(n),
+                                                               static_cast<std::size_t>(m)),
+                                       static_cast<std::size_t>(trials), seed, static_cast<std::size_t>(buckets),
+                                       max_distance);
+    for (std::int64_t b = 0; b <= buckets; ++b) edges[b] = c.bucket_edges[b];
+    for (std::int64_t b = 0; b < buckets; ++b) {
+      probs[b] = c.probabilities[b];
+      counts[b] = c.counts[b];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // ------------------------------------------------------------ sketched Newton
 // (newton_sketch.cpp, the reference's own functions).  Features are row-major
 // fp64 [n][d]; variant < 0 selects the exact (identity) sketch.

@@ -89,7 +89,7 @@ ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_c
                "spn_check_rows_f32", "spn_realize_block", "spn_newton_create", "spn_newton_destroy",
                "spn_logistic_eval_f32", "spn_hessian_sqrt_f32", "spn_sketched_step_f32", "spn_logistic_line_f32",
                "spn_ar1_problem", "spn_newton_set_problem", "spn_logistic_eval_host", "spn_hessian_sqrt_host",
-               "spn_sketched_step_host", "spn_logistic_line_host")
+               "spn_sketched_step_host", "spn_logistic_line_host", "spn_collision_hits_f32")
 
 
 # ----------------------------------------------------------------------- errors
@@ -460,9 +460,12 @@ class CrossPolytopeHasher:
 
 
 def make_hasher_factory(variant, n, m, device=0):
-    """lsh.cpp:32-36: seed -> CrossPolytopeHasher(StackedSpinner(v, n, min(m,n), m, seed))."""
+    """lsh.cpp:32-36: seed -> CrossPolytopeHasher(StackedSpinner(v, n, min(m,n), m, seed)).
+    The returned callable also carries (variant, n, m, device) so the batched drivers
+    (collision_curve) can build all trials' tables in one plan."""
     def factory(seed):
         return CrossPolytopeHasher(StackedSpinner(variant, n, min(m, n), m, seed, device=device))
+    factory.variant, factory.n, factory.m, factory.device = variant, n, m, device
     return factory
 
 
@@ -569,8 +572,11 @@ __all__ = [
     "embed", "SketchOperator", "mix_seed", "sample_rows", "realize_block", "check_rows", "DimensionError", "DomainError",
     "SpinnerError", "SingularSystemError", "variant_from_string", "version", "LIB_PATH", "ABI_SYMBOLS",
     "LogisticProblem", "SketchConfig", "NewtonTrace", "loss", "gradient", "hessian_sqrt", "sketched_step", "solve",
-    "generate_ar1_problem",
+    "generate_ar1_problem", "HashedPair", "CollisionCurve", "FamilyComparison", "collision_curve",
+    "compare_families",
 ]
 
+from .collision import (CollisionCurve, FamilyComparison, HashedPair, collision_curve,  # noqa: E402
+                        compare_families)
 from .newton import (LogisticProblem, NewtonTrace, SketchConfig, generate_ar1_problem, gradient,  # noqa: E402
                      hessian_sqrt, loss, sketched_step, solve)

@@ -428,6 +428,44 @@ spn_status spn_hash_f32(const spn_plan* p, const float* x, int64_t batch, int64_
   return run_vec(p, y ? spn::OP_APPLY : spn::OP_HASH, v, static_cast<cudaStream_t>(stream));
 }
 
+// collision_curve's counting core (lsh.cpp:54-61): per pair, how many tables give
+// hash(x) == hash(y); one thread per pair, one atomic per pair.
+__global__ void collision_count_kernel(const int32_t* __restrict__ ids, int64_t pairs, int tables,
+                                       const int32_t* __restrict__ bucket_of,
+                                       unsigned long long* __restrict__ hits) {
+  for (int64_t pr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pr < pairs; pr += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t* a = ids + (2 * pr) * tables;
+    const int32_t* b = a + tables;
+    unsigned h = 0;
+    for (int t = 0; t < tables; ++t) h += a[t] == b[t];
+    if (h) atomicAdd(hits + bucket_of[pr], (unsigned long long)h);
+  }
+}
+
+spn_status spn_collision_hits_f32(const spn_plan* p, const float* xy, int64_t pairs, int64_t ld, int64_t n_in,
+                                  const int32_t* bucket_of, int64_t buckets, int64_t* hits, void* stream) {
+  if (spn_status s = check_io(p, xy, 2 * pairs, ld, n_in)) return s;
+  if (pairs > 0 && (!bucket_of || !hits)) return fail(SPN_EINVAL, "null pointer");
+  if (buckets < 1) return fail(SPN_EDIM, "collision_curve: need at least one bucket");
+  if (pairs == 0) return SPN_OK;
+  DeviceGuard g(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // ids for a chunk of pairs: [2 * chunk][tables] int32, <= 64 MB of stream-ordered scratch
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(pairs, (int64_t(8) << 20) / p->tables));
+  spn::Scratch scratch;
+  SPN_CUDA(scratch.alloc(sizeof(int32_t) * static_cast<size_t>(2 * chunk * p->tables), s));
+  int32_t* ids = static_cast<int32_t*>(scratch.p);
+  for (int64_t p0 = 0; p0 < pairs; p0 += chunk) {
+    const int64_t pc = std::min(chunk, pairs - p0);
+    if (spn_status st = spn_hash_f32(p, xy + 2 * p0 * ld, 2 * pc, ld, n_in, ids, nullptr, 0, stream)) return st;
+    const int64_t blocks = std::min<int64_t>((pc + 255) / 256, int64_t(p->sms) * 8);
+    collision_count_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        ids, pc, static_cast<int>(p->tables), bucket_of + p0, reinterpret_cast<unsigned long long*>(hits));
+    SPN_CUDA(cudaGetLastError());
+  }
+  return SPN_OK;
+}
+
 spn_status spn_embed_f32(const spn_plan* p, int32_t kind, double sigma, const float* x,
                          int64_t batch, int64_t ld_x, int64_t n_in, float* out, int64_t ld_out,
                          void* stream) {
