@@ -240,6 +240,98 @@ inline HasherFactory make_hasher_factory(SpinnerVariant v, std::size_t n, std::s
   };
 }
 
+// ------------------------------------------------------------------ collision curves
+struct HashedPair {  // lsh.hpp:38-44
+  Vec64 x;
+  Vec64 y;
+  double distance = 0.0;
+};
+
+struct CollisionCurve {  // lsh.hpp:46-50
+  std::vector<double> bucket_edges;
+  std::vector<double> probabilities;  // NaN where a bucket saw no pairs
+  std::vector<std::size_t> counts;
+};
+
+// lsh.cpp:38-74.  Every trial's hasher hashes all 2 * pairs vectors in one device batch.
+inline CollisionCurve collision_curve(const std::vector<HashedPair>& pairs, const HasherFactory& factory,
+                                      std::size_t trials, std::uint64_t seed, std::size_t buckets = 25,
+                                      double max_distance = 2.0) {
+  if (trials < 1) throw DimensionError("collision_curve: trials must be >= 1");
+  if (buckets < 1) throw DimensionError("collision_curve: need at least one bucket");
+  const std::size_t P = pairs.size();
+  std::vector<std::size_t> bucket_of(P);
+  const double width = max_distance / static_cast<double>(buckets);
+  for (std::size_t p = 0; p < P; ++p) {
+    const double d = pairs[p].distance;
+    if (d < 0.0 || !std::isfinite(d)) throw DomainError("collision_curve: distances must be finite and nonnegative");
+    bucket_of[p] = std::min(static_cast<std::size_t>(d / width), buckets - 1);
+  }
+  std::vector<std::size_t> counts(buckets, 0), hits(buckets, 0);
+  if (P > 0) {
+    const std::size_t n = pairs[0].x.size();
+    std::vector<float> xy(2 * P * n);
+    for (std::size_t p = 0; p < P; ++p) {
+      if (pairs[p].x.size() != n || pairs[p].y.size() != n)
+        throw DimensionError("CrossPolytopeHasher::hash: length mismatch");
+      for (const Vec64* v : {&pairs[p].x, &pairs[p].y}) {
+        check_finite(*v, "CrossPolytopeHasher::hash");
+        bool zero = true;
+        for (double e : *v) zero = zero && e == 0.0;
+        if (zero) throw DomainError("CrossPolytopeHasher::hash: zero vector");
+      }
+      for (std::size_t i = 0; i < n; ++i) {
+        xy[(2 * p) * n + i] = static_cast<float>(pairs[p].x[i]);
+        xy[(2 * p + 1) * n + i] = static_cast<float>(pairs[p].y[i]);
+      }
+    }
+    std::vector<int32_t> ids(2 * P);
+    for (std::size_t t = 0; t < trials; ++t) {
+      const CrossPolytopeHasher hasher = factory(mix_seed(seed, t));
+      hasher.hash_batch(xy.data(), 2 * P, n, n, ids.data());
+      for (std::size_t p = 0; p < P; ++p) {
+        counts[bucket_of[p]]++;
+        if (ids[2 * p] == ids[2 * p + 1]) hits[bucket_of[p]]++;
+      }
+    }
+  }
+  CollisionCurve curve;
+  curve.bucket_edges.resize(buckets + 1);
+  for (std::size_t b = 0; b <= buckets; ++b) curve.bucket_edges[b] = width * static_cast<double>(b);
+  curve.counts = counts;
+  curve.probabilities.resize(buckets);
+  for (std::size_t b = 0; b < buckets; ++b)
+    curve.probabilities[b] = counts[b] == 0 ? std::nan("")
+                                            : static_cast<double>(hits[b]) / static_cast<double>(counts[b]);
+  return curve;
+}
+
+struct FamilyComparison {  // lsh.hpp:68-73
+  CollisionCurve curve_a, curve_b;
+  std::vector<double> bucket_differences;
+  double sup_difference = 0.0;
+};
+
+inline FamilyComparison compare_families(const std::vector<HashedPair>& pairs, const HasherFactory& family_a,
+                                         const HasherFactory& family_b, std::size_t trials, std::uint64_t seed_a,
+                                         std::uint64_t seed_b, std::size_t buckets = 25,
+                                         double max_distance = 2.0) {  // lsh.cpp:76-96
+  FamilyComparison cmp;
+  cmp.curve_a = collision_curve(pairs, family_a, trials, seed_a, buckets, max_distance);
+  cmp.curve_b = collision_curve(pairs, family_b, trials, seed_b, buckets, max_distance);
+  cmp.bucket_differences.resize(buckets);
+  for (std::size_t b = 0; b < buckets; ++b) {
+    const double pa = cmp.curve_a.probabilities[b], pb = cmp.curve_b.probabilities[b];
+    if (std::isnan(pa) || std::isnan(pb)) {
+      cmp.bucket_differences[b] = std::nan("");
+    } else {
+      cmp.bucket_differences[b] = std::abs(pa - pb);
+      cmp.sup_difference = std::max(cmp.sup_difference, cmp.bucket_differences[b]);
+    }
+  }
+  return cmp;
+}
+
 struct KernelKind {  // kernels.hpp:11-24
   enum class Tag { gaussian, angular };
   Tag tag = Tag::gaussian;

@@ -221,6 +221,24 @@ int main() {
     CHECK(throws<SingularSystemError>([&] { sketched_step(z, Vec64(12, 0.0), SketchOperator()); }));
   });
 
+  test_case("collision_curve: identical / antipodal pairs, compare_families with equal seeds", [] {
+    const std::size_t n = 16, m = 8;  // test_lsh.cpp:57-78,140-146
+    auto factory = make_hasher_factory(SpinnerVariant::hd3_hd2_hd1, n, m);
+    std::vector<HashedPair> same, anti;
+    for (std::uint64_t p = 0; p < 20; ++p) {
+      Vec64 x = random_vec(n, 100 + p), neg(n);
+      for (std::size_t i = 0; i < n; ++i) neg[i] = -x[i];
+      same.push_back(HashedPair{x, x, 0.0});
+      anti.push_back(HashedPair{x, neg, 2.0});
+    }
+    CollisionCurve cs = collision_curve(same, factory, 5, 11);
+    CHECK(cs.counts[0] == 100 && cs.probabilities[0] == 1.0 && std::isnan(cs.probabilities[1]) && cs.counts[1] == 0);
+    CollisionCurve ca = collision_curve(anti, factory, 5, 11);
+    CHECK(ca.probabilities[24] == 0.0);
+    CHECK(compare_families(same, factory, factory, 5, 9, 9).sup_difference == 0.0);
+    CHECK(throws<DimensionError>([&] { collision_curve(same, factory, 0, 1); }));
+  });
+
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ALL PASSED", g_fail);
   return g_fail ? 1 : 0;
 }
