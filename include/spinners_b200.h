@@ -19,6 +19,7 @@
  *   spn_*_host               <- the same calls on host buffers (the reference's
  *                               value-semantics API), with the H2D/D2H copies inside.
  *   spn_collision_hits_f32   <- collision_curve / compare_families (lsh.hpp:38-75; lsh.cpp:38-96)
+ *   spn_gram_*               <- gram_exact / gram_approx / gram_error (kernels.hpp:35-41; kernels.cpp:38-114)
  *   spn_newton_*, spn_logistic_*, spn_sketched_step_f32, spn_ar1_problem
  *                            <- the sketched Newton method that calls SketchOperator
  *                               (newton_sketch.hpp:63-86; newton_sketch.cpp:45-72,103-204)
@@ -159,6 +160,19 @@ SPN_API spn_status spn_check_rows_f32(const float* x, int64_t batch, int64_t ld_
 SPN_API spn_status spn_collision_hits_f32(const spn_plan* plan, const float* xy, int64_t pairs, int64_t ld,
                                           int64_t n_in, const int32_t* bucket_of, int64_t buckets, int64_t* hits,
                                           void* stream);
+
+/* Gram matrices of the feature maps (kernels.hpp:35-41; kernels.cpp:38-114), fp64 outputs,
+ * device buffers.  kind: SPN_EMBED_GAUSSIAN / SPN_EMBED_ANGULAR.
+ *   gram_exact:  points [count][ld] fp32 -> exact kernel matrix (diag 1);
+ *   gram_approx: features = embed(fm, points) [count][ld] fp32 (width 2d' gaussian, d' angular)
+ *                -> F F^T (gaussian) or 1/2 + F F^T / (2 d') (angular), diag 1;
+ *   gram_error:  ||exact - approx||_F / ||exact||_F into *err (host; synchronises the stream). */
+SPN_API spn_status spn_gram_exact_f32(const float* points, int64_t count, int64_t dim, int64_t ld, int32_t kind,
+                                      double sigma, double* gram, int64_t ld_gram, void* stream);
+SPN_API spn_status spn_gram_approx_f32(const float* features, int64_t count, int64_t width, int64_t ld,
+                                       int32_t kind, int64_t dprime, double* gram, int64_t ld_gram, void* stream);
+SPN_API spn_status spn_gram_error(const double* exact, const double* approx, int64_t count, int64_t ld, double* err,
+                                  void* stream);
 
 /* ------------------------------------------------------------------ sketched Newton
  * Logistic regression with spinner-sketched Hessians (newton_sketch.hpp:13-86).

@@ -315,6 +315,29 @@ class Reference:
                                         threads))
         return out
 
+    def gram_exact(self, points, kind, sigma=1.0):
+        p = np.ascontiguousarray(points, dtype=np.float32)
+        out = np.zeros((p.shape[0], p.shape[0]))
+        self._check(self.lib.ref_gram_exact(p.ctypes.data_as(C.c_void_p), i64(p.shape[0]), i64(p.shape[1]),
+                                            cint(kind), dbl(sigma), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def gram_approx(self, variant, n, dprime, seed, kind, sigma, points):
+        p = np.ascontiguousarray(points, dtype=np.float32)
+        out = np.zeros((p.shape[0], p.shape[0]))
+        self._check(self.lib.ref_gram_approx(cint(variant), i64(n), i64(dprime), u64(seed), cint(kind), dbl(sigma),
+                                             p.ctypes.data_as(C.c_void_p), i64(p.shape[0]),
+                                             out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def gram_error(self, exact, approx):
+        a = np.ascontiguousarray(exact, dtype=np.float64)
+        b = np.ascontiguousarray(approx, dtype=np.float64)
+        err = C.c_double()
+        self._check(self.lib.ref_gram_error(a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+                                            i64(a.shape[0]), C.byref(err)))
+        return err.value
+
     def collision_curve(self, variant, n, m, xs, ys, dist, trials, seed, buckets=25, max_distance=2.0):
         """lsh.cpp:38-74 (the reference's own collision_curve + make_hasher_factory)."""
         xs = np.ascontiguousarray(xs, dtype=np.float32)

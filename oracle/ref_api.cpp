@@ -266,6 +266,54 @@ int ref_batch_chain(std::int64_t n, const double* d1, const double* d2, const do
   }
 }
 
+// gram_exact / gram_approx / gram_error (kernels.cpp:38-114), the reference's own code.
+// points [count][dim] fp32 rows; kind 0 = gaussian(sigma), 1 = angular; out [count][count].
+int ref_gram_exact(const float* points, std::int64_t count, std::int64_t dim, int kind, double sigma, double* out) {
+  try {
+    std::vector<Vec64> pts;
+    for (std::int64_t i = 0; i < count; ++i) pts.push_back(row_of(points, dim, i, dim, dim));
+    Eigen::MatrixXd g = gram_exact(pts, kind == 1 ? KernelKind::angular() : KernelKind::gaussian(sigma));
+    for (std::int64_t i = 0; i < count; ++i)
+      for (std::int64_t j = 0; j < count; ++j) out[i * count + j] = g(i, j);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_gram_approx(int variant, std::int64_t n, std::int64_t dprime, std::uint64_t seed, int kind, double sigma,
+                    const float* points, std::int64_t count, double* out) {
+  try {
+    std::vector<Vec64> pts;
+    for (std::int64_t i = 0; i < count; ++i) pts.push_back(row_of(points, n, i, n, n));
+    FeatureMap fm{StackedSpinner(variant_of(variant), static_cast<std::size_t>(n),
+                                 std::min(static_cast<std::size_t>(n), static_cast<std::size_t>(dprime)),
+                                 static_cast<std::size_t>(dprime), seed),
+                  kind == 1 ? KernelKind::angular() : KernelKind::gaussian(sigma)};
+    Eigen::MatrixXd g = gram_approx(fm, pts);
+    for (std::int64_t i = 0; i < count; ++i)
+      for (std::int64_t j = 0; j < count; ++j) out[i * count + j] = g(i, j);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_gram_error(const double* exact, const double* approx, std::int64_t count, double* err) {
+  try {
+    Eigen::MatrixXd a(count, count), b(count, count);
+    for (std::int64_t i = 0; i < count; ++i)
+      for (std::int64_t j = 0; j < count; ++j) {
+        a(i, j) = exact[i * count + j];
+        b(i, j) = approx[i * count + j];
+      }
+    *err = gram_error(a, b);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // collision_curve(pairs, make_hasher_factory(v, n, m), trials, seed, buckets, max_distance)
 // (lsh.cpp:38-74), the reference's own driver.  xs / ys: [pairs][n] fp32 rows.
 int ref_collision_curve(int variant, std::int64_t n, std::int64_t m, const float* xs, const float* ys,

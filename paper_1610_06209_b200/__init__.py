@@ -89,7 +89,8 @@ ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_c
                "spn_check_rows_f32", "spn_realize_block", "spn_newton_create", "spn_newton_destroy",
                "spn_logistic_eval_f32", "spn_hessian_sqrt_f32", "spn_sketched_step_f32", "spn_logistic_line_f32",
                "spn_ar1_problem", "spn_newton_set_problem", "spn_logistic_eval_host", "spn_hessian_sqrt_host",
-               "spn_sketched_step_host", "spn_logistic_line_host", "spn_collision_hits_f32")
+               "spn_sketched_step_host", "spn_logistic_line_host", "spn_collision_hits_f32", "spn_gram_exact_f32",
+               "spn_gram_approx_f32", "spn_gram_error")
 
 
 # ----------------------------------------------------------------------- errors
@@ -522,6 +523,65 @@ def embed(fm: FeatureMap, x, out=None, stream=None):
     return fm.projector.plan.embed(fm.kind.tag, fm.kind.sigma, x, out=out, stream=stream)
 
 
+_gram_exact = _sig("spn_gram_exact_f32", C.c_int, [_vp, _i64, _i64, _i64, _i32, _dbl, _vp, _i64, _vp])
+_gram_approx = _sig("spn_gram_approx_f32", C.c_int, [_vp, _i64, _i64, _i64, _i32, _i64, _vp, _i64, _vp])
+_gram_error = _sig("spn_gram_error", C.c_int, [_vp, _vp, _i64, _i64, C.POINTER(_dbl), _vp])
+
+
+def _points_dev(points, device=0):
+    torch = _torch()
+    host = not _is_cuda(points)
+    t = points if not host else torch.from_numpy(np.ascontiguousarray(np.asarray(points, dtype=np.float32)))
+    t = t.to(device=f"cuda:{device}" if host else t.device, dtype=torch.float32)
+    if t.dim() != 2:
+        raise DimensionError("expected a [count, dim] point set")
+    return t.contiguous(), host
+
+
+def gram_exact(points, kind: KernelKind, stream=None):
+    """kernels.cpp:38-76: exact kernel matrix (fp64 [count, count]) of fp32 points."""
+    torch = _torch()
+    p, host = _points_dev(points)
+    if p.shape[0] < 1:
+        raise DimensionError("gram_exact: empty dataset")
+    if kind.tag == KernelKind.angular_tag and bool(((check_rows(p) & 2) != 0).any()):
+        raise DomainError("gram_exact: angular kernel undefined at the zero vector")
+    if bool(((check_rows(p) & 1) != 0).any()):
+        raise DomainError("gram_exact: non-finite entry")
+    g = torch.empty((p.shape[0], p.shape[0]), dtype=torch.float64, device=p.device)
+    _check(_gram_exact(p.data_ptr(), p.shape[0], p.shape[1], p.stride(0), kind.tag, kind.sigma, g.data_ptr(),
+                       g.stride(0), _stream_ptr(stream)))
+    return g.cpu().numpy() if host else g
+
+
+def gram_approx(fm: FeatureMap, points, stream=None):
+    """kernels.cpp:78-103: features = embed(fm, points) on the device, then F F^T
+    (gaussian) or 1/2 + F F^T / (2 d') (angular), diagonal 1, in fp64."""
+    torch = _torch()
+    p, host = _points_dev(points, fm.projector.plan.device)
+    if p.shape[0] < 1:
+        raise DimensionError("gram_approx: empty dataset")
+    f = embed(fm, p, stream=stream)
+    g = torch.empty((p.shape[0], p.shape[0]), dtype=torch.float64, device=p.device)
+    _check(_gram_approx(f.data_ptr(), f.shape[0], f.shape[1], f.stride(0), fm.kind.tag, fm.projector.plan.k,
+                        g.data_ptr(), g.stride(0), _stream_ptr(stream)))
+    return g.cpu().numpy() if host else g
+
+
+def gram_error(exact, approx, stream=None) -> float:
+    """kernels.cpp:105-112: ||K - K_approx||_F / ||K||_F."""
+    torch = _torch()
+    a = exact if _is_cuda(exact) else torch.from_numpy(np.ascontiguousarray(exact, dtype=np.float64)).cuda()
+    b = approx if _is_cuda(approx) else torch.from_numpy(np.ascontiguousarray(approx, dtype=np.float64)).cuda()
+    a = a.to(torch.float64).contiguous()
+    b = b.to(device=a.device, dtype=torch.float64).contiguous()
+    if a.shape != b.shape or a.dim() != 2 or a.shape[0] != a.shape[1]:
+        raise DimensionError("gram_error: shape mismatch")
+    err = _dbl()
+    _check(_gram_error(a.data_ptr(), b.data_ptr(), a.shape[0], a.stride(0), C.byref(err), _stream_ptr(stream)))
+    return err.value
+
+
 class SketchOperator:
     """newton_sketch.hpp:50-71 (the spinner sketch; `rows` output rows).
 
@@ -573,7 +633,7 @@ __all__ = [
     "SpinnerError", "SingularSystemError", "variant_from_string", "version", "LIB_PATH", "ABI_SYMBOLS",
     "LogisticProblem", "SketchConfig", "NewtonTrace", "loss", "gradient", "hessian_sqrt", "sketched_step", "solve",
     "generate_ar1_problem", "HashedPair", "CollisionCurve", "FamilyComparison", "collision_curve",
-    "compare_families",
+    "compare_families", "gram_exact", "gram_approx", "gram_error",
 ]
 
 from .collision import (CollisionCurve, FamilyComparison, HashedPair, collision_curve,  # noqa: E402
