@@ -173,6 +173,14 @@ SPN_API spn_status spn_gram_approx_f32(const float* features, int64_t count, int
                                        int32_t kind, int64_t dprime, double* gram, int64_t ld_gram, void* stream);
 SPN_API spn_status spn_gram_error(const double* exact, const double* approx, int64_t count, int64_t ld, double* err,
                                   void* stream);
+/* Host-buffer forms (synchronous): points [count][dim] fp32, gram [count][count] fp64.
+ * spn_gram_approx_host embeds with `plan` (a FeatureMap's projector; kind/sigma as in
+ * spn_embed_f32) and forms the approximate Gram matrix on the device. */
+SPN_API spn_status spn_gram_exact_host(const float* points, int64_t count, int64_t dim, int32_t kind, double sigma,
+                                       double* gram);
+SPN_API spn_status spn_gram_approx_host(const spn_plan* plan, int32_t kind, double sigma, const float* points,
+                                        int64_t count, int64_t dim, double* gram);
+SPN_API spn_status spn_gram_error_host(const double* exact, const double* approx, int64_t count, double* err);
 
 /* ------------------------------------------------------------------ sketched Newton
  * Logistic regression with spinner-sketched Hessians (newton_sketch.hpp:13-86).

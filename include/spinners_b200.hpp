@@ -408,6 +408,62 @@ inline std::vector<int64_t> sample_rows(std::int64_t N, std::int64_t m, std::uin
   return out;
 }
 
+// ------------------------------------------------------------------ Gram matrices
+// kernels.hpp:35-41 without Eigen: a dense row-major count x count matrix.
+struct GramMatrix {
+  std::size_t n = 0;
+  std::vector<double> v;
+  double operator()(std::size_t i, std::size_t j) const { return v[i * n + j]; }
+  std::size_t rows() const { return n; }
+  std::size_t cols() const { return n; }
+};
+
+namespace detail {
+inline std::vector<float> pack_points(const std::vector<Vec64>& points, const char* what) {
+  if (points.empty()) throw DimensionError(std::string(what) + ": empty dataset");
+  const std::size_t dim = points.front().size();
+  std::vector<float> f(points.size() * dim);
+  for (std::size_t i = 0; i < points.size(); ++i) {
+    if (points[i].size() != dim) throw DimensionError(std::string(what) + ": ragged dataset");
+    check_finite(points[i], what);
+    for (std::size_t t = 0; t < dim; ++t) f[i * dim + t] = static_cast<float>(points[i][t]);
+  }
+  return f;
+}
+}  // namespace detail
+
+inline GramMatrix gram_exact(const std::vector<Vec64>& points, const KernelKind& kind) {  // kernels.cpp:38-76
+  std::vector<float> f = detail::pack_points(points, "gram_exact");
+  if (kind.tag == KernelKind::Tag::angular)
+    for (const auto& p : points) {
+      bool zero = true;
+      for (double e : p) zero = zero && e == 0.0;
+      if (zero) throw DomainError("gram_exact: angular kernel undefined at the zero vector");
+    }
+  GramMatrix g{points.size(), std::vector<double>(points.size() * points.size())};
+  check(spn_gram_exact_host(f.data(), static_cast<int64_t>(points.size()), static_cast<int64_t>(points[0].size()),
+                            kind.tag == KernelKind::Tag::angular ? SPN_EMBED_ANGULAR : SPN_EMBED_GAUSSIAN,
+                            kind.sigma, g.v.data()));
+  return g;
+}
+
+inline GramMatrix gram_approx(const FeatureMap& fm, const std::vector<Vec64>& points) {  // kernels.cpp:78-103
+  std::vector<float> f = detail::pack_points(points, "gram_approx");
+  GramMatrix g{points.size(), std::vector<double>(points.size() * points.size())};
+  check(spn_gram_approx_host(fm.projector.plan(),
+                             fm.kind.tag == KernelKind::Tag::angular ? SPN_EMBED_ANGULAR : SPN_EMBED_GAUSSIAN,
+                             fm.kind.sigma, f.data(), static_cast<int64_t>(points.size()),
+                             static_cast<int64_t>(points[0].size()), g.v.data()));
+  return g;
+}
+
+inline double gram_error(const GramMatrix& exact, const GramMatrix& approx) {  // kernels.cpp:105-112
+  if (exact.n != approx.n) throw DimensionError("gram_error: shape mismatch");
+  double err = 0.0;
+  check(spn_gram_error_host(exact.v.data(), approx.v.data(), static_cast<int64_t>(exact.n), &err));
+  return err;
+}
+
 // ------------------------------------------------------------------ sketched Newton
 // newton_sketch.hpp:13-86 / newton_sketch.cpp:28-204.  Features are a row-major
 // n x d host matrix (no Eigen); the problem is uploaded once (fp32) to a device

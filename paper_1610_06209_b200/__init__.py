@@ -90,7 +90,8 @@ ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_c
                "spn_logistic_eval_f32", "spn_hessian_sqrt_f32", "spn_sketched_step_f32", "spn_logistic_line_f32",
                "spn_ar1_problem", "spn_newton_set_problem", "spn_logistic_eval_host", "spn_hessian_sqrt_host",
                "spn_sketched_step_host", "spn_logistic_line_host", "spn_collision_hits_f32", "spn_gram_exact_f32",
-               "spn_gram_approx_f32", "spn_gram_error")
+               "spn_gram_approx_f32", "spn_gram_error", "spn_gram_exact_host", "spn_gram_approx_host",
+               "spn_gram_error_host")
 
 
 # ----------------------------------------------------------------------- errors

@@ -238,4 +238,64 @@ spn_status spn_gram_error(const double* exact, const double* approx, int64_t cou
   return SPN_OK;
 }
 
+// ------------------------------------------------------------- host-buffer forms
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+}  // namespace
+
+spn_status spn_gram_exact_host(const float* points, int64_t count, int64_t dim, int32_t kind, double sigma,
+                               double* gram) {
+  if (!points || !gram) return fail(SPN_EINVAL, "null pointer");
+  if (count < 1) return fail(SPN_EDIM, "gram_exact: empty dataset");
+  DevBuf dp, dg;
+  GRAM_CUDA(cudaMalloc(&dp.p, sizeof(float) * static_cast<size_t>(count * dim)));
+  GRAM_CUDA(cudaMalloc(&dg.p, sizeof(double) * static_cast<size_t>(count * count)));
+  GRAM_CUDA(cudaMemcpy(dp.p, points, sizeof(float) * static_cast<size_t>(count * dim), cudaMemcpyHostToDevice));
+  if (spn_status st = spn_gram_exact_f32(static_cast<float*>(dp.p), count, dim, dim, kind, sigma,
+                                         static_cast<double*>(dg.p), count, nullptr))
+    return st;
+  GRAM_CUDA(cudaMemcpy(gram, dg.p, sizeof(double) * static_cast<size_t>(count * count), cudaMemcpyDeviceToHost));
+  return SPN_OK;
+}
+
+spn_status spn_gram_approx_host(const spn_plan* plan, int32_t kind, double sigma, const float* points, int64_t count,
+                                int64_t dim, double* gram) {
+  if (!plan || !points || !gram) return fail(SPN_EINVAL, "null pointer");
+  if (count < 1) return fail(SPN_EDIM, "gram_approx: empty dataset");
+  int64_t n = 0, m = 0, k = 0, tables = 0, blocks = 0;
+  double scale = 0.0;
+  if (spn_status st = spn_plan_query(plan, &n, &m, &k, &tables, &blocks, &scale)) return st;
+  const int64_t width = kind == SPN_EMBED_GAUSSIAN ? 2 * k : k;
+  DevBuf dp, df, dg;
+  GRAM_CUDA(cudaMalloc(&dp.p, sizeof(float) * static_cast<size_t>(count * dim)));
+  GRAM_CUDA(cudaMalloc(&df.p, sizeof(float) * static_cast<size_t>(count * width)));
+  GRAM_CUDA(cudaMalloc(&dg.p, sizeof(double) * static_cast<size_t>(count * count)));
+  GRAM_CUDA(cudaMemcpy(dp.p, points, sizeof(float) * static_cast<size_t>(count * dim), cudaMemcpyHostToDevice));
+  if (spn_status st = spn_embed_f32(plan, kind, sigma, static_cast<float*>(dp.p), count, dim, dim,
+                                    static_cast<float*>(df.p), width, nullptr))
+    return st;
+  if (spn_status st = spn_gram_approx_f32(static_cast<float*>(df.p), count, width, width, kind, k,
+                                          static_cast<double*>(dg.p), count, nullptr))
+    return st;
+  GRAM_CUDA(cudaMemcpy(gram, dg.p, sizeof(double) * static_cast<size_t>(count * count), cudaMemcpyDeviceToHost));
+  return SPN_OK;
+}
+
+spn_status spn_gram_error_host(const double* exact, const double* approx, int64_t count, double* err) {
+  if (!exact || !approx || !err) return fail(SPN_EINVAL, "null pointer");
+  if (count < 1) return fail(SPN_EDIM, "gram_error: shape mismatch");
+  DevBuf da, db;
+  const size_t bytes = sizeof(double) * static_cast<size_t>(count * count);
+  GRAM_CUDA(cudaMalloc(&da.p, bytes));
+  GRAM_CUDA(cudaMalloc(&db.p, bytes));
+  GRAM_CUDA(cudaMemcpy(da.p, exact, bytes, cudaMemcpyHostToDevice));
+  GRAM_CUDA(cudaMemcpy(db.p, approx, bytes, cudaMemcpyHostToDevice));
+  return spn_gram_error(static_cast<double*>(da.p), static_cast<double*>(db.p), count, count, err, nullptr);
+}
+
 }  // extern "C"

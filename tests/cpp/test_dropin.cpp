@@ -239,6 +239,21 @@ int main() {
     CHECK(throws<DimensionError>([&] { collision_curve(same, factory, 0, 1); }));
   });
 
+  test_case("gram_exact / gram_approx / gram_error (test_kernels.cpp:55-133)", [] {
+    Vec64 a = {1.0, 0.0}, b = {0.0, 1.0};
+    GramMatrix ka = gram_exact({a, a, b}, KernelKind::angular());
+    CHECK(std::abs(ka(0, 1) - 1.0) < 1e-15 && std::abs(ka(0, 2) - 0.5) < 1e-15);
+    CHECK(throws<DomainError>([] { gram_exact({Vec64{0.0, 0.0}}, KernelKind::angular()); }));
+    FeatureMap fm{StackedSpinner(SpinnerVariant::hd3_hd2_hd1, 8, 8, 8, 8), KernelKind::angular()};
+    Vec64 x = random_vec(8, 9), neg(8);
+    for (std::size_t i = 0; i < 8; ++i) neg[i] = -x[i];
+    GramMatrix k = gram_approx(fm, {x, neg});
+    CHECK(k(0, 0) == 1.0 && k(1, 1) == 1.0 && std::abs(k(0, 1)) < 1e-15);
+    GramMatrix id{2, {1.0, 0.0, 0.0, 1.0}}, kt{2, {1.0, 0.1, 0.1, 1.0}};
+    CHECK(gram_error(id, id) == 0.0);
+    CHECK(std::abs(gram_error(id, kt) - 0.1) < 1e-13);
+  });
+
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ALL PASSED", g_fail);
   return g_fail ? 1 : 0;
 }
