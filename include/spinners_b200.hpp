@@ -58,9 +58,23 @@ inline void check_finite(const Vec64& x, const char* what) {  // common.hpp:37-4
     if (!std::isfinite(v)) throw DomainError(std::string(what) + ": non-finite entry");
 }
 
-enum class SpinnerVariant { hd3_hd2_hd1 = SPN_HD3_HD2_HD1, hdg_hd2_hd1 = SPN_HDG_HD2_HD1, gauss3 = SPN_GAUSS3 };
+enum class SpinnerVariant {  // spinner.hpp:18-25
+  hd3_hd2_hd1 = SPN_HD3_HD2_HD1,
+  hdg_hd2_hd1 = SPN_HDG_HD2_HD1,
+  gcirc_d2_hd1 = SPN_GCIRC_D2_HD1,
+  gtoeplitz_d2_hd1 = SPN_GTOEPLITZ_D2_HD1,
+  gskew_circ_d2_hd1 = SPN_GSKEW_CIRC_D2_HD1,
+  gaussian_dense = SPN_GAUSSIAN_DENSE,
+  gauss3 = SPN_GAUSS3
+};
 
-inline double default_scale(SpinnerVariant, std::size_t n) { return std::sqrt(static_cast<double>(n)); }
+inline bool has_hadamard(SpinnerVariant v) { return v != SpinnerVariant::gaussian_dense; }  // spinner.cpp:38
+
+inline double default_scale(SpinnerVariant v, std::size_t n) {  // spinner.cpp:40-45
+  if (v == SpinnerVariant::hd3_hd2_hd1 || v == SpinnerVariant::hdg_hd2_hd1 || v == SpinnerVariant::gauss3)
+    return std::sqrt(static_cast<double>(n));
+  return 1.0;
+}
 
 struct SpinnerSpec {  // spinner.hpp:40-53
   SpinnerVariant variant = SpinnerVariant::hd3_hd2_hd1;
@@ -76,7 +90,7 @@ struct SpinnerSpec {  // spinner.hpp:40-53
   void validate() const {  // spinner.cpp:59-67
     if (n < 1) throw DimensionError("SpinnerSpec: n must be >= 1");
     if (m < 1 || m > n) throw DimensionError("SpinnerSpec: need 1 <= m <= n");
-    if ((n & (n - 1)) != 0)
+    if (has_hadamard(variant) && (n & (n - 1)) != 0)
       throw DimensionError("SpinnerSpec: Hadamard-bearing variant requires power-of-two n, got " +
                            std::to_string(n));
     if (scale != 0.0 && !std::isfinite(scale)) throw DomainError("SpinnerSpec: non-finite scale");

@@ -42,8 +42,15 @@ int fail(const std::exception& e) {
   return 3;
 }
 
-SpinnerVariant variant_of(int v) {
-  return v == 1 ? SpinnerVariant::hdg_hd2_hd1 : SpinnerVariant::hd3_hd2_hd1;
+SpinnerVariant variant_of(int v) {  // spinner.hpp:18-25 order
+  switch (v) {
+    case 1: return SpinnerVariant::hdg_hd2_hd1;
+    case 2: return SpinnerVariant::gcirc_d2_hd1;
+    case 3: return SpinnerVariant::gtoeplitz_d2_hd1;
+    case 4: return SpinnerVariant::gskew_circ_d2_hd1;
+    case 5: return SpinnerVariant::gaussian_dense;
+    default: return SpinnerVariant::hd3_hd2_hd1;
+  }
 }
 
 Vec64 row_of(const float* x, std::int64_t ld, std::int64_t r, std::int64_t n_in, std::int64_t n) {

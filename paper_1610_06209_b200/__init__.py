@@ -141,14 +141,28 @@ def sample_rows(N: int, m: int, seed: int) -> np.ndarray:
 
 
 class SpinnerVariant(enum.IntEnum):
-    """spinner.hpp:18-25 (the Hadamard-only variants) + the all-Gaussian config-5 variant."""
+    """spinner.hpp:18-25 (the full family) + the builder-defined all-Gaussian config-5 variant."""
     hd3_hd2_hd1 = 0
     hdg_hd2_hd1 = 1
+    gcirc_d2_hd1 = 2
+    gtoeplitz_d2_hd1 = 3
+    gskew_circ_d2_hd1 = 4
+    gaussian_dense = 5
     gauss3 = 100  # builder-defined: D1..D3 iid N(0,1)
 
 
 _VARIANT_NAMES = {"HD3HD2HD1": SpinnerVariant.hd3_hd2_hd1, "HDgHD2HD1": SpinnerVariant.hdg_hd2_hd1,
-                  "Gauss3": SpinnerVariant.gauss3}
+                  "GcircD2HD1": SpinnerVariant.gcirc_d2_hd1, "GToeplitzD2HD1": SpinnerVariant.gtoeplitz_d2_hd1,
+                  "GSkewCircD2HD1": SpinnerVariant.gskew_circ_d2_hd1,
+                  "GaussianDense": SpinnerVariant.gaussian_dense, "Gauss3": SpinnerVariant.gauss3}
+
+
+def variant_to_string(v) -> str:
+    """spinner.cpp:9-19."""
+    for k, val in _VARIANT_NAMES.items():
+        if val == v:
+            return k
+    raise DomainError("to_string: unknown variant")
 
 
 def variant_from_string(s: str) -> SpinnerVariant:
@@ -345,14 +359,17 @@ class SpinnerSpec:
             raise DimensionError("SpinnerSpec: n must be >= 1")
         if self.m < 1 or self.m > self.n:
             raise DimensionError("SpinnerSpec: need 1 <= m <= n")
-        if self.n & (self.n - 1):
+        if self.variant != SpinnerVariant.gaussian_dense and self.n & (self.n - 1):
             raise DimensionError(
                 f"SpinnerSpec: Hadamard-bearing variant requires power-of-two n, got {self.n}")
         if self.scale != 0.0 and not math.isfinite(self.scale):
             raise DomainError("SpinnerSpec: non-finite scale")
 
-    def effective_scale(self):  # spinner.cpp:69-71
-        return self.scale if self.scale != 0.0 else math.sqrt(self.n)
+    def effective_scale(self):  # spinner.cpp:40-45,69-71
+        if self.scale != 0.0:
+            return self.scale
+        hadamard_only = self.variant in (SpinnerVariant.hd3_hd2_hd1, SpinnerVariant.hdg_hd2_hd1, SpinnerVariant.gauss3)
+        return math.sqrt(self.n) if hadamard_only else 1.0
 
 
 class StackedSpinner:
@@ -633,7 +650,7 @@ __all__ = [
     "embed", "SketchOperator", "mix_seed", "sample_rows", "realize_block", "check_rows", "DimensionError", "DomainError",
     "SpinnerError", "SingularSystemError", "variant_from_string", "version", "LIB_PATH", "ABI_SYMBOLS",
     "LogisticProblem", "SketchConfig", "NewtonTrace", "loss", "gradient", "hessian_sqrt", "sketched_step", "solve",
-    "generate_ar1_problem", "HashedPair", "CollisionCurve", "FamilyComparison", "collision_curve",
+    "generate_ar1_problem", "variant_to_string", "HashedPair", "CollisionCurve", "FamilyComparison", "collision_curve",
     "compare_families", "gram_exact", "gram_approx", "gram_error",
 ]
 

@@ -1,0 +1,499 @@
+// The rest of the spinner family: the circulant-family
+// variants G D2 H D1 with G a Gaussian circulant / Toeplitz / skew-circulant matrix
+// (proj/src/spinner.cpp:108-126, transforms.cpp:112-208) and the unstructured
+// Gaussian dense baseline (spinner.cpp:127-132,208-214).
+//
+// Circulant family: one CTA per (vector, table); the vector lives in shared memory as
+// complex fp32.  Per block: D1 -> normalised FWHT -> D2 -> the correlation with the
+// generator's first row / column through an in-house radix-2 FFT of length N (n, or 2n
+// for the Toeplitz embedding): forward DIF (natural -> bit-reversed), multiply by the
+// precomputed conj(spectrum) stored in bit-reversed order, inverse DIT (bit-reversed ->
+// natural), 1/N.  Twiddles come from an fp64-computed table (transforms.cpp:24-25 uses
+// the recurrence w *= wlen; the table is the exact e^{-2 pi i t / N} rounded once).
+// Dense baseline: a tiled fp32 GEMM Y = scale * X G^T per block, then the epilogue.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <vector>
+
+#include "../../include/spinners_b200.h"
+#include "errors.hpp"
+#include "family.hpp"
+
+namespace spn {
+
+namespace {
+
+constexpr int kFT = 256;  // threads per family CTA
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+  return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+
+struct FamParams {
+  const float* x;
+  int64_t ld_x, n_in, batch;
+  int n, N, logN, m, k, blocks, tables, kind;  // kind: 2 circ, 3 toeplitz, 4 skew
+  const float* d1;     // [tables][blocks][n]
+  const float* d2;
+  const float2* spec;  // [tables][blocks][N], bit-reversed order, conj applied
+  const float2* tw;    // [N/2]  e^{-2 pi i t / N}
+  const float2* skw;   // [n]    e^{+i pi t / n} (skew twiddle)
+  float scale;
+  int op;              // 0 apply, 1 hash, 2 embed gaussian, 3 embed angular
+  float inv_sigma, norm;
+  int relu;
+  void* out;
+  int64_t ld_out;
+};
+
+__global__ void __launch_bounds__(kFT) family_kernel(const FamParams p) {
+  extern __shared__ float2 c[];  // [N]
+  __shared__ float red_v[kFT];
+  __shared__ int red_i[kFT];
+  __shared__ float red_y[kFT];
+  const int tid = threadIdx.x;
+  const int64_t items = p.batch * (p.op == 1 ? p.tables : 1);
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t v = p.op == 1 ? item / p.tables : item;
+    const int tab = p.op == 1 ? (int)(item - v * p.tables) : 0;
+    const float* xrow = p.x + v * p.ld_x;
+    float best = -1.0f, bestv = 0.0f;
+    int besti = 0x7fffffff;
+    for (int b = 0; b < p.blocks; ++b) {
+      const int64_t tb = (int64_t)tab * p.blocks + b;
+      const float* D1 = p.d1 + tb * p.n;
+      const float* D2 = p.d2 + tb * p.n;
+      // D1, normalised FWHT (transforms.cpp:52-71), D2 (in the real parts)
+      for (int i = tid; i < p.N; i += kFT)
+        c[i] = make_float2(i < p.n && i < p.n_in ? xrow[i] * D1[i] : 0.0f, 0.0f);
+      __syncthreads();
+      for (int h = 1; h < p.n; h <<= 1) {
+        for (int q = tid; q < p.n / 2; q += kFT) {
+          const int i = (q / h) * 2 * h + (q % h);
+          const float u = c[i].x, w = c[i + h].x;
+          c[i].x = u + w;
+          c[i + h].x = u - w;
+        }
+        __syncthreads();
+      }
+      const float rn = rsqrtf((float)p.n);
+      for (int i = tid; i < p.n; i += kFT) {
+        float val = c[i].x * rn * D2[i];
+        c[i] = p.kind == 4 ? make_float2(val * p.skw[i].x, val * p.skw[i].y) : make_float2(val, 0.0f);
+      }
+      __syncthreads();
+      // forward DIF: natural -> bit-reversed
+      for (int len = p.N; len >= 2; len >>= 1) {
+        const int half = len >> 1, stride = p.N / len;
+        for (int q = tid; q < p.N / 2; q += kFT) {
+          const int blk = q / half, kk = q - blk * half, i = blk * len + kk;
+          const float2 u = c[i], w = c[i + half];
+          c[i] = make_float2(u.x + w.x, u.y + w.y);
+          c[i + half] = cmul(make_float2(u.x - w.x, u.y - w.y), p.tw[kk * stride]);
+        }
+        __syncthreads();
+      }
+      const float2* S = p.spec + tb * p.N;
+      for (int i = tid; i < p.N; i += kFT) c[i] = cmul(c[i], S[i]);
+      __syncthreads();
+      // inverse DIT: bit-reversed -> natural
+      for (int len = 2; len <= p.N; len <<= 1) {
+        const int half = len >> 1, stride = p.N / len;
+        for (int q = tid; q < p.N / 2; q += kFT) {
+          const int blk = q / half, kk = q - blk * half, i = blk * len + kk;
+          const float2 u = c[i], w = cmulc(c[i + half], p.tw[kk * stride]);
+          c[i] = make_float2(u.x + w.x, u.y + w.y);
+          c[i + half] = make_float2(u.x - w.x, u.y - w.y);
+        }
+        __syncthreads();
+      }
+      const float invN = 1.0f / (float)p.N;
+      const int rows = min(p.m, p.k - b * p.m);
+      for (int i = tid; i < rows; i += kFT) {
+        float2 z = c[i];
+        float y = p.kind == 4 ? (z.x * p.skw[i].x + z.y * p.skw[i].y) : z.x;  // real(z * conj(skw))
+        y = y * invN * p.scale;
+        const int64_t col = (int64_t)b * p.m + i;
+        if (p.op == 0) {
+          if (p.relu) y = fmaxf(y, 0.0f);
+          static_cast<float*>(p.out)[v * p.ld_out + col] = y;
+        } else if (p.op == 1) {
+          const float a = fabsf(y);
+          if (a > best || (a == best && (int)col < besti)) {
+            best = a;
+            besti = (int)col;
+            bestv = y;
+          }
+        } else if (p.op == 2) {
+          float sn, cs;
+          sincosf(y * p.inv_sigma, &sn, &cs);
+          float* o = static_cast<float*>(p.out) + v * p.ld_out;
+          o[col] = p.norm * cs;
+          o[p.k + col] = p.norm * sn;
+        } else {
+          static_cast<float*>(p.out)[v * p.ld_out + col] = y < 0.0f ? -1.0f : 1.0f;
+        }
+      }
+      __syncthreads();
+    }
+    if (p.op == 1) {  // signed argmax over the k rows (lsh.cpp:9-21): strict >, smallest index wins
+      red_v[tid] = best;
+      red_i[tid] = besti;
+      red_y[tid] = bestv;
+      __syncthreads();
+      for (int o = kFT / 2; o > 0; o >>= 1) {
+        if (tid < o) {
+          const float a = red_v[tid + o];
+          const int ai = red_i[tid + o];
+          if (a > red_v[tid] || (a == red_v[tid] && ai < red_i[tid])) {
+            red_v[tid] = a;
+            red_i[tid] = ai;
+            red_y[tid] = red_y[tid + o];
+          }
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {
+        const int id = red_i[0] + (red_y[0] < 0.0f ? p.k : 0);
+        static_cast<int32_t*>(p.out)[v * p.tables + tab] = id;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------------ dense baseline
+// Y[v][b*m + i] = scale * sum_j G_b[i][j] x_v[j]   (64 x 64 output tiles, fp32 FMA)
+constexpr int kDT = 64, kDK = 16;
+
+__global__ void __launch_bounds__(256) dense_gemm_kernel(const float* __restrict__ X, int64_t ld_x, int64_t n_in,
+                                                         int64_t batch, const float* __restrict__ G, int64_t n,
+                                                         int64_t m, int64_t k, float scale, float* __restrict__ Y,
+                                                         int64_t ld_y) {
+  __shared__ float Xs[kDK][kDT + 1];
+  __shared__ float Gs[kDK][kDT + 1];
+  const int64_t v0 = (int64_t)blockIdx.x * kDT;
+  const int64_t c0 = (int64_t)blockIdx.y * kDT;  // output column (b*m + i) tile
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int64_t j0 = 0; j0 < n; j0 += kDK) {
+    for (int e = threadIdx.x; e < kDK * kDT; e += 256) {
+      const int r = e / kDK, jj = e - r * kDK;
+      const int64_t v = v0 + r, col = c0 + r, j = j0 + jj;
+      Xs[jj][r] = (v < batch && j < n && j < n_in) ? X[v * ld_x + j] : 0.0f;
+      float g = 0.0f;
+      if (col < k && j < n) {
+        const int64_t b = col / m, i = col - b * m;
+        g = G[(b * m + i) * n + j];
+      }
+      Gs[jj][r] = g;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < kDK; ++jj) {
+      float xa[4], ga[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) xa[a] = Xs[jj][ty * 4 + a];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ga[q] = Gs[jj][tx * 4 + q];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[a][q] = fmaf(xa[a], ga[q], acc[a][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t v = v0 + ty * 4 + a, col = c0 + tx * 4 + q;
+      if (v < batch && col < k) Y[v * ld_y + col] = scale * acc[a][q];
+    }
+}
+
+// epilogues on Y rows: relu copy / signed argmax / gaussian or angular features
+__global__ void __launch_bounds__(256) dense_epilogue_kernel(const float* __restrict__ Y, int64_t ld_y, int64_t batch,
+                                                             int64_t k, int op, int relu, float inv_sigma, float norm,
+                                                             void* out, int64_t ld_out, int tables, int tab) {
+  __shared__ float rv[256], ry[256];
+  __shared__ int ri[256];
+  for (int64_t v = blockIdx.x; v < batch; v += gridDim.x) {
+    const float* y = Y + v * ld_y;
+    float best = -1.0f, bv = 0.0f;
+    int bi = 0x7fffffff;
+    for (int64_t c = threadIdx.x; c < k; c += 256) {
+      const float t = y[c];
+      if (op == 0) {
+        static_cast<float*>(out)[v * ld_out + c] = relu ? fmaxf(t, 0.0f) : t;
+      } else if (op == 1) {
+        if (fabsf(t) > best) {
+          best = fabsf(t);
+          bi = (int)c;
+          bv = t;
+        }
+      } else if (op == 2) {
+        float sn, cs;
+        sincosf(t * inv_sigma, &sn, &cs);
+        static_cast<float*>(out)[v * ld_out + c] = norm * cs;
+        static_cast<float*>(out)[v * ld_out + k + c] = norm * sn;
+      } else {
+        static_cast<float*>(out)[v * ld_out + c] = t < 0.0f ? -1.0f : 1.0f;
+      }
+    }
+    if (op == 1) {
+      rv[threadIdx.x] = best;
+      ri[threadIdx.x] = bi;
+      ry[threadIdx.x] = bv;
+      __syncthreads();
+      for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+          const float a = rv[threadIdx.x + o];
+          const int ai = ri[threadIdx.x + o];
+          if (a > rv[threadIdx.x] || (a == rv[threadIdx.x] && ai < ri[threadIdx.x])) {
+            rv[threadIdx.x] = a;
+            ri[threadIdx.x] = ai;
+            ry[threadIdx.x] = ry[threadIdx.x + o];
+          }
+        }
+        __syncthreads();
+      }
+      if (threadIdx.x == 0)
+        static_cast<int32_t*>(out)[v * tables + tab] = ri[0] + (ry[0] < 0.0f ? (int)k : 0);
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host FFT (fp64)
+using cd = std::complex<double>;
+
+void fft_fp64(std::vector<cd>& a) {  // transforms.cpp:15-41 (forward), same bit reversal + butterflies
+  const size_t n = a.size();
+  for (size_t i = 1, j = 0; i < n; ++i) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (size_t len = 2; len <= n; len <<= 1) {
+    const double ang = -2.0 * M_PI / static_cast<double>(len);
+    const cd wlen(std::cos(ang), std::sin(ang));
+    for (size_t i = 0; i < n; i += len) {
+      cd w(1.0, 0.0);
+      for (size_t kk = 0; kk < len / 2; ++kk) {
+        const cd u = a[i + kk], v = a[i + kk + len / 2] * w;
+        a[i + kk] = u + v;
+        a[i + kk + len / 2] = u - v;
+        w *= wlen;
+      }
+    }
+  }
+}
+
+size_t bitrev(size_t i, int bits) {
+  size_t r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((i >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+
+template <class T>
+cudaError_t upload(const std::vector<T>& h, T** d) {
+  cudaError_t e = cudaMalloc(d, h.size() * sizeof(T));
+  if (e == cudaSuccess) e = cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+}  // namespace
+
+struct FamilyPlan {
+  int variant = 0, device = 0, sms = 148;
+  int64_t n = 0, m = 0, k = 0, tables = 0, blocks = 0;
+  int N = 0, logN = 0;
+  double scale = 1.0;
+  float *d1 = nullptr, *d2 = nullptr, *dense = nullptr;
+  float2 *spec = nullptr, *tw = nullptr, *skw = nullptr;
+  ~FamilyPlan() {
+    for (void* q : {(void*)d1, (void*)d2, (void*)dense, (void*)spec, (void*)tw, (void*)skw})
+      if (q) cudaFree(q);
+  }
+};
+
+bool family_variant(int v) { return v >= SPN_GCIRC_D2_HD1 && v <= SPN_GAUSSIAN_DENSE; }
+
+// draw_tail + StructuredSpinner::build (spinner.cpp:92-151) for the family variants.
+void family_realize(int variant, int64_t n, int64_t m, uint64_t spec_seed, double* d1, double* d2, double* tail,
+                    double* trow, double* dense) {
+  if (variant != SPN_GAUSSIAN_DENSE) {
+    HostRng front(mix_seed(spec_seed, 1));
+    for (int64_t i = 0; i < n; ++i) d1[i] = front.rademacher();
+    for (int64_t i = 0; i < n; ++i) d2[i] = front.rademacher();
+  }
+  HostRng rng(mix_seed(spec_seed, 2));
+  switch (variant) {
+    case SPN_GCIRC_D2_HD1:
+    case SPN_GSKEW_CIRC_D2_HD1:
+      for (int64_t i = 0; i < n; ++i) tail[i] = rng.gaussian();
+      break;
+    case SPN_GTOEPLITZ_D2_HD1:
+      for (int64_t i = 0; i < n; ++i) tail[i] = rng.gaussian();
+      trow[0] = tail[0];
+      for (int64_t i = 1; i < n; ++i) trow[i] = rng.gaussian();
+      break;
+    case SPN_GAUSSIAN_DENSE:
+      for (int64_t i = 0; i < m * n; ++i) dense[i] = rng.gaussian();
+      break;
+  }
+}
+
+spn_status family_build(FamilyPlan** out, int variant, int64_t n, int64_t m, int64_t k, int64_t tables,
+                        int64_t blocks, const std::vector<double>* d, const std::vector<double>& trow,
+                        const std::vector<double>& dense, double scale, int device) {
+  auto* f = new FamilyPlan();
+  f->variant = variant;
+  f->n = n;
+  f->m = m;
+  f->k = k;
+  f->tables = tables;
+  f->blocks = blocks;
+  f->scale = scale;
+  f->device = device;
+  cudaDeviceGetAttribute(&f->sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaSuccess;
+  const int64_t tb = tables * blocks;
+  if (variant == SPN_GAUSSIAN_DENSE) {
+    std::vector<float> g(dense.begin(), dense.end());
+    e = upload(g, &f->dense);
+  } else {
+    int lg = 0;
+    while ((int64_t(1) << lg) < n) ++lg;
+    const int N = variant == SPN_GTOEPLITZ_D2_HD1 ? int(2 * n) : int(n);
+    f->N = N;
+    f->logN = variant == SPN_GTOEPLITZ_D2_HD1 ? lg + 1 : lg;
+    std::vector<float> a(d[0].begin(), d[0].end()), b(d[1].begin(), d[1].end());
+    e = upload(a, &f->d1);
+    if (e == cudaSuccess) e = upload(b, &f->d2);
+    // spectra: conj(FFT(first row / embedded row / twiddled row)) (transforms.cpp:116-157), bit-reversed
+    std::vector<float2> spec(static_cast<size_t>(tb * N));
+    std::vector<cd> z(static_cast<size_t>(N));
+    for (int64_t q = 0; q < tb && e == cudaSuccess; ++q) {
+      const double* r = d[2].data() + q * n;
+      std::fill(z.begin(), z.end(), cd(0.0, 0.0));
+      if (variant == SPN_GCIRC_D2_HD1) {
+        for (int64_t i = 0; i < n; ++i) z[i] = cd(r[i], 0.0);
+      } else if (variant == SPN_GTOEPLITZ_D2_HD1) {
+        // first_col = tail, first_row = trow: r_emb[k] = row[k], r_emb[N-k] = col[k]
+        const double* row = trow.data() + q * n;
+        for (int64_t i = 0; i < n; ++i) z[i] = cd(row[i], 0.0);
+        for (int64_t i = 1; i < n; ++i) z[N - i] = cd(r[i], 0.0);
+      } else {
+        for (int64_t i = 0; i < n; ++i) {
+          const double ang = M_PI * static_cast<double>(i) / static_cast<double>(n);
+          z[i] = r[i] * cd(std::cos(ang), std::sin(ang));
+        }
+      }
+      fft_fp64(z);
+      for (int j = 0; j < N; ++j) {
+        const cd s = std::conj(z[bitrev(static_cast<size_t>(j), f->logN)]);
+        spec[static_cast<size_t>(q * N + j)] = make_float2(static_cast<float>(s.real()), static_cast<float>(s.imag()));
+      }
+    }
+    std::vector<float2> tw(static_cast<size_t>(N / 2 > 0 ? N / 2 : 1));
+    for (int t = 0; t < N / 2; ++t) {
+      const double ang = -2.0 * M_PI * t / N;
+      tw[t] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+    }
+    std::vector<float2> skw(static_cast<size_t>(n));
+    for (int64_t t = 0; t < n; ++t) {
+      const double ang = M_PI * static_cast<double>(t) / static_cast<double>(n);
+      skw[t] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+    }
+    if (e == cudaSuccess) e = upload(spec, &f->spec);
+    if (e == cudaSuccess) e = upload(tw, &f->tw);
+    if (e == cudaSuccess) e = upload(skw, &f->skw);
+  }
+  if (e != cudaSuccess) {
+    delete f;
+    return cuda_error(e, "family plan upload");
+  }
+  *out = f;
+  return SPN_OK;
+}
+
+void family_destroy(FamilyPlan* f) { delete f; }
+
+spn_status family_run(const FamilyPlan* f, int op, const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
+                      void* out, int64_t ld_out, int relu, double sigma, cudaStream_t s) {
+  if (batch == 0) return SPN_OK;
+  const float inv_sigma = op == 2 ? static_cast<float>(1.0 / sigma) : 0.0f;
+  const float norm = static_cast<float>(1.0 / std::sqrt(static_cast<double>(f->k)));
+  if (f->variant == SPN_GAUSSIAN_DENSE) {
+    float* Y = nullptr;
+    const bool direct = op == 0 && !relu;
+    if (!direct) {
+      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&Y), sizeof(float) * static_cast<size_t>(batch * f->k), s);
+      if (e != cudaSuccess) return cuda_error(e, "dense scratch");
+    }
+    const int passes = op == 1 ? static_cast<int>(f->tables) : 1;
+    for (int t = 0; t < passes; ++t) {
+      float* dst = direct ? static_cast<float*>(out) : Y;
+      const int64_t ld = direct ? ld_out : f->k;
+      const dim3 grid(static_cast<unsigned>((batch + kDT - 1) / kDT), static_cast<unsigned>((f->k + kDT - 1) / kDT));
+      dense_gemm_kernel<<<grid, 256, 0, s>>>(x, ld_x, n_in, batch, f->dense + t * f->blocks * f->m * f->n, f->n, f->m,
+                                              f->k, static_cast<float>(f->scale), dst, ld);
+      if (!direct) {
+        const int64_t g = std::min<int64_t>(batch, int64_t(f->sms) * 8);
+        dense_epilogue_kernel<<<static_cast<unsigned>(g), 256, 0, s>>>(Y, f->k, batch, f->k, op, relu, inv_sigma,
+                                                                       norm, out, ld_out, static_cast<int>(f->tables),
+                                                                       t);
+      }
+    }
+    cudaError_t e = cudaGetLastError();
+    if (Y) cudaFreeAsync(Y, s);
+    return e == cudaSuccess ? SPN_OK : cuda_error(e, "dense baseline");
+  }
+  FamParams p{};
+  p.x = x;
+  p.ld_x = ld_x;
+  p.n_in = n_in;
+  p.batch = batch;
+  p.n = static_cast<int>(f->n);
+  p.N = f->N;
+  p.logN = f->logN;
+  p.m = static_cast<int>(f->m);
+  p.k = static_cast<int>(f->k);
+  p.blocks = static_cast<int>(f->blocks);
+  p.tables = static_cast<int>(f->tables);
+  p.kind = f->variant;
+  p.d1 = f->d1;
+  p.d2 = f->d2;
+  p.spec = f->spec;
+  p.tw = f->tw;
+  p.skw = f->skw;
+  p.scale = static_cast<float>(f->scale);
+  p.op = op;
+  p.inv_sigma = inv_sigma;
+  p.norm = norm;
+  p.relu = relu;
+  p.out = out;
+  p.ld_out = ld_out;
+  const size_t smem = sizeof(float2) * static_cast<size_t>(f->N);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(family_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  const int64_t items = batch * (op == 1 ? f->tables : 1);
+  const int64_t grid = std::min<int64_t>(items, int64_t(f->sms) * 4);
+  family_kernel<<<static_cast<unsigned>(grid), kFT, smem, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SPN_OK : cuda_error(e, "circulant family");
+}
+
+}  // namespace spn

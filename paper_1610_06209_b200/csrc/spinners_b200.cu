@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "errors.hpp"
+#include "family.hpp"
 #include "host_params.hpp"
 #include "internal.hpp"
 #include "spinner_big.cuh"
@@ -69,6 +70,9 @@ struct spn_plan {
   int sms = 0;
   std::vector<double> d[3];  // realised fp64 diagonals [tables][blocks][n]
   int dsign[3] = {0, 0, 0};
+  // circulant family / dense baseline (family.cu): Toeplitz first rows, dense matrices
+  std::vector<double> trow, dense;
+  spn::FamilyPlan* fam = nullptr;
 
   // vector-kernel layouts (n <= 2^14): [diag][layout]
   uint32_t* vsgn[3][2] = {};
@@ -85,6 +89,7 @@ struct spn_plan {
 
   ~spn_plan() {
     DeviceGuard g(device);
+    if (fam) spn::family_destroy(fam);
     for (auto& a : vsgn)
       for (auto* p : a)
         if (p) cudaFree(p);
@@ -189,6 +194,9 @@ spn_status finish_plan(spn_plan* p) {
   DeviceGuard g(p->device);
   if (!g.ok) return fail(SPN_ECUDA, "cudaSetDevice failed");
   SPN_CUDA(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device));
+  if (spn::family_variant(p->variant))
+    return spn::family_build(&p->fam, p->variant, p->n, p->m, p->k, p->tables, p->blocks, p->d, p->trow, p->dense,
+                             p->scale, p->device);
   if (p->log_n <= kMaxLogNVec) return build_vec_layouts(p);
   return p->big.build(p->n, p->tables * p->blocks, p->d, p->dsign);
 }
@@ -294,9 +302,17 @@ spn_status spn_realize_block(int32_t variant, int64_t n, uint64_t spec_seed, dou
 spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) {
   if (!out || !d) return fail(SPN_EINVAL, "null argument");
   *out = nullptr;
-  if (d->variant != SPN_HD3_HD2_HD1 && d->variant != SPN_HDG_HD2_HD1 && d->variant != SPN_GAUSS3)
+  const bool fam = spn::family_variant(d->variant);
+  if (d->variant != SPN_HD3_HD2_HD1 && d->variant != SPN_HDG_HD2_HD1 && d->variant != SPN_GAUSS3 && !fam)
     return fail(SPN_EDOMAIN, "unknown spinner variant " + std::to_string(d->variant));
-  if (spn_status s = validate_shape(d->n, d->m, d->k, d->tables)) return s;
+  if (d->variant == SPN_GAUSSIAN_DENSE) {  // no Hadamard stage: any n >= 1 (spinner.cpp:59-67)
+    if (d->n < 1 || d->m < 1 || d->m > d->n) return fail(SPN_EDIM, "SpinnerSpec: need 1 <= m <= n");
+    if (d->k < 1 || d->tables < 1) return fail(SPN_EDIM, "k and tables must be >= 1");
+  } else if (spn_status s = validate_shape(d->n, d->m, d->k, d->tables)) {
+    return s;
+  }
+  if (fam && d->variant != SPN_GAUSSIAN_DENSE && d->n > (d->variant == SPN_GTOEPLITZ_D2_HD1 ? 8192 : 16384))
+    return fail(SPN_EUNSUPPORTED, "circulant family: n > 2^14 (Toeplitz 2^13) not supported");
   if (!d->table_seeds && d->tables != 1) return fail(SPN_EINVAL, "tables > 1 needs table_seeds");
   if (d->scale != 0.0 && !std::isfinite(d->scale)) return fail(SPN_EDOMAIN, "non-finite scale");
   auto* p = new spn_plan();
@@ -307,16 +323,25 @@ spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) {
   p->tables = d->tables;
   p->blocks = (d->k + d->m - 1) / d->m;
   p->device = d->device;
-  // default_scale: sqrt(n) for the Hadamard-only variants (spinner.cpp:41-45,69-71)
-  p->scale = d->scale != 0.0 ? d->scale : std::sqrt(static_cast<double>(d->n));
+  // default_scale: sqrt(n) for the Hadamard-only variants, 1 for the circulant family and
+  // the dense baseline (spinner.cpp:41-45,69-71)
+  p->scale = d->scale != 0.0 ? d->scale : (fam ? 1.0 : std::sqrt(static_cast<double>(d->n)));
   const int64_t per = p->blocks * p->n;
   for (auto& v : p->d) v.resize(static_cast<size_t>(p->tables * per));
+  if (d->variant == SPN_GTOEPLITZ_D2_HD1) p->trow.resize(static_cast<size_t>(p->tables * per));
+  if (d->variant == SPN_GAUSSIAN_DENSE) p->dense.resize(static_cast<size_t>(p->tables * p->blocks * p->m * p->n));
   for (int64_t t = 0; t < p->tables; ++t) {
     const uint64_t seed = d->table_seeds ? d->table_seeds[t] : d->seed;
     for (int64_t b = 0; b < p->blocks; ++b) {
       const int64_t off = t * per + b * p->n;
-      spn::realize_block(d->variant, p->n, spn::mix_seed(seed, static_cast<uint64_t>(b)),
-                         p->d[0].data() + off, p->d[1].data() + off, p->d[2].data() + off);
+      const uint64_t spec_seed = spn::mix_seed(seed, static_cast<uint64_t>(b));
+      if (fam)
+        spn::family_realize(d->variant, p->n, p->m, spec_seed, p->d[0].data() + off, p->d[1].data() + off,
+                            p->d[2].data() + off, p->trow.empty() ? nullptr : p->trow.data() + off,
+                            p->dense.empty() ? nullptr : p->dense.data() + (t * p->blocks + b) * p->m * p->n);
+      else
+        spn::realize_block(d->variant, p->n, spec_seed, p->d[0].data() + off, p->d[1].data() + off,
+                           p->d[2].data() + off);
     }
   }
   if (spn_status s = finish_plan(p)) {
@@ -392,6 +417,10 @@ spn_status spn_apply_f32(const spn_plan* p, const float* x, int64_t batch, int64
   if (p->tables != 1) return fail(SPN_EINVAL, "apply needs a single-table plan");
   if (batch > 0 && !y) return fail(SPN_EINVAL, "null output");
   if (ld_y < p->k) return fail(SPN_EINVAL, "ld_y < k");
+  if (p->fam) {
+    DeviceGuard g(p->device);
+    return spn::family_run(p->fam, 0, x, batch, ld_x, n_in, y, ld_y, relu, 0.0, static_cast<cudaStream_t>(stream));
+  }
   if (p->log_n > kMaxLogNVec) {
     DeviceGuard g(p->device);
     return const_cast<spn_plan*>(p)->big.apply(x, batch, ld_x, n_in, y, ld_y, relu, p->k, p->m, p->blocks,
@@ -413,6 +442,12 @@ spn_status spn_hash_f32(const spn_plan* p, const float* x, int64_t batch, int64_
                         int64_t n_in, int32_t* ids, float* y, int64_t ld_y, void* stream) {
   if (spn_status s = check_io(p, x, batch, ld_x, n_in)) return s;
   if (batch > 0 && !ids) return fail(SPN_EINVAL, "null ids");
+  if (p->fam) {
+    if (y) return fail(SPN_EUNSUPPORTED, "hash with y output: circulant family / dense baseline");
+    if (p->k >= (int64_t(1) << 30)) return fail(SPN_EDIM, "2k must fit int32 ids");
+    DeviceGuard g(p->device);
+    return spn::family_run(p->fam, 1, x, batch, ld_x, n_in, ids, p->tables, 0, 0.0, static_cast<cudaStream_t>(stream));
+  }
   if (y && p->tables != 1) return fail(SPN_EINVAL, "y output needs a single-table plan");
   if (y && ld_y < p->k) return fail(SPN_EINVAL, "ld_y < k");
   if (p->k >= (int64_t(1) << 30)) return fail(SPN_EDIM, "2k must fit int32 ids");
@@ -476,6 +511,11 @@ spn_status spn_embed_f32(const spn_plan* p, int32_t kind, double sigma, const fl
     return fail(SPN_EDOMAIN, "KernelKind: sigma must be positive");  // kernels.hpp:17
   if (batch > 0 && !out) return fail(SPN_EINVAL, "null output");
   if (ld_out < (kind == SPN_EMBED_GAUSSIAN ? 2 * p->k : p->k)) return fail(SPN_EINVAL, "ld_out too small");
+  if (p->fam) {
+    DeviceGuard g(p->device);
+    return spn::family_run(p->fam, kind == SPN_EMBED_GAUSSIAN ? 2 : 3, x, batch, ld_x, n_in, out, ld_out, 0, sigma,
+                           static_cast<cudaStream_t>(stream));
+  }
   if (p->log_n > kMaxLogNVec) return fail(SPN_EUNSUPPORTED, "embed with n > 2^14 not implemented");
   spn::VecParams v = base_params(p);
   v.x = x;
@@ -506,6 +546,7 @@ spn_status spn_sketch_f32(const spn_plan* p, const float* a, int64_t n_in, int64
                           const int64_t* rows, int64_t m_out, double norm, float* out,
                           int64_t ld_out, void* stream) {
   if (!p) return fail(SPN_EINVAL, "null plan");
+  if (p->fam) return fail(SPN_EUNSUPPORTED, "sketch: Hadamard-only variants (HD3/HDg) on the device");
   if (p->tables != 1 || p->blocks != 1) return fail(SPN_EUNSUPPORTED, "sketch needs one table of one block");
   if (n_in < 1 || n_in > p->n) return fail(SPN_EDIM, "SketchOperator::apply: row count mismatch");
   if (d < 0 || m_out < 0 || m_out > p->n) return fail(SPN_EDIM, "bad sketch shape");
@@ -534,6 +575,7 @@ int plan_device(const spn_plan* p) { return p->device; }
 spn_status plan_sketch_scaled(const spn_plan* p, const float* a, int64_t n_in, int64_t d, int64_t ld_a,
                               int64_t m_out, double norm, const float* row_scale, float* out, int64_t ld_out,
                               cudaStream_t s) {
+  if (p->fam) return fail(SPN_EUNSUPPORTED, "sketch: Hadamard-only variants (HD3/HDg) on the device");
   if (p->tables != 1 || p->blocks != 1) return fail(SPN_EUNSUPPORTED, "sketch needs one table of one block");
   if (n_in < 1 || n_in > p->n) return fail(SPN_EDIM, "SketchOperator::apply: row count mismatch");
   if (m_out > p->k || m_out > p->n) return fail(SPN_EDIM, "sketch rows exceed the plan");
