@@ -365,6 +365,17 @@ class SpinnerSpec:
         if self.scale != 0.0 and not math.isfinite(self.scale):
             raise DomainError("SpinnerSpec: non-finite scale")
 
+    def to_json(self) -> dict:  # spinner.cpp:72-78 (the wire format of specs)
+        return {"variant": variant_to_string(self.variant), "n": self.n, "m": self.m, "seed": self.seed,
+                "scale": self.effective_scale()}
+
+    @staticmethod
+    def from_json(j: dict) -> "SpinnerSpec":  # spinner.cpp:80-89
+        s = SpinnerSpec(variant_from_string(j["variant"]), int(j["n"]), int(j["m"]), int(j["seed"]),
+                        float(j.get("scale", 0.0)))
+        s.validate()
+        return s
+
     def effective_scale(self):  # spinner.cpp:40-45,69-71
         if self.scale != 0.0:
             return self.scale

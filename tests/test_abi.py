@@ -105,3 +105,16 @@ def test_signed_argmax_host_helper(spn):
     assert spn.signed_argmax([-2.0, 2.0]) == (0, -1)
     assert spn.signed_argmax([0.0, 0.0]) == (0, 1)
     assert spn.decode_id(1030, 1024) == (6, -1) and spn.decode_id(6, 1024) == (6, 1)
+
+
+def test_spec_json_round_trip(spn):
+    """SpinnerSpec::to_json / from_json (spinner.cpp:72-89)."""
+    import json
+    for v in ("HD3HD2HD1", "GToeplitzD2HD1", "GaussianDense"):
+        s = spn.SpinnerSpec.make(spn.variant_from_string(v), 64, 32, 7)
+        j = json.loads(json.dumps(s.to_json()))
+        assert j["variant"] == v and j["scale"] == s.effective_scale()
+        t = spn.SpinnerSpec.from_json(j)
+        assert (t.variant, t.n, t.m, t.seed, t.effective_scale()) == (s.variant, 64, 32, 7, s.effective_scale())
+    with pytest.raises(spn.DomainError):
+        spn.SpinnerSpec.from_json({"variant": "Nope", "n": 4, "m": 4, "seed": 0})
