@@ -71,6 +71,8 @@ struct ColParams {
   float cscale;
   int64_t rows_valid;    // EPI_Y: flat elements < rows_valid are stored
   int relu;
+  int pdl;               // launch with programmatic dependent launch (vector path: c5 1.366 -> 1.323 ms;
+                         // the sketch path measured slightly slower with it, so it stays off there)
   // filled by set_tiling(): fast division by nstripes, log2 of nlo / nhi (powers of two)
   uint32_t fd_m, fd_l;
   int lg_nlo, lg_nhi;
@@ -637,6 +639,7 @@ struct BigPlan {
           cp.nhi = 1;
           cp.nlo = 1;
           cp.nvec = nv;
+          cp.pdl = 1;
           cp.dd[1] = stile2 + b * n;
           const bool tma = lr >= 5 && al16(y, ld_y);
           e = tma ? launch_tcol_ls(lr, SC_VMID, cp, sms, s) : launch_scol_ls(lr, SC_VMID, cp, sms, s);

@@ -7,6 +7,8 @@
 // the register-only kernels there are the fallback.
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -14,6 +16,39 @@
 #include "spinner_vec.cuh"
 
 namespace spn {
+
+// Programmatic dependent launch between consecutive passes of one stream: each pass lets
+// its successor start launching immediately and waits for its predecessor's completion
+// (and memory flush) before touching data — the successor's launch and prologue overlap
+// the predecessor's tail.  Both instructions are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPN_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class K, class... A>
+inline cudaError_t launch_pdl(bool pdl, K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                              A... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 // ----------------------------------------------------------------- staged column pass
 // Tile = 2^LS rows (transformed sub-index s) x 32 contiguous columns; thread (w, lane)
@@ -103,6 +138,7 @@ __device__ __forceinline__ void stage_tile(const ColParams& p, const TileIdx& ti
 // in layout A; SD_ROW diagonals are one value per row, [(lo*nhi + hi)*S + s].
 template <int LS, int NPARTS, int DMASK, bool START_B, int DMODE, int EPI>
 __global__ void __launch_bounds__(SColCfg<LS>::THREADS, SColCfg<LS>::MIN_CTAS) colpass_staged_kernel(const ColParams p) {
+  pdl_enter();
   using C = SColCfg<LS>;
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -237,6 +273,7 @@ struct RowParams2 {
 
 template <int LR, int LT, int PROG>
 __global__ void __launch_bounds__(1 << LT) rowpass_staged_kernel(const RowParams2 p) {
+  pdl_enter();
   using C = VCfg<LR, LT>;
   static_assert(C::GPC == 1, "one segment per CTA");
   extern __shared__ __align__(16) float smem[];
@@ -327,8 +364,7 @@ inline cudaError_t launch_scol(const ColParams& p_in, int sms, cudaStream_t s) {
   }
   const int64_t tiles = p.nvec * p.nhi * p.nlo * p.nstripes;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sms) * occ));
-  kern<<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(p.pdl != 0, kern, static_cast<unsigned>(grid), C::THREADS, C::SMEM, s, p);
 }
 
 // Programs: sketch P1 ([D] H), sketch P2/P3 (H [D] H), sketch P4 (H, gather), sketch
@@ -377,8 +413,7 @@ inline cudaError_t launch_srow(const RowParams2& p, int sms, cudaStream_t s) {
   }
   const int64_t items = p.nvec * p.nseg;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(items, int64_t(sms) * occ));
-  kern<<<static_cast<unsigned>(grid), C::T, smem, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(true, kern, static_cast<unsigned>(grid), C::T, smem, s, p);
 }
 
 // threads per row segment: one warp up to 2^11 floats, two warps (R = T = 64) at 2^12

@@ -152,6 +152,7 @@ __device__ __forceinline__ void tma_issue_tile(const CUtensorMap* m, const TileI
 template <int LS, int NPARTS, int DMASK, bool START_B, int DMODE, int EPI>
 __global__ void __launch_bounds__(SColCfg<LS>::THREADS, TmaCfg<LS>::MIN_CTAS)
     colpass_tma_kernel(const ColParams p, const __grid_constant__ TmaMaps tm) {
+  pdl_enter();
   using C = SColCfg<LS>;
   using T = TmaCfg<LS>;
   constexpr int NB = T::NBUF;  // tiles in flight: NB-1 loads ahead of the compute
@@ -324,9 +325,8 @@ inline cudaError_t launch_tcol(const ColParams& p_in, int sms, cudaStream_t s, b
   }
   const int64_t tiles = p.nvec * p.nhi * p.nlo * p.nstripes;
   const int64_t grid = tiles < int64_t(sms) * occ ? (tiles < 1 ? 1 : tiles) : int64_t(sms) * occ;
-  kern<<<static_cast<unsigned>(grid), C::THREADS, T::SMEM, s>>>(p, tm);
   *done = true;
-  return cudaGetLastError();
+  return launch_pdl(p.pdl != 0, kern, static_cast<unsigned>(grid), C::THREADS, T::SMEM, s, p, tm);
 }
 
 template <int LS>
