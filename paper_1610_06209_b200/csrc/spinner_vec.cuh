@@ -440,6 +440,7 @@ __device__ __forceinline__ void embed_store_perm(const float (&r)[C::R], float* 
     __sincosf(r[4 * q + 1], &s4.y, &c4.y);
     __sincosf(r[4 * q + 2], &s4.z, &c4.z);
     __sincosf(r[4 * q + 3], &s4.w, &c4.w);
+    // (packed FMUL2 for these measured slower: 0.437 vs 0.431 ms)
     c4.x *= p.norm;
     c4.y *= p.norm;
     c4.z *= p.norm;
