@@ -203,6 +203,10 @@ class Workload:
             self.xk = torch.full((cfg["d"],), 0.01, dtype=torch.float64, device="cuda")
             self.vectors = cfg["d"]  # columns sketched per iteration
             self.t = 0
+            import concurrent.futures
+            self.pool = concurrent.futures.ThreadPoolExecutor(1)  # next sketch realised during this step
+            self.mk = lambda it: spn.SketchOperator(V.hd3_hd2_hd1, cfg["N"], cfg["m"], spn.mix_seed(3, it))  # noqa: E731
+            self.pending = self.pool.submit(self.mk, 0)
             # pass over A + 4 sketch passes + line-search pass per iteration (launch count is a lower bound)
             self.launches_per_step = 16
         elif name == "c7":
@@ -246,9 +250,9 @@ class Workload:
                                             stream=stream)
         if self.name == "c6":  # newton_sketch.cpp:155-170, one iteration
             cfg, nt = self.cfg, self.newton
-            sk = self.spn.SketchOperator(self.spn.SpinnerVariant.hd3_hd2_hd1, cfg["N"], cfg["m"],
-                                         self.spn.mix_seed(3, self.t))
+            sk = self.pending.result()
             self.t += 1
+            self.pending = self.pool.submit(self.mk, self.t)
             step, g, f = nt._step_dev(self.prob, self.xk, sk, stream)
             slope = float(self.torch.dot(g, step).item())
             s, _ = nt._backtrack(self.prob, self.xk, step, float(f.item()), slope, stream)

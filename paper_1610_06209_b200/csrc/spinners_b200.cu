@@ -330,20 +330,25 @@ spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) {
   for (auto& v : p->d) v.resize(static_cast<size_t>(p->tables * per));
   if (d->variant == SPN_GTOEPLITZ_D2_HD1) p->trow.resize(static_cast<size_t>(p->tables * per));
   if (d->variant == SPN_GAUSSIAN_DENSE) p->dense.resize(static_cast<size_t>(p->tables * p->blocks * p->m * p->n));
-  for (int64_t t = 0; t < p->tables; ++t) {
+  // every (table, block) has its own generators: realise them in parallel when there is work
+  auto realize = [&](int64_t tb) {
+    const int64_t t = tb / p->blocks, b = tb - t * p->blocks;
     const uint64_t seed = d->table_seeds ? d->table_seeds[t] : d->seed;
-    for (int64_t b = 0; b < p->blocks; ++b) {
-      const int64_t off = t * per + b * p->n;
-      const uint64_t spec_seed = spn::mix_seed(seed, static_cast<uint64_t>(b));
-      if (fam)
-        spn::family_realize(d->variant, p->n, p->m, spec_seed, p->d[0].data() + off, p->d[1].data() + off,
-                            p->d[2].data() + off, p->trow.empty() ? nullptr : p->trow.data() + off,
-                            p->dense.empty() ? nullptr : p->dense.data() + (t * p->blocks + b) * p->m * p->n);
-      else
-        spn::realize_block(d->variant, p->n, spec_seed, p->d[0].data() + off, p->d[1].data() + off,
-                           p->d[2].data() + off);
-    }
-  }
+    const int64_t off = t * per + b * p->n;
+    const uint64_t spec_seed = spn::mix_seed(seed, static_cast<uint64_t>(b));
+    if (fam)
+      spn::family_realize(d->variant, p->n, p->m, spec_seed, p->d[0].data() + off, p->d[1].data() + off,
+                          p->d[2].data() + off, p->trow.empty() ? nullptr : p->trow.data() + off,
+                          p->dense.empty() ? nullptr : p->dense.data() + (t * p->blocks + b) * p->m * p->n);
+    else
+      spn::realize_block(d->variant, p->n, spec_seed, p->d[0].data() + off, p->d[1].data() + off,
+                         p->d[2].data() + off);
+  };
+  const int64_t nblk = p->tables * p->blocks;
+  if (nblk > 1 && nblk * p->n >= (int64_t(1) << 16))
+    spn::parallel_for(nblk, realize);
+  else
+    for (int64_t i = 0; i < nblk; ++i) realize(i);
   if (spn_status s = finish_plan(p)) {
     delete p;
     return s;

@@ -23,6 +23,7 @@ runs in the sm_100a library.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import ctypes as C
 import dataclasses
 import time
@@ -237,11 +238,19 @@ def solve(p: LogisticProblem, cfg: SketchConfig, stream=None) -> NewtonTrace:
 
     trace = NewtonTrace(f_star=f_star)
     x = torch.zeros(d, dtype=torch.float64, device=f"cuda:{p.device}")
+    # fresh sketch every iteration (.cpp:155-157); its seed is known in advance, so the next
+    # iteration's operator is realised on a host thread while this one runs on the GPU
+    pool = concurrent.futures.ThreadPoolExecutor(1) if cfg.sketch_variant is not None else None
+    make = lambda it: SketchOperator(cfg.sketch_variant, n, cfg.sketch_rows, mix_seed(cfg.seed, it),  # noqa: E731
+                                     device=p.device)
+    pending = pool.submit(make, 0) if pool else None
     for t in range(cfg.max_iters):
         tic = time.perf_counter()
         sketch = None
-        if cfg.sketch_variant is not None:  # fresh sketch every iteration (.cpp:155-157)
-            sketch = SketchOperator(cfg.sketch_variant, n, cfg.sketch_rows, mix_seed(cfg.seed, t), device=p.device)
+        if pool is not None:
+            sketch = pending.result()
+            if t + 1 < cfg.max_iters:
+                pending = pool.submit(make, t + 1)
         step, g, f = _step_dev(p, x, sketch, stream)
         f0 = float(f.item())
         if cfg.line_search:
@@ -262,6 +271,8 @@ def solve(p: LogisticProblem, cfg: SketchConfig, stream=None) -> NewtonTrace:
         if f_next - f_star <= cfg.gap_tolerance:
             trace.converged = True
             break
+    if pool is not None:
+        pool.shutdown(wait=True)
     return trace
 
 
