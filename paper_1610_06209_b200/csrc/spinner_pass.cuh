@@ -271,14 +271,23 @@ struct RowParams2 {
   int relu;
 };
 
+#ifndef SPN_ROW_DIRECT
+#define SPN_ROW_DIRECT 1  // c5: 1.321 -> 1.316 ms (3 A/B pairs)
+#endif
+template <int PROG>
+struct RowCfg {  // direct loads (layout B, no smem staging) for the passes that start in layout B
+  static constexpr bool DIRECT = SPN_ROW_DIRECT && PROG != RP_FIRST;
+};
+
 template <int LR, int LT, int PROG>
 __global__ void __launch_bounds__(1 << LT) rowpass_staged_kernel(const RowParams2 p) {
   pdl_enter();
   using C = VCfg<LR, LT>;
   static_assert(C::GPC == 1, "one segment per CTA");
+  constexpr bool DIRECT = RowCfg<PROG>::DIRECT;
   extern __shared__ __align__(16) float smem[];
-  float* xb = smem;          // staging buffer (swizzled 16-B chunks)
-  float* sm = smem + C::N;   // transpose buffer
+  float* xb = smem;                          // staging buffer (swizzled 16-B chunks)
+  float* sm = DIRECT ? smem : smem + C::N;   // transpose buffer
   const int t = threadIdx.x;
   const int64_t items = p.nvec * p.nseg;
   const int lgseg = __ffsll(p.nseg) - 1;
@@ -291,11 +300,16 @@ __global__ void __launch_bounds__(1 << LT) rowpass_staged_kernel(const RowParams
     }
     stage_x<C>(xb, p.src + v * p.src_vstride + seg * C::N, valid, t);
   };
-  if ((int64_t)blockIdx.x < items) stage(blockIdx.x);
+  if (!DIRECT && (int64_t)blockIdx.x < items) stage(blockIdx.x);
   cp_async_commit();
   for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const int64_t v = item >> lgseg, seg = item & (p.nseg - 1);
     float r[C::R];
+    if constexpr (DIRECT) {
+      const float* src = p.src + v * p.src_vstride + seg * C::N + t;
+#pragma unroll
+      for (int j = 0; j < C::R; ++j) r[j] = __ldcg(src + j * C::T);
+    } else {
     cp_async_wait_all();
     group_sync<C>();
     {
@@ -317,6 +331,7 @@ __global__ void __launch_bounds__(1 << LT) rowpass_staged_kernel(const RowParams
     group_sync<C>();
     if (item + gridDim.x < items) stage(item + gridDim.x);
     cp_async_commit();
+    }
     if constexpr (PROG != RP_FIRST) fwht_B_to_A<C>(r, sm, t);
     if constexpr (PROG != RP_LAST) {
       const float4* f = reinterpret_cast<const float4*>(p.d + seg * C::N);
@@ -402,7 +417,7 @@ template <int LR, int LT, int PROG>
 inline cudaError_t launch_srow(const RowParams2& p, int sms, cudaStream_t s) {
   using C = VCfg<LR, LT>;
   auto kern = rowpass_staged_kernel<LR, LT, PROG>;
-  constexpr size_t smem = sizeof(float) * 2 * C::N;
+  constexpr size_t smem = sizeof(float) * (RowCfg<PROG>::DIRECT ? 1 : 2) * C::N;
   static int occ = 0;
   if (occ == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
