@@ -231,7 +231,7 @@ class Workload:
             self.x = torch.randn((cfg["batch"], cfg["n"]), device="cuda", generator=g)
             self.y = torch.empty_like(self.x)
             self.vectors = cfg["batch"]
-            G = max(1, min(cfg["batch"], (32 << 20) // (cfg["n"] * 4)))
+            G = max(1, min(cfg["batch"], (24 << 20) // (cfg["n"] * 4)))
             self.launches_per_step = 4 * math.ceil(cfg["batch"] / G)
         torch.cuda.synchronize()
 

@@ -346,14 +346,17 @@ inline cudaError_t launch_row(const RowParams& p, int sms, cudaStream_t s) {
 #include "spinner_tma.cuh"
 namespace spn {
 
-// L2-resident working set per pass group (default 32 MB; SPN_GROUP_MB overrides, for tuning).
-inline int64_t group_bytes() {
-  static const int64_t v = [] {
+// L2-resident working set per pass group: 24 MB for the vector passes (c5: 1.275 vs
+// 1.316 ms at 32 MB), 32 MB for the sketch's column groups (c4: 0.197 ms; 16/48/64 MB
+// slower).  SPN_GROUP_MB overrides both (tuning).
+inline int64_t group_bytes(bool sketch = false) {
+  static const int64_t env = [] {
     const char* e = std::getenv("SPN_GROUP_MB");
-    const int64_t mb = e ? std::atoll(e) : 32;
-    return (mb > 0 ? mb : 32) << 20;
+    const int64_t mb = e ? std::atoll(e) : 0;
+    return mb > 0 ? (mb << 20) : int64_t(0);
   }();
-  return v;
+  if (env) return env;
+  return sketch ? (int64_t(32) << 20) : (int64_t(24) << 20);
 }
 
 // Stream-ordered scratch (cudaMallocFromPoolAsync / cudaFreeAsync) from one pool per device
@@ -816,7 +819,7 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     return e == cudaSuccess ? SPN_OK : BigPlan::err(e, "sketch single pass");
   }
   // column groups of ~32 MB of workspace
-  int64_t dc = std::max<int64_t>(32, (group_bytes() / (nn * 4)) / 32 * 32);
+  int64_t dc = std::max<int64_t>(32, (group_bytes(true) / (nn * 4)) / 32 * 32);
   dc = std::min<int64_t>(dc, (dcols + 31) / 32 * 32);
   Scratch scratch;
   if (cudaError_t e = scratch.alloc(static_cast<size_t>(BigPlan::nstreams() * nn * dc * 4), s0))
