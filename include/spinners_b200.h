@@ -61,9 +61,9 @@ typedef enum spn_status {
 typedef enum spn_variant {
   SPN_HD3_HD2_HD1 = 0,       /* SpinnerVariant::hd3_hd2_hd1 (spinner.hpp:19) */
   SPN_HDG_HD2_HD1 = 1,       /* SpinnerVariant::hdg_hd2_hd1 (spinner.hpp:20) */
-  SPN_GCIRC_D2_HD1 = 2,      /* gcirc_d2_hd1: Gaussian circulant * D2 H D1 (spinner.hpp:21) */
-  SPN_GTOEPLITZ_D2_HD1 = 3,  /* gtoeplitz_d2_hd1 (spinner.hpp:22) */
-  SPN_GSKEW_CIRC_D2_HD1 = 4, /* gskew_circ_d2_hd1 (spinner.hpp:23) */
+  SPN_GCIRC_D2_HD1 = 2,      /* gcirc_d2_hd1: Gaussian circulant * D2 H D1 (spinner.hpp:21); n <= 2^13 */
+  SPN_GTOEPLITZ_D2_HD1 = 3,  /* gtoeplitz_d2_hd1 (spinner.hpp:22); n <= 2^12 */
+  SPN_GSKEW_CIRC_D2_HD1 = 4, /* gskew_circ_d2_hd1 (spinner.hpp:23); n <= 2^13 */
   SPN_GAUSSIAN_DENSE = 5,    /* gaussian_dense: the unstructured baseline (spinner.hpp:24) */
   SPN_GAUSS3 = 100     /* builder-defined: D1..D3 all N(0,1) (BASELINE config 5) */
 } spn_variant;

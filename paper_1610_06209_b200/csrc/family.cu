@@ -4,8 +4,10 @@
 // Gaussian dense baseline (spinner.cpp:127-132,208-214).
 //
 // Circulant family: one CTA per (vector, table); the vector lives in shared memory as
-// complex fp32.  Per block: D1 -> normalised FWHT -> D2 -> the correlation with the
-// generator's first row / column through an in-house radix-2 FFT of length N (n, or 2n
+// complex fp64 (N <= 2^13: 128 KB) — an fp32 FFT missed the 1e-5 feature bar (1.3-1.8e-5
+// at n = 2048: the cos/sin arguments |y|/sigma reach ~100, amplifying the FFT rounding).
+// Per block: D1 -> normalised FWHT -> D2 -> the correlation with the generator's first
+// row / column through an in-house radix-2 FFT of length N (n, or 2n
 // for the Toeplitz embedding): forward DIF (natural -> bit-reversed), multiply by the
 // precomputed conj(spectrum) stored in bit-reversed order, inverse DIT (bit-reversed ->
 // natural), 1/N.  Twiddles come from an fp64-computed table (transforms.cpp:24-25 uses
@@ -28,11 +30,11 @@ namespace {
 
 constexpr int kFT = 256;  // threads per family CTA
 
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
-__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
-  return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
 
 struct FamParams {
@@ -41,9 +43,9 @@ struct FamParams {
   int n, N, logN, m, k, blocks, tables, kind;  // kind: 2 circ, 3 toeplitz, 4 skew
   const float* d1;     // [tables][blocks][n]
   const float* d2;
-  const float2* spec;  // [tables][blocks][N], bit-reversed order, conj applied
-  const float2* tw;    // [N/2]  e^{-2 pi i t / N}
-  const float2* skw;   // [n]    e^{+i pi t / n} (skew twiddle)
+  const double2* spec;  // [tables][blocks][N], bit-reversed order, conj applied
+  const double2* tw;    // [N/2]  e^{-2 pi i t / N}
+  const double2* skw;   // [n]    e^{+i pi t / n} (skew twiddle)
   float scale;
   int op;              // 0 apply, 1 hash, 2 embed gaussian, 3 embed angular
   float inv_sigma, norm;
@@ -53,7 +55,7 @@ struct FamParams {
 };
 
 __global__ void __launch_bounds__(kFT) family_kernel(const FamParams p) {
-  extern __shared__ float2 c[];  // [N]
+  extern __shared__ double2 c[];  // [N]
   __shared__ float red_v[kFT];
   __shared__ int red_i[kFT];
   __shared__ float red_y[kFT];
@@ -71,21 +73,21 @@ __global__ void __launch_bounds__(kFT) family_kernel(const FamParams p) {
       const float* D2 = p.d2 + tb * p.n;
       // D1, normalised FWHT (transforms.cpp:52-71), D2 (in the real parts)
       for (int i = tid; i < p.N; i += kFT)
-        c[i] = make_float2(i < p.n && i < p.n_in ? xrow[i] * D1[i] : 0.0f, 0.0f);
+        c[i] = make_double2(i < p.n && i < p.n_in ? (double)xrow[i] * (double)D1[i] : 0.0, 0.0);
       __syncthreads();
       for (int h = 1; h < p.n; h <<= 1) {
         for (int q = tid; q < p.n / 2; q += kFT) {
           const int i = (q / h) * 2 * h + (q % h);
-          const float u = c[i].x, w = c[i + h].x;
+          const double u = c[i].x, w = c[i + h].x;
           c[i].x = u + w;
           c[i + h].x = u - w;
         }
         __syncthreads();
       }
-      const float rn = rsqrtf((float)p.n);
+      const double rn = 1.0 / sqrt((double)p.n);
       for (int i = tid; i < p.n; i += kFT) {
-        float val = c[i].x * rn * D2[i];
-        c[i] = p.kind == 4 ? make_float2(val * p.skw[i].x, val * p.skw[i].y) : make_float2(val, 0.0f);
+        const double val = c[i].x * rn * (double)D2[i];
+        c[i] = p.kind == 4 ? make_double2(val * p.skw[i].x, val * p.skw[i].y) : make_double2(val, 0.0);
       }
       __syncthreads();
       // forward DIF: natural -> bit-reversed
@@ -93,13 +95,13 @@ __global__ void __launch_bounds__(kFT) family_kernel(const FamParams p) {
         const int half = len >> 1, stride = p.N / len;
         for (int q = tid; q < p.N / 2; q += kFT) {
           const int blk = q / half, kk = q - blk * half, i = blk * len + kk;
-          const float2 u = c[i], w = c[i + half];
-          c[i] = make_float2(u.x + w.x, u.y + w.y);
-          c[i + half] = cmul(make_float2(u.x - w.x, u.y - w.y), p.tw[kk * stride]);
+          const double2 u = c[i], w = c[i + half];
+          c[i] = make_double2(u.x + w.x, u.y + w.y);
+          c[i + half] = cmul(make_double2(u.x - w.x, u.y - w.y), p.tw[kk * stride]);
         }
         __syncthreads();
       }
-      const float2* S = p.spec + tb * p.N;
+      const double2* S = p.spec + tb * p.N;
       for (int i = tid; i < p.N; i += kFT) c[i] = cmul(c[i], S[i]);
       __syncthreads();
       // inverse DIT: bit-reversed -> natural
@@ -107,18 +109,18 @@ __global__ void __launch_bounds__(kFT) family_kernel(const FamParams p) {
         const int half = len >> 1, stride = p.N / len;
         for (int q = tid; q < p.N / 2; q += kFT) {
           const int blk = q / half, kk = q - blk * half, i = blk * len + kk;
-          const float2 u = c[i], w = cmulc(c[i + half], p.tw[kk * stride]);
-          c[i] = make_float2(u.x + w.x, u.y + w.y);
-          c[i + half] = make_float2(u.x - w.x, u.y - w.y);
+          const double2 u = c[i], w = cmulc(c[i + half], p.tw[kk * stride]);
+          c[i] = make_double2(u.x + w.x, u.y + w.y);
+          c[i + half] = make_double2(u.x - w.x, u.y - w.y);
         }
         __syncthreads();
       }
-      const float invN = 1.0f / (float)p.N;
+      const double invN = 1.0 / (double)p.N;
       const int rows = min(p.m, p.k - b * p.m);
       for (int i = tid; i < rows; i += kFT) {
-        float2 z = c[i];
-        float y = p.kind == 4 ? (z.x * p.skw[i].x + z.y * p.skw[i].y) : z.x;  // real(z * conj(skw))
-        y = y * invN * p.scale;
+        const double2 z = c[i];
+        const double yd = p.kind == 4 ? (z.x * p.skw[i].x + z.y * p.skw[i].y) : z.x;  // real(z * conj(skw))
+        float y = (float)(yd * invN * (double)p.scale);
         const int64_t col = (int64_t)b * p.m + i;
         if (p.op == 0) {
           if (p.relu) y = fmaxf(y, 0.0f);
@@ -318,7 +320,7 @@ struct FamilyPlan {
   int N = 0, logN = 0;
   double scale = 1.0;
   float *d1 = nullptr, *d2 = nullptr, *dense = nullptr;
-  float2 *spec = nullptr, *tw = nullptr, *skw = nullptr;
+  double2 *spec = nullptr, *tw = nullptr, *skw = nullptr;
   ~FamilyPlan() {
     for (void* q : {(void*)d1, (void*)d2, (void*)dense, (void*)spec, (void*)tw, (void*)skw})
       if (q) cudaFree(q);
@@ -380,7 +382,7 @@ spn_status family_build(FamilyPlan** out, int variant, int64_t n, int64_t m, int
     e = upload(a, &f->d1);
     if (e == cudaSuccess) e = upload(b, &f->d2);
     // spectra: conj(FFT(first row / embedded row / twiddled row)) (transforms.cpp:116-157), bit-reversed
-    std::vector<float2> spec(static_cast<size_t>(tb * N));
+    std::vector<double2> spec(static_cast<size_t>(tb * N));
     std::vector<cd> z(static_cast<size_t>(N));
     for (int64_t q = 0; q < tb && e == cudaSuccess; ++q) {
       const double* r = d[2].data() + q * n;
@@ -401,18 +403,18 @@ spn_status family_build(FamilyPlan** out, int variant, int64_t n, int64_t m, int
       fft_fp64(z);
       for (int j = 0; j < N; ++j) {
         const cd s = std::conj(z[bitrev(static_cast<size_t>(j), f->logN)]);
-        spec[static_cast<size_t>(q * N + j)] = make_float2(static_cast<float>(s.real()), static_cast<float>(s.imag()));
+        spec[static_cast<size_t>(q * N + j)] = make_double2(s.real(), s.imag());
       }
     }
-    std::vector<float2> tw(static_cast<size_t>(N / 2 > 0 ? N / 2 : 1));
+    std::vector<double2> tw(static_cast<size_t>(N / 2 > 0 ? N / 2 : 1));
     for (int t = 0; t < N / 2; ++t) {
       const double ang = -2.0 * M_PI * t / N;
-      tw[t] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+      tw[t] = make_double2(std::cos(ang), std::sin(ang));
     }
-    std::vector<float2> skw(static_cast<size_t>(n));
+    std::vector<double2> skw(static_cast<size_t>(n));
     for (int64_t t = 0; t < n; ++t) {
       const double ang = M_PI * static_cast<double>(t) / static_cast<double>(n);
-      skw[t] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+      skw[t] = make_double2(std::cos(ang), std::sin(ang));
     }
     if (e == cudaSuccess) e = upload(spec, &f->spec);
     if (e == cudaSuccess) e = upload(tw, &f->tw);
@@ -483,10 +485,10 @@ spn_status family_run(const FamilyPlan* f, int op, const float* x, int64_t batch
   p.relu = relu;
   p.out = out;
   p.ld_out = ld_out;
-  const size_t smem = sizeof(float2) * static_cast<size_t>(f->N);
+  const size_t smem = sizeof(double2) * static_cast<size_t>(f->N);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(family_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(family_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 136 * 1024);
     attr = true;
   }
   const int64_t items = batch * (op == 1 ? f->tables : 1);

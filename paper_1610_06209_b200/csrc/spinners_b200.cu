@@ -311,8 +311,8 @@ spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) {
   } else if (spn_status s = validate_shape(d->n, d->m, d->k, d->tables)) {
     return s;
   }
-  if (fam && d->variant != SPN_GAUSSIAN_DENSE && d->n > (d->variant == SPN_GTOEPLITZ_D2_HD1 ? 8192 : 16384))
-    return fail(SPN_EUNSUPPORTED, "circulant family: n > 2^14 (Toeplitz 2^13) not supported");
+  if (fam && d->variant != SPN_GAUSSIAN_DENSE && d->n > (d->variant == SPN_GTOEPLITZ_D2_HD1 ? 4096 : 8192))
+    return fail(SPN_EUNSUPPORTED, "circulant family: n > 2^13 (Toeplitz 2^12) not supported (fp64 FFT in smem)");
   if (!d->table_seeds && d->tables != 1) return fail(SPN_EINVAL, "tables > 1 needs table_seeds");
   if (d->scale != 0.0 && !std::isfinite(d->scale)) return fail(SPN_EDOMAIN, "non-finite scale");
   auto* p = new spn_plan();

@@ -29,8 +29,8 @@ def torch():
     return t
 
 
-CASES = [(CIRC, 8, 8, 8), (CIRC, 64, 32, 96), (CIRC, 1024, 1024, 1024), (CIRC, 16384, 512, 512),
-         (TOEP, 16, 16, 16), (TOEP, 256, 100, 300), (TOEP, 8192, 1024, 1024),
+CASES = [(CIRC, 8, 8, 8), (CIRC, 64, 32, 96), (CIRC, 1024, 1024, 1024), (CIRC, 8192, 512, 512),
+         (TOEP, 16, 16, 16), (TOEP, 256, 100, 300), (TOEP, 4096, 1024, 1024),
          (SKEW, 8, 8, 8), (SKEW, 512, 512, 1024), (SKEW, 4096, 4096, 4096),
          (DENSE, 100, 50, 120), (DENSE, 256, 64, 64), (DENSE, 1024, 1024, 2048)]
 
@@ -76,6 +76,13 @@ def test_embed_matches_reference(spn, oracle, ref, torch, variant, n):
             assert row_rel(got, want).max() <= RTOL
         else:
             assert np.count_nonzero(got != want) <= 2  # sign flips only for |projection| ~ 0
+
+
+def test_family_size_limits(spn):
+    with pytest.raises(spn.SpinnerError):
+        spn.StackedSpinner(spn.SpinnerVariant.gcirc_d2_hd1, 16384, 16, 16, 1)
+    with pytest.raises(spn.SpinnerError):
+        spn.StackedSpinner(spn.SpinnerVariant.gtoeplitz_d2_hd1, 8192, 16, 16, 1)
 
 
 def test_default_scale_and_names(spn):
