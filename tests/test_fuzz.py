@@ -88,3 +88,43 @@ def test_fuzz_apply_hash_embed(spn, oracle, ref, torch, case):
                 scale = np.maximum(np.abs(proj).max(axis=1, keepdims=True), 1e-30)
                 flip = got != want
                 assert np.all(np.abs(proj[flip]) <= 1e-6 * np.broadcast_to(scale, proj.shape)[flip]), (variant, n)
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_fuzz_multipass_apply(spn, ref, oracle, torch, case):
+    """n = 2^15 .. 2^20 (the row/column pass path): random m, stacking, ragged n_in, strides, ReLU."""
+    rng = np.random.default_rng(5000 + case)
+    logn = int(rng.integers(15, 21))
+    n = 1 << logn
+    variant = int(rng.choice([0, 1]))
+    m = int(rng.integers(1, n + 1)) if rng.random() < 0.5 else n
+    k = m if rng.random() < 0.6 else min(2 * m + int(rng.integers(0, 7)), 3 * n)
+    batch = int(rng.integers(1, 4))
+    n_in = n if rng.random() < 0.5 else int(rng.integers(1, n + 1))
+    ld = n_in + (int(rng.integers(1, 9)) if rng.random() < 0.4 else 0)
+    relu = bool(rng.random() < 0.3)
+    seed = int(rng.integers(0, 2**62))
+    xs = oracle.gaussian_rows(7000 + case, batch, ld)
+    xd = torch.from_numpy(xs).cuda()
+    sp = spn.StackedSpinner(spn.SpinnerVariant(variant), n, m, k, seed)
+    y = sp.apply(xd[:, :n_in], relu=relu).cpu().numpy()
+    want = ref.apply(variant, n, m, k, seed, 0.0, xs[:, :n_in], n_in=n_in, relu=relu, threads=8)
+    assert row_rel(y, want).max() <= RTOL, (variant, n, m, k, n_in, relu)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_fuzz_sketch(spn, ref, oracle, torch, case):
+    """SketchOperator with random (non-pow2) input dims, ragged column counts, first-m and random P."""
+    rng = np.random.default_rng(9000 + case)
+    N_in = int(rng.integers(2, 1 << int(rng.integers(3, 18))))
+    padded = 1 << max(0, (N_in - 1).bit_length())
+    d = int(rng.integers(1, 300))
+    m = int(rng.integers(1, padded + 1))
+    mode = "first" if rng.random() < 0.5 else "random"
+    seed = int(rng.integers(0, 2**62))
+    a = oracle.gaussian_rows(9100 + case, N_in, d)
+    sk = spn.SketchOperator(spn.SpinnerVariant.hd3_hd2_hd1, N_in, m, seed, mode=mode, p_seed=seed + 1)
+    got = sk.apply(torch.from_numpy(a).cuda()).cpu().numpy()
+    rows = None if mode == "first" else sk.row_list
+    want = ref.sketch(0, a, m, seed, row_list=rows, threads=8)
+    assert row_rel(got.T, want.T).max() <= RTOL, (N_in, d, m, mode)
