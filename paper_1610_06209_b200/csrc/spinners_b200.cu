@@ -602,8 +602,13 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
   std::lock_guard<std::mutex> lock(p->mu);
   DeviceGuard g(p->device);
   const int64_t in_row = n_in * 4;
-  // ~48 MB of output per chunk keeps copies and kernels overlapped on PCIe/HBM.
-  int64_t chunk = std::max<int64_t>(1, (int64_t(48) << 20) / std::max<int64_t>(out_row_bytes, 1));
+  // Chunks of ~1/8 of the traffic, 4..48 MB (the larger of input / output row bytes): small
+  // calls still overlap H2D, kernel and D2H on the two copy engines; large ones keep the
+  // per-chunk launch/copy overhead small.
+  const int64_t row_bytes = std::max<int64_t>(std::max<int64_t>(out_row_bytes, in_row), 1);
+  const int64_t target = std::min<int64_t>(int64_t(48) << 20,
+                                           std::max<int64_t>(int64_t(4) << 20, batch * row_bytes / 8));
+  int64_t chunk = std::max<int64_t>(1, target / row_bytes);
   chunk = std::min(chunk, batch);
   for (int s = 0; s < 2; ++s) {
     if (!p->hs[s]) SPN_CUDA(cudaStreamCreateWithFlags(&p->hs[s], cudaStreamNonBlocking));
