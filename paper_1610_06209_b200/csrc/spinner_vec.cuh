@@ -50,6 +50,10 @@ struct VecParams {
   int x_vec_ok;        // x and ld_x 16-B aligned (cp.async staging allowed)
 };
 
+#ifndef SPN_EMBED_WARPS
+#define SPN_EMBED_WARPS 24  // n = 1024 embed register budget (resident warps / SM); 20/22/26 measured slower
+#endif
+
 template <int LOG_R_, int LOG_T_>
 struct VCfg {
   static constexpr int LOG_R = LOG_R_, LOG_T = LOG_T_, LOG_N = LOG_R + LOG_T;
@@ -66,7 +70,8 @@ struct VCfg {
   // apply; the embed kernels keep 24 (80 registers; at 72 they spill: 0.475 vs 0.443 ms)
   static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 28 : (R == 64 ? 12 : 12));
   __host__ __device__ static constexpr int min_ctas(int op) {
-    return (R == 32 && op >= 2) ? (24 / (THREADS / 32) > 0 ? 24 / (THREADS / 32) : 1) : MIN_CTAS_BASE;
+    return (R == 32 && op >= 2) ? (SPN_EMBED_WARPS / (THREADS / 32) > 0 ? SPN_EMBED_WARPS / (THREADS / 32) : 1)
+                                : MIN_CTAS_BASE;
   }
   // looped chain (one copy of the D -> H body, R == T only): keeps the n = 16384 kernel
   // (R = 128, fully unrolled ~57 KB of SASS) inside the 32 KB L1.5 instruction cache.
