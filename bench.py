@@ -154,7 +154,7 @@ class ClockSampler:
 class Workload:
     """Device-resident inputs/outputs for one config + a `step()` that launches the hot path."""
 
-    def __init__(self, name, cfg, rank, device):
+    def __init__(self, name, cfg, rank, device, world=1):
         import torch
         import paper_1610_06209_b200 as spn
         self.spn, self.torch, self.name, self.cfg = spn, torch, name, cfg
@@ -184,6 +184,16 @@ class Workload:
                 del blk
             self.ids = torch.empty((cfg["batch"], cfg["tables"]), device="cuda", dtype=torch.int32)
             self.vectors = cfg["batch"]
+            # multi-GPU: the all-gather of the codes fused into the hash kernel (peer stores over
+            # NVLink through CUDA IPC mappings); NCCL all_gather stays as the fallback
+            self.pc, self.rank, self.exchange = None, rank, None
+            if world > 1:
+                try:
+                    from paper_1610_06209_b200.shard import PeerCodes
+                    self.pc = PeerCodes(world * cfg["batch"], cfg["tables"], world, rank, device)
+                    self.exchange = "fused peer stores in the hash kernel (CUDA IPC / NVLink), one barrier"
+                except Exception as exc:  # pragma: no cover - depends on the node's IPC support
+                    self.exchange = f"nccl all_gather_into_tensor (peer mapping unavailable: {type(exc).__name__})"
         elif name == "c4":
             self.sk = spn.SketchOperator(V.hd3_hd2_hd1, cfg["N"], cfg["m"], 11 + rank, mode="random", p_seed=77)
             self.x = torch.randn((cfg["N"], cfg["d"]), device="cuda", generator=g)
@@ -241,6 +251,8 @@ class Workload:
         if self.name == "c2":
             return self.spn.embed(self.fm, self.x, out=self.out, stream=stream)
         if self.name == "c3":
+            if self.pc is not None:
+                return self.pc.hash(self.h, self.x, self.rank * self.cfg["batch"], stream=stream)
             return self.h.plan.hash(self.x, stream=stream)
         if self.name == "c4":
             return self.sk.apply(self.x, out=self.out, stream=stream)
@@ -264,7 +276,7 @@ class Workload:
 def run_ours(args, rank, world, local):
     import torch
     cfg = CONFIGS[args.config]
-    w = Workload(args.config, cfg, rank, local)
+    w = Workload(args.config, cfg, rank, local, world)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if cfg["flush"] else None
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -272,7 +284,8 @@ def run_ours(args, rank, world, local):
         # warm-up, continued (untimed) until nvidia-smi has seen the GPU under this load
         t_end = time.time() + 3.0
         i = 0
-        while i < max(3, args.warmup) or (len(clk.samples) < 3 and time.time() < t_end):
+        # (multi-rank: a fixed count — steps may contain collectives, so every rank must run as many)
+        while i < max(3, args.warmup) or (world == 1 and len(clk.samples) < 3 and time.time() < t_end):
             w.step(stream)
             i += 1
             if i >= max(3, args.warmup):
@@ -290,7 +303,7 @@ def run_ours(args, rank, world, local):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
     ids = None
-    if args.config == "c3" and world > 1:  # the real exchange step: all-gather the codes over NCCL
+    if args.config == "c3" and world > 1 and w.pc is None:  # exchange step: NCCL all-gather of the codes
         from paper_1610_06209_b200.shard import gather_codes
         ids = w.step(stream)
         t0 = torch.cuda.Event(enable_timing=True)
@@ -315,7 +328,8 @@ def run_ours(args, rank, world, local):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE config shapes)",
         "config": {"workload": cfg["workload"], "name": args.config, "vectors_per_gpu_step": w.vectors,
                    "l2": "L2 flushed (256 MB write) between timed steps" if cfg["flush"]
-                   else "inputs+outputs > 126 MB L2", "parallelism": f"dp{world} (independent shards)"},
+                   else "inputs+outputs > 126 MB L2", "parallelism": f"dp{world} (independent shards)",
+                   **({"exchange": w.exchange} if getattr(w, "exchange", None) else {})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic_from_profiles(args.config), "peak_source": peak_src,
                      "algorithmic_bytes_per_step": alg_bytes, "mean_kernel_ms": kernel_ms},

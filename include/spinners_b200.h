@@ -156,6 +156,16 @@ SPN_API uint64_t spn_mix_seed(uint64_t base, uint64_t stream);
 SPN_API spn_status spn_check_rows_f32(const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
                                       int32_t* flags, void* stream);
 
+/* Multi-GPU hashing with the all-gather fused into the kernel: each id of this rank's rows
+ * is stored at row row0 + v of EVERY rank's gathered [total][tables] int32 table, through
+ * the device pointers in `peers` (a device array of npeers pointers mapped with CUDA IPC
+ * over NVLink / NVSwitch; the local table is one of them).  After a barrier on all
+ * ranks, every table holds all codes — the NCCL all-gather of config 3 without a
+ * separate collective. */
+SPN_API spn_status spn_hash_f32_peers(const spn_plan* plan, const float* x, int64_t batch, int64_t ld_x,
+                                      int64_t n_in, int32_t* const* peers, int32_t npeers, int64_t row0,
+                                      void* stream);
+
 /* collision_curve / compare_families (lsh.cpp:38-96; lsh.hpp:38-75), the counting core.
  * plan: `trials` tables of make_hasher_factory(v, n, m) with table seeds mix_seed(seed, t)
  * (lsh.cpp:56).  xy: 2*pairs device rows, row 2p = x_p, row 2p+1 = y_p.  bucket_of: device

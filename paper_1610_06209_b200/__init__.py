@@ -72,6 +72,7 @@ _plan_query = _sig("spn_plan_query", C.c_int, [_vp] + [C.POINTER(_i64)] * 5 + [C
 _plan_diagonals = _sig("spn_plan_diagonals", C.c_int, [_vp, _vp, _vp, _vp])
 _apply = _sig("spn_apply_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i32, _vp])
 _hash = _sig("spn_hash_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp])
+_hash_peers = _sig("spn_hash_f32_peers", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _i64, _vp])
 _embed = _sig("spn_embed_f32", C.c_int, [_vp, _i32, _dbl, _vp, _i64, _i64, _i64, _vp, _i64, _vp])
 _sketch = _sig("spn_sketch_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _dbl, _vp, _i64, _vp])
 _apply_host = _sig("spn_apply_f32_host", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i32])
@@ -91,7 +92,7 @@ ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_c
                "spn_ar1_problem", "spn_newton_set_problem", "spn_logistic_eval_host", "spn_hessian_sqrt_host",
                "spn_sketched_step_host", "spn_logistic_line_host", "spn_collision_hits_f32", "spn_gram_exact_f32",
                "spn_gram_approx_f32", "spn_gram_error", "spn_gram_exact_host", "spn_gram_approx_host",
-               "spn_gram_error_host")
+               "spn_gram_error_host", "spn_hash_f32_peers")
 
 
 # ----------------------------------------------------------------------- errors

@@ -48,6 +48,11 @@ struct VecParams {
   int64_t ld_y;
   int relu;
   int x_vec_ok;        // x and ld_x 16-B aligned (cp.async staging allowed)
+  // fused all-gather (OP_HASH): every id is also stored, at row peer_row0 + v, into each
+  // rank's gathered [total][tables] table through peer (CUDA IPC / NVLink) pointers
+  int32_t* const* peers;
+  int npeers;
+  int64_t peer_row0;
 };
 
 #ifndef SPN_EMBED_WARPS
@@ -720,7 +725,12 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
       if (writer && active) {
         const float yb = best.val * p.c;
         const int id = best.gi + ((yb < 0.0f) ? (int)p.k : 0);  // sign(0) = +1 (lsh.cpp:20)
-        p.ids[v * p.tables + tab] = id;
+        if (p.npeers > 0) {
+          const int64_t off = (p.peer_row0 + v) * p.tables + tab;
+          for (int r = 0; r < p.npeers; ++r) p.peers[r][off] = id;
+        } else {
+          p.ids[v * p.tables + tab] = id;
+        }
       }
     }
   }

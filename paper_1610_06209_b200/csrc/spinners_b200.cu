@@ -506,6 +506,25 @@ spn_status spn_collision_hits_f32(const spn_plan* p, const float* xy, int64_t pa
   return SPN_OK;
 }
 
+spn_status spn_hash_f32_peers(const spn_plan* p, const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
+                              int32_t* const* peers, int32_t npeers, int64_t row0, void* stream) {
+  if (spn_status s = check_io(p, x, batch, ld_x, n_in)) return s;
+  if (npeers < 1 || !peers) return fail(SPN_EINVAL, "need >= 1 peer table");
+  if (row0 < 0) return fail(SPN_EINVAL, "row0 < 0");
+  if (p->fam) return fail(SPN_EUNSUPPORTED, "peer hash: Hadamard-only variants");
+  if (p->k >= (int64_t(1) << 30)) return fail(SPN_EDIM, "2k must fit int32 ids");
+  if (p->log_n > kMaxLogNVec) return fail(SPN_EUNSUPPORTED, "hash with n > 2^14 not implemented");
+  spn::VecParams v = base_params(p);
+  v.x = x;
+  v.ld_x = ld_x;
+  v.n_in = n_in;
+  v.batch = batch;
+  v.peers = peers;
+  v.npeers = npeers;
+  v.peer_row0 = row0;
+  return run_vec(p, spn::OP_HASH, v, static_cast<cudaStream_t>(stream));
+}
+
 spn_status spn_embed_f32(const spn_plan* p, int32_t kind, double sigma, const float* x,
                          int64_t batch, int64_t ld_x, int64_t n_in, float* out, int64_t ld_out,
                          void* stream) {

@@ -3,8 +3,11 @@
 The spinner hot path partitions trivially: every vector (row) is independent,
 so rank r of W owns a contiguous shard of rows and runs the same plan (same
 seeded diagonals) on it.  The only real exchange step is the all-gather of the
-int32 bucket codes of multi-table LSH (BASELINE config 3); it goes over
-torch.distributed (NCCL on GPUs, gloo in the CPU tests).
+int32 bucket codes of multi-table LSH (BASELINE config 3).  Two forms:
+  * gather_codes: torch.distributed all-gather (NCCL on GPUs, gloo in the CPU tests);
+  * PeerCodes: the all-gather fused into the hash kernel — every rank's epilogue stores
+    its codes straight into each rank's gathered table through CUDA IPC mappings of the
+    peers' buffers (NVLink / NVSwitch peer memory), then one barrier.
 """
 from __future__ import annotations
 
@@ -44,3 +47,42 @@ def gather_codes(local, world: int, total: int | None = None):
     if total is not None and full.shape[0] != total:
         raise RuntimeError("gathered row count mismatch")
     return full
+
+
+class PeerCodes:
+    """Gathered [total, tables] int32 code table on every rank, written by all ranks'
+    hash kernels directly (spn_hash_f32_peers).  Peer buffers are exchanged once as CUDA
+    IPC handles (torch's CUDA tensor sharing) over torch.distributed."""
+
+    def __init__(self, total: int, tables: int, world: int, rank: int, device: int = 0):
+        import torch
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.total, self.tables, self.world, self.rank = total, tables, world, rank
+        self.table = torch.full((total, tables), -1, dtype=torch.int32, device=f"cuda:{device}")
+        torch.cuda.synchronize(device)  # the fill must land before any peer can write into the table
+        handles = [None] * world
+        if world > 1:
+            dist.all_gather_object(handles, reduce_tensor(self.table))
+        peers = []
+        for r in range(world):
+            if r == rank:
+                peers.append(self.table)
+            else:
+                fn, args = handles[r]
+                peers.append(fn(*args))  # maps rank r's table into this process (cudaIpcOpenMemHandle)
+        self._peers = peers  # keep the mappings alive
+        self.ptrs = torch.tensor([t.data_ptr() for t in peers], dtype=torch.int64, device=f"cuda:{device}")
+
+    def hash(self, hasher, x_local, row0: int, stream=None):
+        """Hash this rank's rows (starting at global row row0) into every rank's table."""
+        import torch
+        import torch.distributed as dist
+        from . import _check, _hash_peers, _stream_ptr
+        x, _ = hasher.plan._device_in(x_local)
+        _check(_hash_peers(hasher.plan._h, x.data_ptr(), x.shape[0], x.stride(0), x.shape[1],
+                           self.ptrs.data_ptr(), self.world, row0, _stream_ptr(stream)))
+        torch.cuda.synchronize(x.device)
+        if self.world > 1:
+            dist.barrier()  # every rank's stores into this table are complete
+        return self.table

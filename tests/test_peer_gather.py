@@ -1,0 +1,58 @@
+"""The all-gather fused into the hash kernel (PeerCodes / spn_hash_f32_peers): two ranks
+each hash their shard of rows and store every code into BOTH ranks' gathered tables
+through CUDA IPC mappings; after one barrier each table must equal the single-process
+result.  On the GPU box the two processes share the one device (the IPC mapping path is
+the same one NVLink peers use; the kernels never wait on each other — the only
+synchronisation is the host barrier)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, total, out_dir):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+    import paper_1610_06209_b200 as spn
+    from paper_1610_06209_b200.shard import PeerCodes, shard_range
+    from oracle.oracle import Oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n, tables = 1024, 4
+    x = Oracle().gaussian_rows(91, total, n, unit=True)
+    h = spn.MultiTableHasher(spn.SpinnerVariant.hd3_hd2_hd1, n, n, tables, seed=17)
+    start, count = shard_range(total, rank, world)
+    pc = PeerCodes(total, tables, world, rank)
+    table = pc.hash(h, torch.from_numpy(x[start:start + count]).cuda(), start)
+    np.save(os.path.join(out_dir, f"table{rank}.npy"), table.cpu().numpy())
+    if rank == 0:
+        np.save(os.path.join(out_dir, "single.npy"), h.hash_ids(torch.from_numpy(x).cuda()).cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [1000, 4097])
+def test_fused_peer_gather_two_ranks(tmp_path, total):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), total, str(tmp_path)), nprocs=world, join=True)
+    single = np.load(tmp_path / "single.npy")
+    for r in range(world):
+        t = np.load(tmp_path / f"table{r}.npy")
+        assert np.array_equal(t, single), r
