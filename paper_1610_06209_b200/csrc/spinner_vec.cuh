@@ -103,7 +103,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // ---------------------------------------------------------------- primitives
 
-// (a0,a1),(b0,b1) <- (a+b, a-b) on packed f32x2 (sm_100a FADD2; one issue slot for two adds).
+// (a0,a1),(b0,b1) <- (a+b, a-b) on packed f32x2 (sm_100a FADD2: one instruction for two adds,
+// though it holds the issue port two cycles — the FP32 add rate equals two FADDs).
 __device__ __forceinline__ void bfly2(float& a0, float& a1, float& b0, float& b1) {
   asm("{\n\t.reg .b64 pa, pb, ps, pd;\n\t"
       "mov.b64 pa, {%0, %1};\n\t"
@@ -274,6 +275,12 @@ __device__ __forceinline__ void fwht_A_to_B(float (&r)[C::R], float* sm, int t) 
   }
 }
 
+// Sign bit jj of a mask word moved to bit 31 with a funnel shift (SHF, ALU pipe): the plain
+// `w << (31 - jj)` compiles to IMAD.SHL, which issues on the FMA pipe the butterflies saturate.
+__device__ __forceinline__ uint32_t sign_bit(uint32_t w, int jj) {
+  return __funnelshift_l(w, w, 31 - jj) & 0x80000000u;
+}
+
 // r <- D r, D given in the current layout (diag_matvec, transforms.cpp:228-235).
 template <class C>
 __device__ __forceinline__ void apply_diag(float (&r)[C::R], const DiagArrays& d, int is_sign,
@@ -286,7 +293,7 @@ __device__ __forceinline__ void apply_diag(float (&r)[C::R], const DiagArrays& d
 #pragma unroll
       for (int jj = 0; jj < C::BITS; ++jj) {
         const int j = q * 32 + jj;
-        r[j] = __uint_as_float(__float_as_uint(r[j]) ^ ((word << (31 - jj)) & 0x80000000u));
+        r[j] = __uint_as_float(__float_as_uint(r[j]) ^ sign_bit(word, jj));
       }
     }
   } else {
@@ -315,7 +322,7 @@ __device__ __forceinline__ void xor_signs(float (&r)[C::R], const uint32_t (&w)[
 #pragma unroll
     for (int jj = 0; jj < C::BITS; ++jj) {
       const int j = q * 32 + jj;
-      r[j] = __uint_as_float(__float_as_uint(r[j]) ^ ((w[q] << (31 - jj)) & 0x80000000u));
+      r[j] = __uint_as_float(__float_as_uint(r[j]) ^ sign_bit(w[q], jj));
     }
 }
 
@@ -351,7 +358,9 @@ __device__ __forceinline__ void spinner_chain(float (&r)[C::R], float* sm, const
       xor_signs<C>(r, w);
       if (h < 2) load_words<C>(w, h == 0 ? w1p : w2p, tb, t);  // in flight during the butterflies
       reg_fwht<C::R, 0, C::LOG_R>(r);
+#ifndef SPN_DBG_NOXPOSE  // (bound experiments only: wrong results)
       xpose_A_to_B<C>(r, sm, t);
+#endif
       reg_fwht<C::R, 0, C::LOG_R>(r);
     }
   } else if constexpr (SIGNS) {
@@ -541,6 +550,135 @@ __device__ __forceinline__ ArgBest group_argmax(ArgBest b, float* red) {
   return b;
 }
 
+// ---- signed argmax of a single-block table (lsh.cpp:9-21) without per-element index
+// tracking in every warp.  Element i of register j is first_i + j*stride_i (increasing in
+// j); elements with i >= rows are excluded.  Keys order candidates so that the reference
+// scan's winner (max |y|, strict '>' keeps the FIRST index on ties) wins.
+
+// max |y| over this thread's valid registers (-1 if none); 8 independent FMNMX chains
+template <class C>
+__device__ __forceinline__ float thread_absmax(const float (&r)[C::R], int first_i, int stride_i, int rows, bool full) {
+  constexpr int K = C::R >= 8 ? 8 : C::R;
+  float m[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) m[k] = -1.0f;
+  if (full) {
+#pragma unroll
+    for (int j = 0; j < C::R; ++j) m[j % K] = fmaxf(m[j % K], fabsf(r[j]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < C::R; ++j)
+      if (first_i + j * stride_i < rows) m[j % K] = fmaxf(m[j % K], fabsf(r[j]));
+  }
+#pragma unroll
+  for (int w = K / 2; w > 0; w >>= 1)
+#pragma unroll
+    for (int k = 0; k < w; ++k) m[k] = fmaxf(m[k], m[k + w]);
+  return m[0];
+}
+
+// smallest valid register j with |r[j]| == M and its value (4 independent select chains)
+template <class C>
+__device__ __forceinline__ void thread_first_hit(const float (&r)[C::R], float M, int first_i, int stride_i, int rows,
+                                                 bool full, int& jb, float& vb) {
+  constexpr int K = C::R >= 16 ? 4 : 1, S = C::R / K;
+  int jk[K];
+  float vk[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    jk[k] = -1;
+    vk[k] = 0.0f;
+#pragma unroll
+    for (int j = (k + 1) * S - 1; j >= k * S; --j) {
+      const bool hit = fabsf(r[j]) == M && (full || first_i + j * stride_i < rows);
+      jk[k] = hit ? j : jk[k];
+      vk[k] = hit ? r[j] : vk[k];
+    }
+  }
+  jb = jk[K - 1];
+  vb = vk[K - 1];
+#pragma unroll
+  for (int k = K - 2; k >= 0; --k) {
+    jb = jk[k] >= 0 ? jk[k] : jb;
+    vb = jk[k] >= 0 ? vk[k] : vb;
+  }
+}
+
+__device__ __forceinline__ int argmax_key(int i, float v, float c) {
+  return (i << 1) | ((v * c < 0.0f) ? 1 : 0);  // sign(0) = +1 (lsh.cpp:20)
+}
+__device__ __forceinline__ int key_to_id(int key, int64_t k) {
+  return key == 0x7fffffff ? key : (key >> 1) + ((key & 1) ? (int)k : 0);
+}
+// Single-warp groups (T <= 32): group max by shuffles, the lanes holding it search their
+// registers, then a shuffle min over keys.  Returns the key in every thread of the group.
+template <class C>
+__device__ __forceinline__ int group_signed_argmax(const float (&r)[C::R], int first_i, int stride_i, int rows,
+                                                   float c) {
+  const bool full = first_i + (C::R - 1) * stride_i < rows;
+  const float m = thread_absmax<C>(r, first_i, stride_i, rows, full);
+  constexpr int LIM = C::T < 32 ? C::T : 32;
+  float M = m;
+#pragma unroll
+  for (int off = LIM / 2; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  const bool cand = m == M && m >= 0.0f;
+  int key = 0x7fffffff;
+  if (__any_sync(0xffffffffu, cand)) {
+    int jb;
+    float vb;
+    thread_first_hit<C>(r, M, first_i, stride_i, rows, full, jb, vb);
+    if (cand) key = argmax_key(first_i + jb * stride_i, vb, c);
+  }
+#pragma unroll
+  for (int off = LIM / 2; off > 0; off >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, off));
+  return key;
+}
+
+// Multi-warp groups (T > 32, one group per CTA): CTA max of |y| (one barrier), then only
+// the warps holding it search, posting their key into smem slot `par` with a shared
+// atomicMin and NO trailing barrier — the kernel takes the slot after the next table's
+// transposes (their barriers order the atomics), so the argmax adds one barrier to the
+// per-table critical path (c3: 283.6 -> 276.2 ms).  Every warp searching against its own
+// warp max with a 64-bit atomicMax key (no barrier at all) measured slower (297 ms).
+template <class C>
+__device__ __forceinline__ void cta_signed_argmax_post(const float (&r)[C::R], int first_i, int stride_i, int rows,
+                                                       float c, float* red, int par) {
+  constexpr int W = C::T / 32;
+  const bool full = first_i + (C::R - 1) * stride_i < rows;
+  const float m = thread_absmax<C>(r, first_i, stride_i, rows, full);
+  float M = m;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = M;
+  __syncthreads();
+  M = red[0];
+#pragma unroll
+  for (int q = 1; q < W; ++q) M = fmaxf(M, red[q]);
+  const bool cand = m == M && m >= 0.0f;
+  if (__any_sync(0xffffffffu, cand)) {
+    int jb;
+    float vb;
+    thread_first_hit<C>(r, M, first_i, stride_i, rows, full, jb, vb);
+    if (cand) atomicMin(reinterpret_cast<int*>(red) + W + par, argmax_key(first_i + jb * stride_i, vb, c));
+  }
+}
+
+// Thread 0: take (and reset) the id posted into slot `par` (after a barrier).
+template <class C>
+__device__ __forceinline__ int cta_signed_argmax_take(float* red, int par, int64_t k) {
+  int* s = reinterpret_cast<int*>(red) + C::T / 32 + par;
+  const int key = *s;
+  *s = 0x7fffffff;
+  return key_to_id(key, k);
+}
+template <class C>
+__device__ __forceinline__ void cta_signed_argmax_init(float* red) {
+  if (threadIdx.x == 0) {
+    reinterpret_cast<int*>(red)[C::T / 32] = 0x7fffffff;
+    reinterpret_cast<int*>(red)[C::T / 32 + 1] = 0x7fffffff;
+  }
+}
+
 // Issue the cp.async copies of one row (n_in valid floats, zero fill to N) into the
 // swizzled staging buffer; 16-B chunk c = t + T*u, coalesced across the group.
 template <class C>
@@ -578,6 +716,30 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
   const int64_t stride = (int64_t)gridDim.x * C::GPC;
   const bool want_ids = (OP == OP_HASH) || (OP == OP_APPLY && p.ids != nullptr);
   const bool staged = STAGE_X && p.x_vec_ok;
+  // single-block tables take the two-phase argmax (group_signed_argmax / cta_signed_argmax_*);
+  // multi-warp groups post each table's winner into smem and write its id one table later
+  const bool fast_ids = want_ids && p.blocks == 1;
+  constexpr bool DEFER = C::MULTI_WARP;
+  int64_t pend_v = -1, pend_tab = 0;
+  bool pend_active = false;
+  int par = 0;
+  if constexpr (DEFER) cta_signed_argmax_init<C>(red);  // visible after the chain's barriers
+  auto emit_id = [&](int64_t vv, int64_t tt, int id) {
+    if (p.npeers > 0) {
+      const int64_t off = (p.peer_row0 + vv) * p.tables + tt;
+      for (int q = 0; q < p.npeers; ++q) p.peers[q][off] = id;
+    } else {
+      p.ids[vv * p.tables + tt] = id;
+    }
+  };
+  // (DEFER) write the previous table's id: its atomics are ordered by the barriers since
+  auto flush_pending = [&]() {
+    if (pend_v >= 0 && threadIdx.x == 0) {
+      const int id = cta_signed_argmax_take<C>(red, par ^ 1, p.k);
+      if (pend_active) emit_id(pend_v, pend_tab, id);
+    }
+    pend_v = -1;
+  };
 
   if constexpr (STAGE_X) {
     const int64_t item0 = (int64_t)blockIdx.x * C::GPC + g;
@@ -646,6 +808,7 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
     }
 
     ArgBest best{-1.0f, 0x7fffffff, 0.0f};
+    int fast_key = 0x7fffffff;
     for (int b = 0; b < p.blocks; ++b) {
       if (STAGE_X && staged) {
         if constexpr (STAGE_X) {
@@ -666,7 +829,15 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
           }
         }
       } else {
+#ifdef SPN_DBG_NOLOAD  // (bound experiments only: wrong results)
+        if (base == (int64_t)blockIdx.x * C::GPC) load_x_B<C>(r, xrow, p.n_in, t);
+        else {
+#pragma unroll
+          for (int j = 0; j < C::R; ++j) r[j] = __int_as_float(0x3f800000 + j * 977 + t * 131 + (int)base);
+        }
+#else
         load_x_B<C>(r, xrow, p.n_in, t);
+#endif
         if constexpr (END_B) {
           if constexpr (C::T > 1) xpose_B_to_A<C>(r, sm, t);
         }
@@ -681,15 +852,38 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
       spinner_chain<C, END_B, SIGNS>(r, sm, p, tb, t);
       if constexpr (!END_B) {
         // layout A: element i = t*R + j, increasing j
-        float am, vb;
-        int jb;
-        thread_argmax<C>(r, t * C::R, 1, (int)rows, am, jb, vb);
-        if (jb >= 0) argbest_merge(best, am, (int)row0 + t * C::R + jb, vb);
+        if (fast_ids) {
+#ifdef SPN_DBG_NOARGMAX  // (bound experiments only: wrong results)
+          float acc = 0.0f;
+#pragma unroll
+          for (int j = 0; j < C::R; ++j) acc += (j & 1) ? r[j] : 0.0f;
+          fast_key = __float_as_int(acc) & 0xffff;
+#else
+          if constexpr (DEFER) {
+            flush_pending();
+            cta_signed_argmax_post<C>(r, t * C::R, 1, (int)rows, p.c, red, par);
+          } else {
+            fast_key = group_signed_argmax<C>(r, t * C::R, 1, (int)rows, p.c);
+          }
+#endif
+        } else {
+          float am, vb;
+          int jb;
+          thread_argmax<C>(r, t * C::R, 1, (int)rows, am, jb, vb);
+          if (jb >= 0) argbest_merge(best, am, (int)row0 + t * C::R + jb, vb);
+        }
       } else {
         // layout B: element i = j*T + t -> coalesced stores
         float* yrow = p.y + v * p.ld_y + row0;
         if constexpr (OP == OP_APPLY) {
-          if (want_ids) {
+          if (fast_ids) {
+            if constexpr (DEFER) {
+              flush_pending();
+              cta_signed_argmax_post<C>(r, t, C::T, (int)rows, p.c, red, par);
+            } else {
+              fast_key = group_signed_argmax<C>(r, t, C::T, (int)rows, p.c);
+            }
+          } else if (want_ids) {
             float am, vb;
             int jb;
             thread_argmax<C>(r, t, C::T, (int)rows, am, jb, vb);
@@ -720,18 +914,31 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
     }
 
     if (want_ids) {
-      best = group_argmax<C>(best, red);
-      const bool writer = C::MULTI_WARP ? (threadIdx.x == 0) : (t == 0);
-      if (writer && active) {
-        const float yb = best.val * p.c;
-        const int id = best.gi + ((yb < 0.0f) ? (int)p.k : 0);  // sign(0) = +1 (lsh.cpp:20)
-        if (p.npeers > 0) {
-          const int64_t off = (p.peer_row0 + v) * p.tables + tab;
-          for (int r = 0; r < p.npeers; ++r) p.peers[r][off] = id;
-        } else {
-          p.ids[v * p.tables + tab] = id;
-        }
+      if (fast_ids && DEFER) {
+#ifndef SPN_DBG_NOARGMAX
+        pend_v = v;
+        pend_tab = tab;
+        pend_active = active;
+        par ^= 1;
+        continue;
+#endif
       }
+      int id;
+      if (fast_ids) {
+        id = key_to_id(fast_key, p.k);
+      } else {
+        best = group_argmax<C>(best, red);
+        const float yb = best.val * p.c;
+        id = best.gi + ((yb < 0.0f) ? (int)p.k : 0);  // sign(0) = +1 (lsh.cpp:20)
+      }
+      const bool writer = C::MULTI_WARP ? (threadIdx.x == 0) : (t == 0);
+      if (writer && active) emit_id(v, tab, id);
+    }
+  }
+  if constexpr (DEFER) {
+    if (fast_ids) {
+      __syncthreads();
+      flush_pending();
     }
   }
 }
