@@ -275,10 +275,18 @@ __device__ __forceinline__ void fwht_A_to_B(float (&r)[C::R], float* sm, int t) 
   }
 }
 
-// Sign bit jj of a mask word moved to bit 31 with a funnel shift (SHF, ALU pipe): the plain
-// `w << (31 - jj)` compiles to IMAD.SHL, which issues on the FMA pipe the butterflies saturate.
-__device__ __forceinline__ uint32_t sign_bit(uint32_t w, int jj) {
-  return __funnelshift_l(w, w, 31 - jj) & 0x80000000u;
+// r <- -r when bit jj of the mask word w is set.  Written as a predicated XOR so ptxas
+// turns each 7 bits of w into predicates with one R2P and flips with @P LOP3: ~1.25 ALU
+// instructions per element instead of a shift + LOP3 (tools/microbench/fwht_regs.cu,
+// R = 128: 82.5 -> 93.4 adds/clk/SM; the plain `(w << (31 - jj)) & 0x80000000` shift even
+// compiles to IMAD.SHL on the FMA pipe the butterflies saturate).
+__device__ __forceinline__ void flip_if(float& r, uint32_t w, int jj) {
+  uint32_t x = __float_as_uint(r);
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+      "and.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t@p xor.b32 %0, %0, 0x80000000;\n\t}"
+      : "+r"(x)
+      : "r"(w), "r"(1u << jj));
+  r = __uint_as_float(x);
 }
 
 // r <- D r, D given in the current layout (diag_matvec, transforms.cpp:228-235).
@@ -293,7 +301,7 @@ __device__ __forceinline__ void apply_diag(float (&r)[C::R], const DiagArrays& d
 #pragma unroll
       for (int jj = 0; jj < C::BITS; ++jj) {
         const int j = q * 32 + jj;
-        r[j] = __uint_as_float(__float_as_uint(r[j]) ^ sign_bit(word, jj));
+        flip_if(r[j], word, jj);
       }
     }
   } else {
@@ -322,7 +330,7 @@ __device__ __forceinline__ void xor_signs(float (&r)[C::R], const uint32_t (&w)[
 #pragma unroll
     for (int jj = 0; jj < C::BITS; ++jj) {
       const int j = q * 32 + jj;
-      r[j] = __uint_as_float(__float_as_uint(r[j]) ^ sign_bit(w[q], jj));
+      flip_if(r[j], w[q], jj);
     }
 }
 

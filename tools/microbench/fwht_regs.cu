@@ -17,13 +17,21 @@ __global__ void __launch_bounds__(128, MINB) k_fwht(float* out, const unsigned* 
   for (int q = 0; q < (R / 32 > 0 ? R / 32 : 1); ++q) w[q] = masks[q * 128 + threadIdx.x];
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
-    if constexpr (SIGNS == 1) {  // SHF + LOP3 per element (the kernel's form)
+    if constexpr (SIGNS == 1) {  // SHF + LOP3 per element
 #pragma unroll
-      for (int j = 0; j < R; ++j) r[j] = __uint_as_float(__float_as_uint(r[j]) ^ spn::sign_bit(w[j / 32], j % 32));
+      for (int j = 0; j < R; ++j)
+        r[j] = __uint_as_float(__float_as_uint(r[j]) ^ (__funnelshift_l(w[j / 32], w[j / 32], 31 - j % 32) & 0x80000000u));
     } else if constexpr (SIGNS == 2) {  // LOP3 only (timing probe, not a sign diagonal)
 #pragma unroll
       for (int j = 0; j < R; ++j) r[j] = __uint_as_float(__float_as_uint(r[j]) ^ (w[j / 32] & 0x80000000u));
       w[0] = (w[0] << 1) | (w[0] >> 31);
+    } else if constexpr (SIGNS == 4) {  // predicated negation (ptxas: R2P + FSEL per element)
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (w[j / 32] & (1u << (j % 32))) r[j] = -r[j];
+    } else if constexpr (SIGNS == 5) {  // predicated XOR (ptxas: R2P + @P LOP3 per element; the kernel's form)
+#pragma unroll
+      for (int j = 0; j < R; ++j) spn::flip_if(r[j], w[j / 32], j % 32);
     } else if constexpr (SIGNS == 3) {  // SHF only into a sink (timing probe)
 #pragma unroll
       for (int j = 0; j < R; ++j) w[0] ^= __funnelshift_l(w[j / 32 ^ 1 & (R / 32 - 1)], w[j / 32], j % 32);
@@ -75,7 +83,14 @@ int main() {
   run<7, 3, 1>(out, m, sms);
   run<7, 3, 2>(out, m, sms);
   run<7, 3, 3>(out, m, sms);
+  run<7, 3, 4>(out, m, sms);
+  run<7, 3, 5>(out, m, sms);
   run<6, 4, 0>(out, m, sms);
   run<6, 4, 1>(out, m, sms);
+  run<6, 4, 4>(out, m, sms);
+  run<6, 4, 5>(out, m, sms);
+  run<5, 8, 1>(out, m, sms);
+  run<5, 8, 4>(out, m, sms);
+  run<5, 8, 5>(out, m, sms);
   return 0;
 }
