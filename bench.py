@@ -279,6 +279,7 @@ def run_ours(args, rank, world, local):
     w = Workload(args.config, cfg, rank, local, world)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if cfg["flush"] else None
+    flush_sink = torch.zeros((), dtype=torch.int64, device="cuda")
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         # warm-up, continued (untimed) until nvidia-smi has seen the GPU under this load
@@ -295,7 +296,13 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         for i in range(args.steps):
             if flush is not None:
-                flush.fill_(i & 0xFF)  # evict L2 (256 MB > 126 MB) outside the timed region
+                # evict L2 outside the timed region: write 256 MB (> 126 MB L2), then read it back so
+                # the lines left in L2 are clean (otherwise the timed kernel pays for write-backs of
+                # the flush's own dirty lines)
+                flush.fill_(i & 0xFF)
+                flush_sink += flush.view(torch.int64).sum()
+            # keep the device busy past the start event so it never times the host's launch latency
+            torch.cuda._sleep(200_000)
             evs[i][0].record(stream)
             w.step(stream)
             evs[i][1].record(stream)
@@ -327,7 +334,7 @@ def run_ours(args, rank, world, local):
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE config shapes)",
         "config": {"workload": cfg["workload"], "name": args.config, "vectors_per_gpu_step": w.vectors,
-                   "l2": "L2 flushed (256 MB write) between timed steps" if cfg["flush"]
+                   "l2": "L2 flushed (256 MB write + read-back) between timed steps" if cfg["flush"]
                    else "inputs+outputs > 126 MB L2", "parallelism": f"dp{world} (independent shards)",
                    **({"exchange": w.exchange} if getattr(w, "exchange", None) else {})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
