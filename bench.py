@@ -500,6 +500,10 @@ def main():
         if world == 1 and not args.no_cpu:
             v, info = cpu_reference(args.config)
             res["cpu_baseline"] = dict(info, value=v, unit=UNIT)
+            if args.config in ("c1", "c2", "c3", "c4", "c5"):  # the reference's own contract: one thread
+                v1, info1 = cpu_reference(args.config, budget_s=4.0, threads=1)
+                res["cpu_baseline"]["value_1thread"] = v1
+                res["cpu_baseline"]["sample_1thread"] = info1["sample"]
         print(json.dumps(res), flush=True)
     if world > 1:
         import torch.distributed as dist

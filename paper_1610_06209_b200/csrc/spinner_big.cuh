@@ -24,10 +24,12 @@
 #include <cstdlib>
 #include <cmath>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "../../include/spinners_b200.h"
 #include "errors.hpp"
+#include "host_params.hpp"
 #include "spinner_vec.cuh"
 
 namespace spn {
@@ -384,6 +386,108 @@ inline cudaMemPool_t scratch_pool() {
   return pools[dev];
 }
 
+// Per-device library streams: the multi-pass drivers' group streams (shared by every plan on
+// the device — plans are short-lived, e.g. a fresh sketch per Newton iteration, and stream
+// creation / destruction would cost more than the sketch) and the stream that returns plan
+// memory to the pool.
+inline cudaStream_t device_stream(int slot) {
+  static std::mutex mu;
+  static cudaStream_t ss[64][8] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || slot < 0 || slot >= 8) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ss[dev][slot]) {
+    // slot 6 (plan-time realisation) runs at the highest priority: its two CTAs take the
+    // first SM slots that free up between the running passes' CTAs
+    int lo = 0, hi = 0;
+    if (slot != 6 || cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) hi = 0;
+    if (cudaStreamCreateWithPriority(&ss[dev][slot], cudaStreamNonBlocking, hi) != cudaSuccess) {
+      cudaGetLastError();
+      ss[dev][slot] = nullptr;
+    }
+  }
+  return ss[dev][slot];
+}
+constexpr int kFreeStreamSlot = 7;
+constexpr int kRealiseStreamSlot = 6;
+
+inline cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
+  cudaMemPool_t pool = scratch_pool();
+  if (!pool) return cudaErrorMemoryAllocation;
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+// Device realisation of a Rademacher (HD3) block's diagonals with the reference's own
+// generator (proj/src/spinner.cpp:137-151; common.hpp:61-92): std::mt19937_64 seeded with
+// mix_seed(spec_seed, 1) gives D1 then D2 (n draws each), mix_seed(spec_seed, 2) gives D3,
+// and rademacher(u) = (u & 1) ? +1 : -1 (common.hpp:86).  One CTA per stream; each 312-word
+// twist runs as its two data-parallel halves (i < 156 reads only old words, i >= 156 reads
+// the new words i - 156, and i = 311 the new word 0 — the sequential order of the library
+// engine), then the block is tempered and emitted in parallel.  Bit-exact with the host
+// realisation (tests/test_newton.py), ~20x faster than drawing 3n values on the host, and
+// stream-ordered, so creating a fresh sketch per Newton iteration costs no host time.
+// Outputs are the sketch layouts: D1, D3 natural, D2 transposed for the high-bit pass
+// (f[lo * 2^lsb + s] = D2[(s << lsa) + lo], see build_sketch).
+__global__ void __launch_bounds__(160) mt_rademacher_sketch_kernel(uint64_t seed_front, uint64_t seed_tail,
+                                                                   int64_t n, int lsa, int lsb, float* d1,
+                                                                   float* d2t, float* d3) {
+  constexpr int N = 312, M = 156;
+  constexpr uint64_t A = 0xB5026F5AA96619E9ULL, UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL;
+  __shared__ uint64_t mt[N];
+  const bool front = blockIdx.x == 0;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    mt[0] = front ? seed_front : seed_tail;
+    for (int i = 1; i < N; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + uint64_t(i);
+  }
+  __syncthreads();
+  const int64_t draws = front ? 2 * n : n;
+  const int64_t lo_mask = (int64_t(1) << lsa) - 1;
+  for (int64_t base = 0; base < draws; base += N) {
+    uint64_t v = 0;
+    if (t < M) {
+      const uint64_t y = (mt[t] & UM) | (mt[t + 1] & LM);
+      v = mt[t + M] ^ (y >> 1) ^ ((0 - (y & 1)) & A);
+    }
+    __syncthreads();
+    if (t < M) mt[t] = v;
+    __syncthreads();
+    if (t < N - M) {
+      const int i = M + t;
+      const uint64_t y = (mt[i] & UM) | (mt[i + 1 < N ? i + 1 : 0] & LM);
+      v = mt[i - M] ^ (y >> 1) ^ ((0 - (y & 1)) & A);
+    }
+    __syncthreads();
+    if (t < N - M) mt[M + t] = v;
+    __syncthreads();
+    for (int j = t; j < N; j += blockDim.x) {
+      const int64_t k = base + j;
+      if (k >= draws) break;
+      uint64_t y = mt[j];
+      y ^= (y >> 29) & 0x5555555555555555ULL;
+      y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+      y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+      y ^= y >> 43;
+      const float r = (y & 1) ? 1.0f : -1.0f;
+      if (!front) {
+        d3[k] = r;
+      } else if (k < n) {
+        d1[k] = r;
+      } else {
+        const int64_t e = k - n;
+        d2t[lsb > 0 ? (e & lo_mask) * (int64_t(1) << lsb) + (e >> lsa) : e] = r;
+      }
+    }
+    // (the next twist's first barrier orders these reads before its writes)
+  }
+}
+
+// rowmap[i] = i for i < m (the reference's P = first m rows), -1 beyond
+__global__ void rowmap_first_kernel(int32_t* map, int64_t nn, int64_t m) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x)
+    map[i] = i < m ? static_cast<int32_t>(i) : -1;
+}
+
 struct Scratch {  // freed (stream-ordered) on `s` when the scope ends
   void* p = nullptr;
   cudaStream_t s = nullptr;
@@ -419,6 +523,34 @@ struct BigPlan {
   int sk_lsa = 0, sk_lsb = 0;
   float* sk_d[3] = {nullptr, nullptr, nullptr};
   float* sk_d1s = nullptr;  // D1 * row scale (Newton step), lazily allocated
+  // Rademacher (HD3) single-block plans realise their sketch diagonals on the device
+  // (mt_rademacher_sketch_kernel) instead of uploading host draws
+  bool dev_rad = false;
+  uint64_t dev_seed = 0;  // spec seed of the block
+  // sk_d, sk_d1s and rowmap come from the stream-ordered pool; they go back to it after the
+  // last call on every stream that used them (uses), without a device-wide cudaFree
+  // synchronisation.  ev_ready marks the realisation / row map on the stream that made them;
+  // calls on other streams wait for it.
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
+  cudaEvent_t ev_ready = nullptr;
+  cudaError_t note_use(cudaStream_t s) {
+    for (auto& u : uses)
+      if (u.first == s) return cudaEventRecord(u.second, s);
+    cudaEvent_t e = nullptr;
+    cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (r != cudaSuccess) return r;
+    uses.emplace_back(s, e);
+    return cudaEventRecord(e, s);
+  }
+  cudaError_t wait_uses(cudaStream_t s) {
+    for (auto& u : uses)
+      if (cudaError_t r = cudaStreamWaitEvent(s, u.second, 0)) return r;
+    return cudaSuccess;
+  }
+  cudaError_t mark_ready(cudaStream_t s) {
+    cudaError_t r = ev_ready ? cudaSuccess : cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming);
+    return r == cudaSuccess ? cudaEventRecord(ev_ready, s) : r;
+  }
   // scratch
   float* work = nullptr;
   size_t work_bytes = 0;
@@ -426,7 +558,8 @@ struct BigPlan {
   std::vector<int64_t> rowmap_key;
   // groups alternate between two internal streams so one group's pass tail overlaps the
   // next group's work (each pass is a full-GPU persistent kernel; fill/drain dominate
-  // otherwise).  Forked from / joined back into the caller's stream with events.
+  // otherwise).  Forked from / joined back into the caller's stream with events.  The
+  // streams are the device's library streams (device_stream), shared by all plans.
   static constexpr int kMaxStreams = 4;
   cudaStream_t ss[kMaxStreams] = {};
   cudaEvent_t evf = nullptr, evj[kMaxStreams] = {};
@@ -437,21 +570,35 @@ struct BigPlan {
       if (q) cudaFree(q);
       q = nullptr;
     }
-    for (auto*& q : sk_d) {
-      if (q) cudaFree(q);
-      q = nullptr;
+    {
+      cudaStream_t fs = device_stream(kFreeStreamSlot);
+      if (fs) {
+        wait_uses(fs);
+        if (ev_ready) cudaStreamWaitEvent(fs, ev_ready, 0);
+      }
+      auto pfree = [&](void* q) {
+        if (!q) return;
+        if (!fs || cudaFreeAsync(q, fs) != cudaSuccess) cudaFree(q);
+      };
+      for (auto*& q : sk_d) {
+        pfree(q);
+        q = nullptr;
+      }
+      pfree(sk_d1s);
+      sk_d1s = nullptr;
+      pfree(rowmap);
+      rowmap = nullptr;
+      for (auto& u : uses) cudaEventDestroy(u.second);
+      uses.clear();
+      if (ev_ready) cudaEventDestroy(ev_ready);
+      ev_ready = nullptr;
     }
-    if (sk_d1s) cudaFree(sk_d1s);
-    sk_d1s = nullptr;
     if (drow2) cudaFree(drow2);
     for (float** q : {&srow1, &srow3, &stile2}) {
       if (*q) cudaFree(*q);
       *q = nullptr;
     }
     if (work) cudaFree(work);
-    if (rowmap) cudaFree(rowmap);
-    for (auto& q : ss)
-      if (q) cudaStreamDestroy(q);
     if (evf) cudaEventDestroy(evf);
     for (auto& q : evj)
       if (q) cudaEventDestroy(q);
@@ -475,7 +622,8 @@ struct BigPlan {
   spn_status fork(cudaStream_t s) {
     cudaError_t e = cudaSuccess;
     for (int i = 0; i < nstreams() && e == cudaSuccess; ++i) {
-      if (!ss[i]) e = cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking);
+      if (!ss[i]) ss[i] = device_stream(i);
+      if (!ss[i]) e = cudaErrorInvalidResourceHandle;
       if (e == cudaSuccess && !evj[i]) e = cudaEventCreateWithFlags(&evj[i], cudaEventDisableTiming);
     }
     if (e == cudaSuccess && !evf) e = cudaEventCreateWithFlags(&evf, cudaEventDisableTiming);
@@ -708,7 +856,18 @@ struct BigPlan {
     return join(s0);
   }
 
-  spn_status build_sketch(int64_t nn, const std::vector<double>* d) {
+  // Rademacher plans: realise the sketch diagonals at plan creation on the library's
+  // realisation stream, so the draws overlap whatever the device is running (a Newton
+  // solve creates the next iteration's sketch while the current step runs).
+  spn_status prefetch_sketch(int64_t nn) {
+    if (!dev_rad) return SPN_OK;
+    std::lock_guard<std::mutex> lock(mu);
+    cudaStream_t rs = device_stream(kRealiseStreamSlot);
+    if (!rs) return err(cudaErrorInvalidResourceHandle, "realisation stream");
+    return build_sketch(nn, nullptr, rs);
+  }
+
+  spn_status build_sketch(int64_t nn, const std::vector<double>* d, cudaStream_t s) {
     if (sk_ready) return SPN_OK;
     const int LL = ilog2_i(nn);
     if (LL <= 10) {
@@ -717,6 +876,20 @@ struct BigPlan {
     } else {
       sk_lsa = (LL + 1) / 2;
       sk_lsb = LL / 2;
+    }
+    if (dev_rad) {
+      cudaError_t e = cudaSuccess;
+      for (int di = 0; di < 3 && e == cudaSuccess; ++di)
+        e = pool_alloc(reinterpret_cast<void**>(&sk_d[di]), static_cast<size_t>(nn) * 4, s);
+      if (e == cudaSuccess) {
+        mt_rademacher_sketch_kernel<<<2, 160, 0, s>>>(mix_seed(dev_seed, 1), mix_seed(dev_seed, 2), nn, sk_lsa,
+                                                      sk_lsb, sk_d[0], sk_d[1], sk_d[2]);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = mark_ready(s);
+      if (e != cudaSuccess) return err(e, "device realisation of the sketch diagonals");
+      sk_ready = true;
+      return SPN_OK;
     }
     std::vector<float> f(static_cast<size_t>(nn));
     for (int di = 0; di < 3; ++di) {
@@ -728,8 +901,9 @@ struct BigPlan {
       } else {
         for (int64_t i = 0; i < nn; ++i) f[static_cast<size_t>(i)] = static_cast<float>(d[di][static_cast<size_t>(i)]);
       }
-      cudaError_t e = cudaMalloc(&sk_d[di], f.size() * 4);
-      if (e == cudaSuccess) e = cudaMemcpy(sk_d[di], f.data(), f.size() * 4, cudaMemcpyHostToDevice);
+      cudaError_t e = pool_alloc(reinterpret_cast<void**>(&sk_d[di]), f.size() * 4, s);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(sk_d[di], f.data(), f.size() * 4, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // f is pageable and goes out of scope
       if (e != cudaSuccess) return err(e, "upload sketch diagonals");
     }
     sk_ready = true;
@@ -740,6 +914,21 @@ struct BigPlan {
     std::vector<int64_t> key;
     if (rows) key.assign(rows, rows + m_out);
     if (rowmap && rowmap_m == m_out && key == rowmap_key) return SPN_OK;
+    if (!rows) {  // P = first m_out rows: filled on the device, stream-ordered
+      cudaError_t e = cudaSuccess;
+      if (!rowmap) e = pool_alloc(reinterpret_cast<void**>(&rowmap), static_cast<size_t>(nn) * 4, s);
+      else e = wait_uses(s);  // earlier calls (any stream) are done with the old map
+      if (e == cudaSuccess) {
+        rowmap_first_kernel<<<static_cast<unsigned>(std::min<int64_t>((nn + 255) / 256, 1024)), 256, 0, s>>>(
+            rowmap, nn, m_out);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = mark_ready(s);
+      if (e != cudaSuccess) return err(e, "row map");
+      rowmap_key.clear();
+      rowmap_m = m_out;
+      return SPN_OK;
+    }
     std::vector<int32_t> map(static_cast<size_t>(nn), -1);
     for (int64_t r = 0; r < m_out; ++r) {
       const int64_t i = rows ? rows[r] : r;
@@ -747,7 +936,7 @@ struct BigPlan {
       map[static_cast<size_t>(i)] = static_cast<int32_t>(r);
     }
     cudaError_t e = cudaSuccess;
-    if (!rowmap) e = cudaMalloc(&rowmap, static_cast<size_t>(nn) * 4);
+    if (!rowmap) e = pool_alloc(reinterpret_cast<void**>(&rowmap), static_cast<size_t>(nn) * 4, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // previous users of the map are done
     if (e == cudaSuccess) e = cudaMemcpy(rowmap, map.data(), map.size() * 4, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return err(e, "row map");
@@ -771,12 +960,15 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
                              int64_t ld_out, int sms, cudaStream_t s0, BigPlan* bp,
                              const float* row_scale = nullptr) {
   std::lock_guard<std::mutex> lock(bp->mu);
-  if (spn_status st = bp->build_sketch(nn, d)) return st;
+  if (spn_status st = bp->build_sketch(nn, d, s0)) return st;
   if (spn_status st = bp->set_rowmap(nn, rows, m_out, s0)) return st;
+  if (bp->ev_ready) {  // realisation / row map made on another stream
+    if (cudaError_t e = cudaStreamWaitEvent(s0, bp->ev_ready, 0)) return BigPlan::err(e, "sketch ready");
+  }
   const float* d1 = bp->sk_d[0];
   if (row_scale) {
     cudaError_t e = cudaSuccess;
-    if (!bp->sk_d1s) e = cudaMalloc(&bp->sk_d1s, static_cast<size_t>(nn) * 4);
+    if (!bp->sk_d1s) e = pool_alloc(reinterpret_cast<void**>(&bp->sk_d1s), static_cast<size_t>(nn) * 4, s0);
     if (e != cudaSuccess) return BigPlan::err(e, "scaled D1");
     const int64_t blocks = std::min<int64_t>((nn + 255) / 256, int64_t(sms) * 8);
     scale_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, s0>>>(bp->sk_d[0], row_scale, n_in, nn, bp->sk_d1s);
@@ -816,6 +1008,7 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     cp.rowmap = bp->rowmap;
     cp.dst = out;
     cudaError_t e = lcol(lsa, CP_SINGLE, cp);
+    if (e == cudaSuccess) e = bp->note_use(s0);
     return e == cudaSuccess ? SPN_OK : BigPlan::err(e, "sketch single pass");
   }
   // column groups of ~32 MB of workspace
@@ -878,7 +1071,9 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     e = lcol(lsb, CP_LAST, pb);
     if (e != cudaSuccess) return BigPlan::err(e, "sketch P4");
   }
-  return bp->join(s0);
+  if (spn_status st = bp->join(s0)) return st;
+  if (cudaError_t e = bp->note_use(s0)) return BigPlan::err(e, "sketch use event");
+  return SPN_OK;
 }
 
 }  // namespace spn

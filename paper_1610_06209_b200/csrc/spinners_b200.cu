@@ -70,6 +70,19 @@ struct spn_plan {
   int sms = 0;
   std::vector<double> d[3];  // realised fp64 diagonals [tables][blocks][n]
   int dsign[3] = {0, 0, 0};
+  // Single-block Rademacher plans with n > 2^14 (a sketch: SketchOperator, one per Newton
+  // iteration) defer the host draws: the sketch realises its diagonals on the device from
+  // the same generator; d is drawn on the host only if something asks for it.
+  bool lazy_d = false;
+  uint64_t spec_seed = 0;
+  std::once_flag d_once;
+  void ensure_host_d() {
+    if (!lazy_d) return;
+    std::call_once(d_once, [this] {
+      for (auto& v : d) v.resize(static_cast<size_t>(n));
+      spn::realize_block(spn::V_HD3, n, spec_seed, d[0].data(), d[1].data(), d[2].data());
+    });
+  }
   // circulant family / dense baseline (family.cu): Toeplitz first rows, dense matrices
   std::vector<double> trow, dense;
   spn::FamilyPlan* fam = nullptr;
@@ -182,7 +195,7 @@ spn_status build_vec_layouts(spn_plan* p) {
 
 spn_status finish_plan(spn_plan* p) {
   p->log_n = ilog2(p->n);
-  for (int di = 0; di < 3; ++di) {
+  for (int di = 0; di < 3 && !p->lazy_d; ++di) {
     bool all = true;
     for (double v : p->d[di])
       if (v != 1.0 && v != -1.0) {
@@ -327,6 +340,26 @@ spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) {
   // the dense baseline (spinner.cpp:41-45,69-71)
   p->scale = d->scale != 0.0 ? d->scale : (fam ? 1.0 : std::sqrt(static_cast<double>(d->n)));
   const int64_t per = p->blocks * p->n;
+  if (d->variant == SPN_HD3_HD2_HD1 && p->tables == 1 && p->blocks == 1 && ilog2(p->n) > kMaxLogNVec) {
+    p->lazy_d = true;
+    p->spec_seed = spn::mix_seed(d->table_seeds ? d->table_seeds[0] : d->seed, 0);
+    for (int di = 0; di < 3; ++di) p->dsign[di] = 1;
+    if (spn_status s = finish_plan(p)) {
+      delete p;
+      return s;
+    }
+    p->big.dev_rad = true;
+    p->big.dev_seed = p->spec_seed;
+    {
+      DeviceGuard g(p->device);
+      if (spn_status s = p->big.prefetch_sketch(p->n)) {
+        delete p;
+        return s;
+      }
+    }
+    *out = p;
+    return SPN_OK;
+  }
   for (auto& v : p->d) v.resize(static_cast<size_t>(p->tables * per));
   if (d->variant == SPN_GTOEPLITZ_D2_HD1) p->trow.resize(static_cast<size_t>(p->tables * per));
   if (d->variant == SPN_GAUSSIAN_DENSE) p->dense.resize(static_cast<size_t>(p->tables * p->blocks * p->m * p->n));
@@ -411,6 +444,7 @@ spn_status spn_plan_query(const spn_plan* p, int64_t* n, int64_t* m, int64_t* k,
 spn_status spn_plan_diagonals(const spn_plan* p, double* d1, double* d2, double* d3) {
   if (!p) return fail(SPN_EINVAL, "null plan");
   double* dst[3] = {d1, d2, d3};
+  const_cast<spn_plan*>(p)->ensure_host_d();
   for (int di = 0; di < 3; ++di)
     if (dst[di]) std::copy(p->d[di].begin(), p->d[di].end(), dst[di]);
   return SPN_OK;
@@ -428,6 +462,7 @@ spn_status spn_apply_f32(const spn_plan* p, const float* x, int64_t batch, int64
   }
   if (p->log_n > kMaxLogNVec) {
     DeviceGuard g(p->device);
+    const_cast<spn_plan*>(p)->ensure_host_d();
     return const_cast<spn_plan*>(p)->big.apply(x, batch, ld_x, n_in, y, ld_y, relu, p->k, p->m, p->blocks,
                         p->scale * std::pow(static_cast<double>(p->n), -1.5), p->sms,
                         static_cast<cudaStream_t>(stream));

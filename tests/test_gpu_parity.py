@@ -298,3 +298,46 @@ def test_big_inplace_groups(spn, oracle, torch, logn):
     y = sp.apply(dev(torch, x), relu=True).cpu().numpy()
     want = oracle.apply(*d, n, n, n, 1.0, x, relu=True)
     assert row_rel(y, want).max() <= RTOL
+
+
+# ------------------------------------------- device realisation of Rademacher sketch plans
+@pytest.mark.parametrize("N", [1 << 15, 1 << 17, 1 << 20])
+def test_sketch_device_realisation_bit_exact(spn, oracle, torch, N):
+    """Single-block HD3 plans with N > 2^14 (SketchOperator) draw D1..D3 on the device with the
+    reference's mt19937_64 (mt_rademacher_sketch_kernel).  The sketch must equal, bit for bit,
+    the same sketch through an explicit plan carrying the C oracle's host realisation, and the
+    lazily host-drawn diagonals of the plan must equal the oracle's."""
+    m, d, seed = 256, 32, 23
+    sk = spn.SketchOperator(spn.SpinnerVariant.hd3_hd2_hd1, N, m, seed)
+    a = dev(torch, oracle.gaussian_rows(77, N, d))
+    out = sk.apply(a).cpu().numpy()
+    D = oracle.realize(HD3, N, m, m, seed)
+    ex = spn.StackedSpinner.from_diagonals(D[0][0], D[1][0], D[2][0], N, m, m)
+    want = ex.plan.sketch(a, m, sk.norm).cpu().numpy()
+    assert np.array_equal(out, want)
+    got_d = sk.plan.diagonals()
+    for g, w in zip(got_d, D):
+        assert np.array_equal(g.reshape(-1), w.reshape(-1))
+
+
+def test_lazy_plan_apply_and_side_stream(spn, oracle, torch):
+    """A lazily realised plan used through apply (host draws on demand) and a device-realised
+    sketch made on a side stream then reused on the default stream."""
+    N, seed = 1 << 16, 31
+    sp = spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, N, N, N, seed)
+    x = dev(torch, oracle.gaussian_rows(5, 3, N))
+    D = oracle.realize(HD3, N, N, N, seed)
+    ex = spn.StackedSpinner.from_diagonals(D[0][0], D[1][0], D[2][0], N, N, N)
+    assert np.array_equal(sp.apply(x).cpu().numpy(), ex.apply(x).cpu().numpy())
+    sk = spn.SketchOperator(spn.SpinnerVariant.hd3_hd2_hd1, N, 512, seed)
+    a = dev(torch, oracle.gaussian_rows(6, N, 64))
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        o1 = sk.apply(a, stream=side)
+    o2 = sk.apply(a)
+    torch.cuda.synchronize()
+    want = ex.plan.sketch(a, 512, sk.norm)
+    assert torch.equal(o1, want) and torch.equal(o2, want)
+    del sk  # pool memory goes back after the uses recorded on both streams
+    torch.cuda.synchronize()
