@@ -19,6 +19,12 @@ elif cfg == "c5":
     x = torch.randn(batch, 1 << 20, device="cuda")
     y = torch.empty_like(x)
     run = lambda: sp.apply(x, relu=True, out=y)
+elif cfg == "c2":
+    sp = spn.StackedSpinner(V.hd3_hd2_hd1, 1024, 1024, 4096, 5)
+    fm = spn.FeatureMap(sp, spn.KernelKind.gaussian(5.0))
+    x = torch.rand(batch, 784, device="cuda")
+    out = torch.empty(batch, 8192, device="cuda")
+    run = lambda: spn.embed(fm, x, out=out)
 elif cfg == "c1":
     sp = spn.StackedSpinner(V.hd3_hd2_hd1, 1024, 1024, 1024, 42, scale=1.0)
     x = torch.randn(batch, 1024, device="cuda")
