@@ -420,50 +420,50 @@ inline cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
 // Device realisation of a Rademacher (HD3) block's diagonals with the reference's own
 // generator (proj/src/spinner.cpp:137-151; common.hpp:61-92): std::mt19937_64 seeded with
 // mix_seed(spec_seed, 1) gives D1 then D2 (n draws each), mix_seed(spec_seed, 2) gives D3,
-// and rademacher(u) = (u & 1) ? +1 : -1 (common.hpp:86).  One CTA per stream; each 312-word
-// twist runs as its two data-parallel halves (i < 156 reads only old words, i >= 156 reads
-// the new words i - 156, and i = 311 the new word 0 — the sequential order of the library
-// engine), then the block is tempered and emitted in parallel.  Bit-exact with the host
-// realisation (tests/test_newton.py), ~20x faster than drawing 3n values on the host, and
-// stream-ordered, so creating a fresh sketch per Newton iteration costs no host time.
+// and rademacher(u) = (u & 1) ? +1 : -1 (common.hpp:86).  One CTA per stream, one thread per
+// state word; each 312-word twist runs as its two data-parallel halves (i < 156 reads only
+// old words, i >= 156 reads the new words i - 156, and i = 311 the new word 0 — the
+// sequential order of the library engine) into the other half of a ping-pong state (two
+// barriers per twist), then every thread tempers and emits its word.  Bit-exact with the
+// host realisation (tests/test_gpu_parity.py::test_sketch_device_realisation_bit_exact),
+// stream-ordered, and launched at plan creation, so a fresh sketch per Newton iteration
+// costs no host time.
 // Outputs are the sketch layouts: D1, D3 natural, D2 transposed for the high-bit pass
 // (f[lo * 2^lsb + s] = D2[(s << lsa) + lo], see build_sketch).
-__global__ void __launch_bounds__(160) mt_rademacher_sketch_kernel(uint64_t seed_front, uint64_t seed_tail,
+__global__ void __launch_bounds__(320) mt_rademacher_sketch_kernel(uint64_t seed_front, uint64_t seed_tail,
                                                                    int64_t n, int lsa, int lsb, float* d1,
                                                                    float* d2t, float* d3) {
   constexpr int N = 312, M = 156;
   constexpr uint64_t A = 0xB5026F5AA96619E9ULL, UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL;
-  __shared__ uint64_t mt[N];
+  __shared__ uint64_t buf[2][N];  // ping-pong states: a twist reads one and writes the other
   const bool front = blockIdx.x == 0;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x;  // word t of the state
   if (t == 0) {
-    mt[0] = front ? seed_front : seed_tail;
-    for (int i = 1; i < N; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + uint64_t(i);
+    buf[0][0] = front ? seed_front : seed_tail;
+    for (int i = 1; i < N; ++i)
+      buf[0][i] = 6364136223846793005ULL * (buf[0][i - 1] ^ (buf[0][i - 1] >> 62)) + uint64_t(i);
   }
   __syncthreads();
   const int64_t draws = front ? 2 * n : n;
   const int64_t lo_mask = (int64_t(1) << lsa) - 1;
-  for (int64_t base = 0; base < draws; base += N) {
-    uint64_t v = 0;
-    if (t < M) {
-      const uint64_t y = (mt[t] & UM) | (mt[t + 1] & LM);
-      v = mt[t + M] ^ (y >> 1) ^ ((0 - (y & 1)) & A);
+  int c = 0;
+  for (int64_t base = 0; base < draws; base += N, c ^= 1) {
+    const uint64_t* cur = buf[c];
+    uint64_t* nxt = buf[c ^ 1];
+    if (t < M) {  // words 0..155: old words only
+      const uint64_t y = (cur[t] & UM) | (cur[t + 1] & LM);
+      nxt[t] = cur[t + M] ^ (y >> 1) ^ ((0 - (y & 1)) & A);
     }
     __syncthreads();
-    if (t < M) mt[t] = v;
-    __syncthreads();
-    if (t < N - M) {
-      const int i = M + t;
-      const uint64_t y = (mt[i] & UM) | (mt[i + 1 < N ? i + 1 : 0] & LM);
-      v = mt[i - M] ^ (y >> 1) ^ ((0 - (y & 1)) & A);
+    if (t >= M && t < N) {  // words 156..311: new words t - 156 (and new word 0 for t = 311)
+      const uint64_t y = (cur[t] & UM) | ((t + 1 < N ? cur[t + 1] : nxt[0]) & LM);
+      nxt[t] = nxt[t - M] ^ (y >> 1) ^ ((0 - (y & 1)) & A);
     }
     __syncthreads();
-    if (t < N - M) mt[M + t] = v;
-    __syncthreads();
-    for (int j = t; j < N; j += blockDim.x) {
-      const int64_t k = base + j;
-      if (k >= draws) break;
-      uint64_t y = mt[j];
+    // temper + emit word t (the next twist writes the other buffer)
+    const int64_t k = base + t;
+    if (t < N && k < draws) {
+      uint64_t y = nxt[t];
       y ^= (y >> 29) & 0x5555555555555555ULL;
       y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
       y ^= (y << 37) & 0xFFF7EEE000000000ULL;
@@ -478,7 +478,6 @@ __global__ void __launch_bounds__(160) mt_rademacher_sketch_kernel(uint64_t seed
         d2t[lsb > 0 ? (e & lo_mask) * (int64_t(1) << lsb) + (e >> lsa) : e] = r;
       }
     }
-    // (the next twist's first barrier orders these reads before its writes)
   }
 }
 
@@ -882,7 +881,7 @@ struct BigPlan {
       for (int di = 0; di < 3 && e == cudaSuccess; ++di)
         e = pool_alloc(reinterpret_cast<void**>(&sk_d[di]), static_cast<size_t>(nn) * 4, s);
       if (e == cudaSuccess) {
-        mt_rademacher_sketch_kernel<<<2, 160, 0, s>>>(mix_seed(dev_seed, 1), mix_seed(dev_seed, 2), nn, sk_lsa,
+        mt_rademacher_sketch_kernel<<<2, 320, 0, s>>>(mix_seed(dev_seed, 1), mix_seed(dev_seed, 2), nn, sk_lsa,
                                                       sk_lsb, sk_d[0], sk_d[1], sk_d[2]);
         e = cudaGetLastError();
       }
