@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -660,7 +661,12 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
   // calls still overlap H2D, kernel and D2H on the two copy engines; large ones keep the
   // per-chunk launch/copy overhead small.
   const int64_t row_bytes = std::max<int64_t>(std::max<int64_t>(out_row_bytes, in_row), 1);
-  const int64_t target = std::min<int64_t>(int64_t(48) << 20,
+  static const int64_t cap_mb = [] {
+    const char* e = std::getenv("SPN_HOST_CHUNK_MB");
+    const int64_t v = e ? std::atoll(e) : 48;
+    return v > 0 ? v : int64_t(48);
+  }();
+  const int64_t target = std::min<int64_t>(cap_mb << 20,
                                            std::max<int64_t>(int64_t(4) << 20, batch * row_bytes / 8));
   int64_t chunk = std::max<int64_t>(1, target / row_bytes);
   chunk = std::min(chunk, batch);
@@ -681,11 +687,18 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
     const int64_t rows = std::min(chunk, batch - r0);
     float* dx = static_cast<float*>(p->hbuf[s][0]);
     char* dout = static_cast<char*>(p->hbuf[s][1]);
-    SPN_CUDA(cudaMemcpy2DAsync(dx, in_row, x + r0 * ld_x, ld_x * 4, in_row, rows, cudaMemcpyHostToDevice,
-                               p->hs[s]));
+    if (ld_x * 4 == in_row)  // contiguous rows: one linear copy
+      SPN_CUDA(cudaMemcpyAsync(dx, x + r0 * ld_x, in_row * rows, cudaMemcpyHostToDevice, p->hs[s]));
+    else
+      SPN_CUDA(cudaMemcpy2DAsync(dx, in_row, x + r0 * ld_x, ld_x * 4, in_row, rows, cudaMemcpyHostToDevice,
+                                 p->hs[s]));
     if (spn_status st = launch(dx, rows, n_in, dout, p->hs[s])) return st;
-    SPN_CUDA(cudaMemcpy2DAsync(static_cast<char*>(out) + r0 * ld_out_bytes, ld_out_bytes, dout, out_row_bytes,
-                               out_row_bytes, rows, cudaMemcpyDeviceToHost, p->hs[s]));
+    if (ld_out_bytes == out_row_bytes)
+      SPN_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + r0 * ld_out_bytes, dout, out_row_bytes * rows,
+                               cudaMemcpyDeviceToHost, p->hs[s]));
+    else
+      SPN_CUDA(cudaMemcpy2DAsync(static_cast<char*>(out) + r0 * ld_out_bytes, ld_out_bytes, dout, out_row_bytes,
+                                 out_row_bytes, rows, cudaMemcpyDeviceToHost, p->hs[s]));
   }
   SPN_CUDA(cudaStreamSynchronize(p->hs[0]));
   SPN_CUDA(cudaStreamSynchronize(p->hs[1]));
