@@ -145,8 +145,9 @@ __device__ __forceinline__ void reg_fwht(float (&r)[R]) {
     const int h = 1 << b;
     if (b == 0) {
       // FFMA2 halves the issue slots but occupies the FP32 pipe longer than two FADDs:
-      // a win where issue/instruction fetch binds (R = 128, c3: 312 -> 302 ms), a loss
-      // where the FP32 pipe binds (R = 32, c2: 0.458 -> 0.479 ms).
+      // a win only while the unrolled R = 128 chain was instruction-fetch bound (c3:
+      // 312 -> 302 ms); with the looped chain it loses (289 vs 277 ms), and for R = 32
+      // too (c2: 0.458 -> 0.479 ms), so it is off by default (SPN_INPAIR_FFMA2_MIN_R).
       if constexpr (R >= kInpairFfma2MinR) {
 #pragma unroll
         for (int j = 0; j < R; j += 2) bfly_inpair(r[j], r[j + 1]);
