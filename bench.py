@@ -343,9 +343,52 @@ def run_ours(args, rank, world, local):
         "clocks": clk.summary(),
         "gpu_launches": w.launches_per_step * args.steps,
     }
+    result.update(secondary_rooflines(args.config, cfg, w, statistics.mean(step_ms), result["clocks"]))
     if args.config in ("c1", "c2") and not args.no_e2e:
         result["e2e"] = e2e_measure(args, w, world)
     return result, w
+
+
+# Issue floors from the ncu instruction mix (tools/sass_mix.py on profiles/r01_<c>_ncu_full.json, DESIGN.md
+# sections 3-4): warp-issue cycles per unit with FADD2 counted twice, at the clock the floor was computed for.
+ISSUE_FLOOR = {
+    "c2": {"ms": 0.356, "mhz": 1785.0, "model": "6.26 K issue cycles per sample (1536 FADD2 x2, 768 FADD, 432 sign "
+           "flips, 555 LDS/STS, 416 FMUL, 256 MUFU, ~450 address/loop) over 60000 samples on 592 SMSPs"},
+    "c3": {"ms": 205.6, "mhz": 1965.0, "model": "28.5 K warp-issue cycles per (vector, table) (9216 FADD2 x2, 3072 "
+           "FADD, 1931 LOP3 + 192 R2P sign flips, 1925 LDS/STS transposes, 576 LDG, 754 IMAD, argmax) over "
+           "2^20 x 8 items on 592 SMSPs"},
+}
+
+
+# L2-resident read-modify-write bandwidth measured on this pool's B200 (tools/microbench/mb.cu, in-place
+# float4 r+w over a 32 MB buffer, 148 x 4 CTAs): 12.3-12.9 TB/s at 16-32 MB, 9.3 TB/s at 64 MB.  (A torch
+# elementwise probe reaches only ~6.5 TB/s, its own kernel's limit, so it is not used as the roof.)
+L2_RMW_GBS = 12877.8
+
+
+def secondary_rooflines(name, cfg, w, step_ms, clocks):
+    """The roofs that actually bind the configs whose HBM fraction is low by construction: the multi-pass
+    configs (c4, c5) against the L2 read-modify-write rate (4 passes, each reading and writing the working
+    set through L2), the issue-bound ones (c2, c3) against their instruction-count floor."""
+    out = {}
+    if name in ("c4", "c5"):
+        if name == "c5":
+            l2_bytes = 4 * 2 * w.vectors * cfg["n"] * 4
+        else:  # passes 1-3 read + write A's columns, pass 4 reads them and writes the m gathered rows
+            l2_bytes = 7 * cfg["N"] * cfg["d"] * 4 + cfg["m"] * cfg["d"] * 4
+        peak = L2_RMW_GBS
+        ach = l2_bytes / (step_ms * 1e-3) / 1e9
+        out["roofline_l2"] = {"bound": "l2", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                              "traffic_model": "4 passes x (read + write) of the working set through L2",
+                              "l2_bytes_per_step": l2_bytes,
+                              "peak_source": "tools/microbench/mb.cu L2 rmw, 32 MB, this pool's B200"}
+    if name in ISSUE_FLOOR:
+        f = ISSUE_FLOOR[name]
+        mhz = clocks.get("sm_mhz") or f["mhz"]
+        floor = f["ms"] * f["mhz"] / mhz
+        out["roofline_issue"] = {"bound": "issue", "floor_ms": floor, "measured_ms": step_ms,
+                                 "frac": floor / step_ms, "sm_mhz": mhz, "model": f["model"]}
+    return out
 
 
 def traffic_from_profiles(config):
