@@ -288,7 +288,7 @@ constexpr int kPanelThreads = 256;
 __global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __restrict__ A, int d, int j0,
                                                                    int* __restrict__ flag) {
   __shared__ double L11[kNB][kNB + 1];
-  __shared__ double lkk_s;
+  __shared__ double lkk_s, inv_s[kNB];  // reciprocals of the pivots (multiplies, not divides)
   __shared__ int bad;
   if (*flag) return;
   const int nb = min(kNB, d - j0);
@@ -307,8 +307,10 @@ __global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __res
       if (!(p > 0.0)) {
         bad = 1;
       } else {
-        lkk_s = sqrt(p);
-        L11[k][k] = lkk_s;
+        const double sp = sqrt(p);
+        lkk_s = 1.0 / sp;
+        L11[k][k] = sp;
+        inv_s[k] = lkk_s;
       }
     }
     __syncthreads();
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __res
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int r = rq + 8 * q;
-        if (r > k && r < nb) L11[r][k] /= lkk_s;
+        if (r > k && r < nb) L11[r][k] *= lkk_s;
       }
     }
     __syncthreads();
@@ -339,6 +341,8 @@ __global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __res
     const int r = rq + 8 * q;
     if (r < nb && j <= r) A[(int64_t)(j0 + r) * d + j0 + j] = L11[r][j];
   }
+  // (the block is read through a volatile view: ptxas otherwise hoists all 528 entries into
+  // registers and spills — 255 registers + 112 B of stack)
   for (int i = j0 + nb + tid; i < d; i += kPanelThreads) {
     double l[kNB];
 #pragma unroll
@@ -348,8 +352,8 @@ __global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __res
       if (k < nb) {
         double sum = l[k];
 #pragma unroll
-        for (int m = 0; m < k; ++m) sum -= l[m] * L11[k][m];
-        l[k] = sum / L11[k][k];
+        for (int m = 0; m < k; ++m) sum -= l[m] * reinterpret_cast<volatile double(*)[kNB + 1]>(L11)[k][m];
+        l[k] = sum * inv_s[k];
       }
     }
 #pragma unroll
@@ -395,11 +399,15 @@ __global__ void __launch_bounds__(256) chol_update_kernel(double* __restrict__ A
 __global__ void __launch_bounds__(256) chol_solve_kernel(const double* __restrict__ L, int d,
                                                          const double* __restrict__ grad, double* __restrict__ step,
                                                          const int* __restrict__ flag) {
-  extern __shared__ double b[];  // [d]
+  extern __shared__ double b[];  // [d] right-hand side, then [d] reciprocals of the diagonal
+  double* inv = b + d;
   __shared__ double T[32][33];
   if (*flag) return;
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < d; i += blockDim.x) b[i] = -grad[i];
+  for (int i = tid; i < d; i += blockDim.x) {
+    b[i] = -grad[i];
+    inv[i] = 1.0 / L[(int64_t)i * d + i];  // off the sequential chains below
+  }
   __syncthreads();
   // forward: L y = b
   for (int kb = 0; kb < d; kb += 32) {
@@ -412,7 +420,7 @@ __global__ void __launch_bounds__(256) chol_solve_kernel(const double* __restric
     if (tid < 32) {
       double y = lane < nb ? b[kb + lane] : 0.0;
       for (int k = 0; k < nb; ++k) {
-        if (lane == k) y = y / T[k][k];
+        if (lane == k) y *= inv[kb + k];
         const double yk = __shfl_sync(0xffffffffu, y, k);
         if (lane > k) y -= T[lane][k] * yk;
       }
@@ -443,7 +451,7 @@ __global__ void __launch_bounds__(256) chol_solve_kernel(const double* __restric
     if (tid < 32) {
       double xv = lane < nb ? b[kb + lane] : 0.0;
       for (int k = nb - 1; k >= 0; --k) {
-        if (lane == k) xv = xv / T[k][k];
+        if (lane == k) xv *= inv[kb + k];
         const double xk = __shfl_sync(0xffffffffu, xv, k);
         if (lane < k) xv -= T[k][lane] * xk;
       }
@@ -696,7 +704,7 @@ spn_status factor_solve(spn_newton* w, const double* grad, double* step, cudaStr
       NWT_CUDA(cudaGetLastError());
     }
   }
-  chol_solve_kernel<<<1, 256, sizeof(double) * (size_t)d, s>>>(w->fact, d, grad, step, w->flag);
+  chol_solve_kernel<<<1, 256, 2 * sizeof(double) * (size_t)d, s>>>(w->fact, d, grad, step, w->flag);
   NWT_CUDA(cudaGetLastError());
   NWT_CUDA(cudaMemcpyAsync(w->flag_h, w->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   NWT_CUDA(cudaStreamSynchronize(s));
