@@ -480,7 +480,7 @@ def cpu_reference(config, budget_s=20.0, threads=None):
         y = np.cos(ang)[:, None] * x + np.sin(ang)[:, None] * u
         d = 2.0 * np.sin(ang / 2.0)
         dt = timed(lambda c: r.collision_curve(HD3, n, cfg["m"], x, y, d, 2, 91), 1)
-        return 2 * P * 2 / dt, {"kind": "reference", "cores": 1,
+        return 2 * P * 2 / dt, {"kind": "reference", "cores": 1, "cpu_model": cpu_model(),
                                 "sample": "collision_curve over all 20000 pairs x 2 trials (80000 hashed vectors); "
                                           "the reference's lsh.cpp driver, single-threaded"}
     elif config == "c6":  # one reference sketched_step (newton_sketch.cpp:103-122, single-threaded code)
@@ -488,7 +488,7 @@ def cpu_reference(config, budget_s=20.0, threads=None):
         y = np.where(rng.random(cfg["N"]) < 0.5, -1.0, 1.0)
         x = np.full(cfg["d"], 0.01)
         dt = timed(lambda c: r.sketched_step(a, y, x, HD3, cfg["m"], o.mix_seed(3, 0)), 1)
-        return cfg["d"] / dt, {"kind": "reference", "cores": 1,
+        return cfg["d"] / dt, {"kind": "reference", "cores": 1, "cpu_model": cpu_model(),
                                "sample": "1 sketched_step (131072 x 256, m = 2048, HD3) of c6 = 256 sketched "
                                          "columns; the reference's newton_sketch.cpp, single-threaded"}
     else:
@@ -503,8 +503,19 @@ def cpu_reference(config, budget_s=20.0, threads=None):
     dt = timed(fn, probe)
     count = int(min(total, max(probe, probe * budget_s / max(dt, 1e-6) * 0.5)))
     dt = timed(fn, count)
-    return count / dt, {"kind": "reference", "cores": threads,
+    return count / dt, {"kind": "reference", "cores": threads, "cpu_model": cpu_model(),
                         "sample": f"{count} of {total} vectors of {config}: {what}; oracle/_ref on {threads} threads"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(args, rank, world):
