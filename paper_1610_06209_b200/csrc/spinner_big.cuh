@@ -528,10 +528,11 @@ struct BigPlan {
   uint64_t dev_seed = 0;  // spec seed of the block
   // sk_d, sk_d1s and rowmap come from the stream-ordered pool; they go back to it after the
   // last call on every stream that used them (uses), without a device-wide cudaFree
-  // synchronisation.  ev_ready marks the realisation / row map on the stream that made them;
-  // calls on other streams wait for it.
+  // synchronisation.  ev_ready marks the device realisation, ev_map the last row-map fill;
+  // every call waits for both on its own stream (they may have been made on other streams).
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
-  cudaEvent_t ev_ready = nullptr;
+  cudaEvent_t ev_ready = nullptr;  // the device realisation (made on the realisation stream)
+  cudaEvent_t ev_map = nullptr;    // the last row-map fill (made on the calling stream)
   cudaError_t note_use(cudaStream_t s) {
     for (auto& u : uses)
       if (u.first == s) return cudaEventRecord(u.second, s);
@@ -546,9 +547,16 @@ struct BigPlan {
       if (cudaError_t r = cudaStreamWaitEvent(s, u.second, 0)) return r;
     return cudaSuccess;
   }
-  cudaError_t mark_ready(cudaStream_t s) {
-    cudaError_t r = ev_ready ? cudaSuccess : cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming);
-    return r == cudaSuccess ? cudaEventRecord(ev_ready, s) : r;
+  static cudaError_t mark(cudaEvent_t* ev, cudaStream_t s) {
+    cudaError_t r = *ev ? cudaSuccess : cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    return r == cudaSuccess ? cudaEventRecord(*ev, s) : r;
+  }
+  // make s wait for the realisation and the current row map, wherever they were made
+  cudaError_t wait_ready(cudaStream_t s) {
+    cudaError_t r = cudaSuccess;
+    if (ev_ready) r = cudaStreamWaitEvent(s, ev_ready, 0);
+    if (r == cudaSuccess && ev_map) r = cudaStreamWaitEvent(s, ev_map, 0);
+    return r;
   }
   // scratch
   float* work = nullptr;
@@ -573,7 +581,7 @@ struct BigPlan {
       cudaStream_t fs = device_stream(kFreeStreamSlot);
       if (fs) {
         wait_uses(fs);
-        if (ev_ready) cudaStreamWaitEvent(fs, ev_ready, 0);
+        wait_ready(fs);
       }
       auto pfree = [&](void* q) {
         if (!q) return;
@@ -590,7 +598,8 @@ struct BigPlan {
       for (auto& u : uses) cudaEventDestroy(u.second);
       uses.clear();
       if (ev_ready) cudaEventDestroy(ev_ready);
-      ev_ready = nullptr;
+      if (ev_map) cudaEventDestroy(ev_map);
+      ev_ready = ev_map = nullptr;
     }
     if (drow2) cudaFree(drow2);
     for (float** q : {&srow1, &srow3, &stile2}) {
@@ -885,7 +894,7 @@ struct BigPlan {
                                                       sk_lsb, sk_d[0], sk_d[1], sk_d[2]);
         e = cudaGetLastError();
       }
-      if (e == cudaSuccess) e = mark_ready(s);
+      if (e == cudaSuccess) e = mark(&ev_ready, s);
       if (e != cudaSuccess) return err(e, "device realisation of the sketch diagonals");
       sk_ready = true;
       return SPN_OK;
@@ -922,7 +931,7 @@ struct BigPlan {
             rowmap, nn, m_out);
         e = cudaGetLastError();
       }
-      if (e == cudaSuccess) e = mark_ready(s);
+      if (e == cudaSuccess) e = mark(&ev_map, s);
       if (e != cudaSuccess) return err(e, "row map");
       rowmap_key.clear();
       rowmap_m = m_out;
@@ -961,9 +970,8 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
   std::lock_guard<std::mutex> lock(bp->mu);
   if (spn_status st = bp->build_sketch(nn, d, s0)) return st;
   if (spn_status st = bp->set_rowmap(nn, rows, m_out, s0)) return st;
-  if (bp->ev_ready) {  // realisation / row map made on another stream
-    if (cudaError_t e = cudaStreamWaitEvent(s0, bp->ev_ready, 0)) return BigPlan::err(e, "sketch ready");
-  }
+  // the realisation (realisation stream) and the row map (possibly another caller stream)
+  if (cudaError_t e = bp->wait_ready(s0)) return BigPlan::err(e, "sketch ready");
   const float* d1 = bp->sk_d[0];
   if (row_scale) {
     cudaError_t e = cudaSuccess;

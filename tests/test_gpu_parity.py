@@ -341,3 +341,24 @@ def test_lazy_plan_apply_and_side_stream(spn, oracle, torch):
     assert torch.equal(o1, want) and torch.equal(o2, want)
     del sk  # pool memory goes back after the uses recorded on both streams
     torch.cuda.synchronize()
+
+
+def test_plan_destroyed_while_in_flight(spn, oracle, torch):
+    """Dropping a sketch plan right after an asynchronous call returns its pooled memory only after
+    that call (stream-ordered free after the recorded use): a plan created next, reusing the pool,
+    must not disturb the first result."""
+    N, m = 1 << 17, 512
+    a = dev(torch, oracle.gaussian_rows(12, N, 64))
+    ref1 = spn.SketchOperator(spn.SpinnerVariant.hd3_hd2_hd1, N, m, 101).apply(a).clone()
+    ref2 = spn.SketchOperator(spn.SpinnerVariant.hd3_hd2_hd1, N, m, 202).apply(a).clone()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        torch.cuda._sleep(50_000_000)  # keep the device busy so the calls below are still queued
+        sk1 = spn.SketchOperator(spn.SpinnerVariant.hd3_hd2_hd1, N, m, 101)
+        out1 = sk1.apply(a)
+        del sk1
+        sk2 = spn.SketchOperator(spn.SpinnerVariant.hd3_hd2_hd1, N, m, 202)
+        out2 = sk2.apply(a)
+        del sk2
+        torch.cuda.synchronize()
+        assert torch.equal(out1, ref1) and torch.equal(out2, ref2)
