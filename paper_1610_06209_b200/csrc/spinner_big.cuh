@@ -945,7 +945,8 @@ struct BigPlan {
     }
     cudaError_t e = cudaSuccess;
     if (!rowmap) e = pool_alloc(reinterpret_cast<void**>(&rowmap), static_cast<size_t>(nn) * 4, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // previous users of the map are done
+    else e = wait_uses(s);  // earlier calls (any stream) are done with the old map ...
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // ... once s is
     if (e == cudaSuccess) e = cudaMemcpy(rowmap, map.data(), map.size() * 4, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return err(e, "row map");
     rowmap_key = std::move(key);
