@@ -83,8 +83,15 @@ def dist_init():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("SPN_BENCH_BACKEND") == "gloo":
+            # test mode only: exercise the multi-rank code path with every rank on the GPUs there
+            # are (ranks share a device; timings are then contended and not a scaling result)
+            local = local % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
