@@ -287,8 +287,9 @@ constexpr int kPanelThreads = 256;
 // pairs per thread); the sub-diagonal rows (one per thread per round) are solved after.
 __global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __restrict__ A, int d, int j0,
                                                                    int* __restrict__ flag) {
-  __shared__ double L11[kNB][kNB + 1];
-  __shared__ double lkk_s, inv_s[kNB];  // reciprocals of the pivots (multiplies, not divides)
+  __shared__ double L11[kNB][kNB + 1];  // working block: columns > k still being updated
+  __shared__ double Ls[kNB][kNB + 1];   // finished, scaled columns: Ls[c][r] = L[r][c]
+  __shared__ double inv_s[kNB];         // 1 / L_kk
   __shared__ int bad;
   if (*flag) return;
   const int nb = min(kNB, d - j0);
@@ -301,33 +302,37 @@ __global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __res
     if (r < nb && j <= r) L11[r][j] = A[(int64_t)(j0 + r) * d + j0 + j];
   }
   __syncthreads();
+  // Two barriers per pivot (the pivot chain is the panel's critical path: tools/microbench/
+  // f64lat.cu): thread 0 publishes 1/sqrt(p) (rsqrt, 66 cycles dependent latency, instead of
+  // sqrt + divide, 160); then in one step the j == k threads store the scaled column k into Ls
+  // (not in place, so nobody overwrites what the others read) and the j > k threads apply the
+  // rank-1 update with the same rounded scaled values.
   for (int k = 0; k < nb; ++k) {
     if (tid == 0) {
       const double p = L11[k][k];
       if (!(p > 0.0)) {
         bad = 1;
       } else {
-        const double sp = sqrt(p);
-        lkk_s = 1.0 / sp;
-        L11[k][k] = sp;
-        inv_s[k] = lkk_s;
+        const double ik = rsqrt(p);
+        inv_s[k] = ik;
+        Ls[k][k] = p * ik;  // sqrt(p) to an ulp
       }
     }
     __syncthreads();
     if (bad) break;
+    const double ik = inv_s[k];
     if (j == k) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int r = rq + 8 * q;
-        if (r > k && r < nb) L11[r][k] *= lkk_s;
+        if (r > k && r < nb) Ls[k][r] = L11[r][k] * ik;
       }
-    }
-    __syncthreads();
-    if (j > k) {
+    } else if (j > k && j < nb) {
+      const double ljk = L11[j][k] * ik;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int r = rq + 8 * q;
-        if (r >= j && r < nb) L11[r][j] -= L11[r][k] * L11[j][k];
+        if (r >= j && r < nb) L11[r][j] -= (L11[r][k] * ik) * ljk;
       }
     }
     __syncthreads();
@@ -339,7 +344,7 @@ __global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __res
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int r = rq + 8 * q;
-    if (r < nb && j <= r) A[(int64_t)(j0 + r) * d + j0 + j] = L11[r][j];
+    if (r < nb && j <= r) A[(int64_t)(j0 + r) * d + j0 + j] = Ls[j][r];
   }
   // (the block is read through a volatile view: ptxas otherwise hoists all 528 entries into
   // registers and spills — 255 registers + 112 B of stack)
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __res
       if (k < nb) {
         double sum = l[k];
 #pragma unroll
-        for (int m = 0; m < k; ++m) sum -= l[m] * reinterpret_cast<volatile double(*)[kNB + 1]>(L11)[k][m];
+        for (int m = 0; m < k; ++m) sum -= l[m] * reinterpret_cast<volatile double(*)[kNB + 1]>(Ls)[m][k];
         l[k] = sum * inv_s[k];
       }
     }
