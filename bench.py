@@ -432,7 +432,7 @@ def e2e_measure(args, w, world):
     dt = max_over_ranks(dt, world)
     return {"value": w.vectors * world * steps / dt, "unit": UNIT, "h2d_bytes_per_step": bi,
             "d2h_bytes_per_step": bo, "steps": steps, "api": "spn_embed_f32_host" if args.config == "c2"
-            else "spn_apply_f32_host"}
+            else "spn_apply_f32_host (the y projection only; the host API returns ids through spn_hash_f32_host)"}
 
 
 # ---------------------------------------------------------------- CPU reference
