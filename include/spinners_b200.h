@@ -110,13 +110,15 @@ SPN_API spn_status spn_apply_f32(const spn_plan* plan, const float* x, int64_t b
 
 /* ids[b*tables + t] = index + (sign < 0 ? k : 0) of signed_argmax over table t's
  * k rows (ties -> smallest index, sign(0) = +1).  If y != NULL (tables == 1)
- * the projection is stored as by spn_apply_f32. */
+ * the projection is stored as by spn_apply_f32.  Any n <= 2^20: n <= 2^14 runs the fused
+ * kernel, larger n the multi-pass projection followed by a row argmax. */
 SPN_API spn_status spn_hash_f32(const spn_plan* plan, const float* x, int64_t batch,
                                 int64_t ld_x, int64_t n_in, int32_t* ids, float* y,
                                 int64_t ld_y, void* stream);
 
 /* Gaussian: out[b*ld + i] = cos(z_i/sigma)/sqrt(k), out[b*ld + k + i] = sin(z_i/sigma)/sqrt(k);
- * angular: out[b*ld + i] = z_i < 0 ? -1 : +1.   z = scale * stacked(x). */
+ * angular: out[b*ld + i] = z_i < 0 ? -1 : +1.   z = scale * stacked(x).  Any n <= 2^20 (n > 2^14:
+ * the multi-pass projection into out, then the feature epilogue in place). */
 SPN_API spn_status spn_embed_f32(const spn_plan* plan, int32_t kind, double sigma, const float* x,
                                  int64_t batch, int64_t ld_x, int64_t n_in, float* out,
                                  int64_t ld_out, void* stream);

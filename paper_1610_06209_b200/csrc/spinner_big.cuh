@@ -487,6 +487,80 @@ __global__ void rowmap_first_kernel(int32_t* map, int64_t nn, int64_t m) {
     map[i] = i < m ? static_cast<int32_t>(i) : -1;
 }
 
+// ------------------------------------------------ row epilogues for n > 2^14 (hash / embed)
+// The multi-pass path produces y = s * first_m(H D3 H D2 H D1 x) per block; these kernels turn
+// the stacked rows into the reference's hash ids and features (one CTA per row, coalesced).
+
+// signed argmax of a row (lsh.cpp:9-21): max |y|, ties to the smallest index, sign(0) = +1;
+// id = index + (y < 0 ? k : 0), stored at ids[v * ld_ids + col]
+__global__ void __launch_bounds__(256) rows_signed_argmax_kernel(const float* __restrict__ y, int64_t ld_y,
+                                                                 int64_t k, int64_t batch, int32_t* __restrict__ ids,
+                                                                 int64_t ld_ids, int64_t col) {
+  __shared__ float sa[8], sv[8];
+  __shared__ int64_t si[8];
+  for (int64_t v = blockIdx.x; v < batch; v += gridDim.x) {
+    const float* row = y + v * ld_y;
+    float ba = -1.0f, bv = 0.0f;
+    int64_t bi = INT64_MAX;
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {  // increasing i: strict '>' keeps the first
+      const float val = row[i], a = fabsf(val);
+      if (a > ba) {
+        ba = a;
+        bi = i;
+        bv = val;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float oa = __shfl_xor_sync(0xffffffffu, ba, off), ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (oa > ba || (oa == ba && oi < bi)) {
+        ba = oa;
+        bi = oi;
+        bv = ov;
+      }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+      sa[w] = ba;
+      si[w] = bi;
+      sv[w] = bv;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+        if (sa[q] > ba || (sa[q] == ba && si[q] < bi)) {
+          ba = sa[q];
+          bi = si[q];
+          bv = sv[q];
+        }
+      ids[v * ld_ids + col] = static_cast<int32_t>(bi + (bv < 0.0f ? k : 0));
+    }
+    __syncthreads();
+  }
+}
+
+// embed epilogue in place on rows whose first k entries hold z (kernels.cpp:17-36):
+// Gaussian: out[i] = norm cos(z_i / sigma), out[k + i] = norm sin(z_i / sigma); angular:
+// out[i] = sign(z_i), sign(0) = +1
+__global__ void __launch_bounds__(256) rows_embed_kernel(float* __restrict__ out, int64_t ld_out, int64_t k,
+                                                         int64_t batch, int gaussian, float inv_sigma, float norm) {
+  for (int64_t v = blockIdx.x; v < batch; v += gridDim.x) {
+    float* row = out + v * ld_out;
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
+      const float z = row[i];
+      if (gaussian) {
+        float sn, cs;
+        sincosf(z * inv_sigma, &sn, &cs);
+        row[i] = norm * cs;
+        row[k + i] = norm * sn;
+      } else {
+        row[i] = z < 0.0f ? -1.0f : 1.0f;
+      }
+    }
+  }
+}
+
 struct Scratch {  // freed (stream-ordered) on `s` when the scope ends
   void* p = nullptr;
   cudaStream_t s = nullptr;
@@ -744,8 +818,10 @@ struct BigPlan {
   }
 
   // y = relu?(c * first rows of (H D3 H D2 H D1 x)) for every block (tables == 1).
+  // tb0: first (table, block) diagonal set to use — table t of a multi-table plan is tb0 = t * blocks
   spn_status apply(const float* x, int64_t batch, int64_t ld_x, int64_t n_in, float* y, int64_t ld_y,
-                   int relu, int64_t k, int64_t m, int64_t blocks, double c, int sms, cudaStream_t s0) {
+                   int relu, int64_t k, int64_t m, int64_t blocks, double c, int sms, cudaStream_t s0,
+                   int64_t tb0 = 0) {
     if (batch == 0) return SPN_OK;
     std::lock_guard<std::mutex> lock(mu);
     if (spn_status st = build_now()) return st;
@@ -781,7 +857,7 @@ struct BigPlan {
           rp.dst_vstride = wstride;
           rp.nseg = n / C;
           rp.nvec = nv;
-          rp.d = srow1 + b * n;
+          rp.d = srow1 + (tb0 + b) * n;
           e = launch_srow_lc(lc, RP_FIRST, rp, sms, s);
           if (e != cudaSuccess) return err(e, "rowpass P1");
           ColParams cp{};
@@ -799,14 +875,14 @@ struct BigPlan {
           cp.nlo = 1;
           cp.nvec = nv;
           cp.pdl = 1;
-          cp.dd[1] = stile2 + b * n;
+          cp.dd[1] = stile2 + (tb0 + b) * n;
           const bool tma = lr >= 5 && al16(y, ld_y);
           e = tma ? launch_tcol_ls(lr, SC_VMID, cp, sms, s) : launch_scol_ls(lr, SC_VMID, cp, sms, s);
           if (e != cudaSuccess) return err(e, "colpass P2");
           rp.src = W;
           rp.src_vstride = wstride;
           rp.n_in = n;
-          rp.d = srow3 + b * n;
+          rp.d = srow3 + (tb0 + b) * n;
           e = launch_srow_lc(lc, RP_MID, rp, sms, s);
           if (e != cudaSuccess) return err(e, "rowpass P3");
           cp.dd[1] = nullptr;
@@ -833,7 +909,7 @@ struct BigPlan {
         cp.nhi = 1;
         cp.nlo = 1;
         cp.nvec = nv;
-        cp.dd[0] = dnat[0] + b * n;
+        cp.dd[0] = dnat[0] + (tb0 + b) * n;
         cp.d_ld = C;
         e = launch_col_ls(lr, CP_FIRST, DM_PER_ELEM, cp, sms, s);  // P1: D1, Hr
         if (e != cudaSuccess) return err(e, "colpass P1");
@@ -842,14 +918,14 @@ struct BigPlan {
         rp.vstride = wstride;
         rp.nseg = n / C;
         rp.nvec = nv;
-        rp.d_mid = drow2 + b * n;
+        rp.d_mid = drow2 + (tb0 + b) * n;
         e = launch_row<false>(rp, sms, s);  // P2: Hc, D2, Hc
         if (e != cudaSuccess) return err(e, "rowpass P2");
         cp.src = W;
         cp.src_vstride = wstride;
         cp.src_valid = n;
         cp.dd[0] = nullptr;
-        cp.dd[1] = dnat[2] + b * n;
+        cp.dd[1] = dnat[2] + (tb0 + b) * n;
         e = launch_col_ls(lr, CP_MID, DM_PER_ELEM, cp, sms, s);  // P3: Hr, D3, Hr
         if (e != cudaSuccess) return err(e, "colpass P3");
         rp.y = y + v0 * ld_y + b * m;

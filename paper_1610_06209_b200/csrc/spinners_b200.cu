@@ -271,6 +271,58 @@ spn_status run_vec(const spn_plan* p, int op, spn::VecParams& v, cudaStream_t s)
   return SPN_OK;
 }
 
+// n > 2^14: the multi-pass apply per table into y (or a chunked workspace), then the signed
+// argmax per row (lsh.cpp:23-30 over the stacked rows; SURVEY a14.6 multi-table encoding).
+spn_status big_hash(spn_plan* p, const float* x, int64_t batch, int64_t ld_x, int64_t n_in, int32_t* ids,
+                    float* y, int64_t ld_y, cudaStream_t s) {
+  if (batch == 0) return SPN_OK;
+  DeviceGuard g(p->device);
+  p->ensure_host_d();
+  const double c = p->scale * std::pow(static_cast<double>(p->n), -1.5);
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(batch, int64_t(p->sms) * 8));
+  if (y) {  // single table: y is the caller's buffer
+    if (spn_status st = p->big.apply(x, batch, ld_x, n_in, y, ld_y, 0, p->k, p->m, p->blocks, c, p->sms, s)) return st;
+    spn::rows_signed_argmax_kernel<<<grid, 256, 0, s>>>(y, ld_y, p->k, batch, ids, p->tables, 0);
+    SPN_CUDA(cudaGetLastError());
+    return SPN_OK;
+  }
+  const int64_t ld = (p->k + 3) / 4 * 4;
+  const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t(256) << 20) / (ld * 4)));
+  spn::Scratch ws;
+  SPN_CUDA(ws.alloc(sizeof(float) * static_cast<size_t>(rows * ld), s));
+  float* w = static_cast<float*>(ws.p);
+  for (int64_t r0 = 0; r0 < batch; r0 += rows) {
+    const int64_t nr = std::min(rows, batch - r0);
+    for (int64_t t = 0; t < p->tables; ++t) {
+      if (spn_status st = p->big.apply(x + r0 * ld_x, nr, ld_x, n_in, w, ld, 0, p->k, p->m, p->blocks, c, p->sms, s,
+                                        t * p->blocks))
+        return st;
+      spn::rows_signed_argmax_kernel<<<static_cast<unsigned>(std::min<int64_t>(nr, int64_t(p->sms) * 8)), 256, 0, s>>>(
+          w, ld, p->k, nr, ids + r0 * p->tables, p->tables, t);
+      SPN_CUDA(cudaGetLastError());
+    }
+  }
+  return SPN_OK;
+}
+
+// n > 2^14: z = the multi-pass apply straight into the feature rows, then the cos/sin (or sign)
+// epilogue in place (kernels.cpp:17-36).
+spn_status big_embed(spn_plan* p, int32_t kind, double sigma, const float* x, int64_t batch, int64_t ld_x,
+                     int64_t n_in, float* out, int64_t ld_out, cudaStream_t s) {
+  if (batch == 0) return SPN_OK;
+  DeviceGuard g(p->device);
+  p->ensure_host_d();
+  const double c = p->scale * std::pow(static_cast<double>(p->n), -1.5);
+  if (spn_status st = p->big.apply(x, batch, ld_x, n_in, out, ld_out, 0, p->k, p->m, p->blocks, c, p->sms, s))
+    return st;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(batch, int64_t(p->sms) * 8));
+  spn::rows_embed_kernel<<<grid, 256, 0, s>>>(out, ld_out, p->k, batch, kind == SPN_EMBED_GAUSSIAN ? 1 : 0,
+                                               static_cast<float>(1.0 / sigma),
+                                               static_cast<float>(1.0 / std::sqrt(static_cast<double>(p->k))));
+  SPN_CUDA(cudaGetLastError());
+  return SPN_OK;
+}
+
 }  // namespace
 
 // =============================================================================== C ABI
@@ -492,7 +544,8 @@ spn_status spn_hash_f32(const spn_plan* p, const float* x, int64_t batch, int64_
   if (y && p->tables != 1) return fail(SPN_EINVAL, "y output needs a single-table plan");
   if (y && ld_y < p->k) return fail(SPN_EINVAL, "ld_y < k");
   if (p->k >= (int64_t(1) << 30)) return fail(SPN_EDIM, "2k must fit int32 ids");
-  if (p->log_n > kMaxLogNVec) return fail(SPN_EUNSUPPORTED, "hash with n > 2^14 not implemented");
+  if (p->log_n > kMaxLogNVec)
+    return big_hash(const_cast<spn_plan*>(p), x, batch, ld_x, n_in, ids, y, ld_y, static_cast<cudaStream_t>(stream));
   spn::VecParams v = base_params(p);
   v.x = x;
   v.ld_x = ld_x;
@@ -576,7 +629,9 @@ spn_status spn_embed_f32(const spn_plan* p, int32_t kind, double sigma, const fl
     return spn::family_run(p->fam, kind == SPN_EMBED_GAUSSIAN ? 2 : 3, x, batch, ld_x, n_in, out, ld_out, 0, sigma,
                            static_cast<cudaStream_t>(stream));
   }
-  if (p->log_n > kMaxLogNVec) return fail(SPN_EUNSUPPORTED, "embed with n > 2^14 not implemented");
+  if (p->log_n > kMaxLogNVec)
+    return big_embed(const_cast<spn_plan*>(p), kind, sigma, x, batch, ld_x, n_in, out, ld_out,
+                     static_cast<cudaStream_t>(stream));
   spn::VecParams v = base_params(p);
   v.x = x;
   v.ld_x = ld_x;

@@ -362,3 +362,55 @@ def test_plan_destroyed_while_in_flight(spn, oracle, torch):
         del sk2
         torch.cuda.synchronize()
         assert torch.equal(out1, ref1) and torch.equal(out2, ref2)
+
+
+# ---------------------------------------------- hash / embed beyond the fused sizes (n > 2^14)
+@pytest.mark.parametrize("logn", [15, 16, 18])
+def test_big_hash_multitable(spn, oracle, torch, logn):
+    """CrossPolytopeHasher::hash at n > 2^14 (multi-pass projection + row argmax), three tables,
+    full and truncated tables, against the oracle (lsh.cpp:9-30)."""
+    n = 1 << logn
+    for m in (n, n // 2 + 3):
+        seeds = [spn.mix_seed(9 + logn, t) for t in range(3)]
+        h = spn.MultiTableHasher(spn.SpinnerVariant.hd3_hd2_hd1, n, m, 3, table_seeds=seeds)
+        x = oracle.gaussian_rows(logn + m, 5, n, unit=True)
+        ids = h.hash_ids(dev(torch, x)).cpu().numpy()
+        assert ids.shape == (5, 3)
+        for t in range(3):
+            d = oracle.realize(HD3, n, m, m, seeds[t])
+            want, gaps = oracle.hash(*d, n, m, m, 1, math.sqrt(n), x)
+            assert_ids(ids[:, t], want[:, 0], gaps[:, 0])
+
+
+def test_big_hash_with_projection(spn, oracle, torch):
+    n = 1 << 15
+    sp = spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, n, n, n, 44, scale=1.0)
+    x = oracle.gaussian_rows(3, 4, n, unit=True)
+    y = torch.empty((4, n), device="cuda")
+    ids = sp.plan.hash(dev(torch, x), y_out=y).cpu().numpy()[:, 0]
+    d = oracle.realize(HD3, n, n, n, 44)
+    assert row_rel(y.cpu().numpy(), oracle.apply(*d, n, n, n, 1.0, x)).max() <= RTOL
+    want, gaps = oracle.hash(*d, n, n, n, 1, 1.0, x)
+    assert_ids(ids, want[:, 0], gaps[:, 0])
+
+
+@pytest.mark.parametrize("logn", [15, 17])
+@pytest.mark.parametrize("kind", ["gaussian", "angular"])
+def test_big_embed(spn, oracle, torch, logn, kind):
+    """embed (kernels.cpp:17-36) at n > 2^14, stacked k > m with a truncated last block, ragged n_in."""
+    n = 1 << logn
+    k = n + n // 2 + 5
+    sp = spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, n, n, k, 5 + logn)
+    kk = spn.KernelKind.gaussian(3.0) if kind == "gaussian" else spn.KernelKind.angular()
+    n_in = n - 77
+    # rows of norm 20 (angles |z / sigma| of a few units): the fp32 projection's absolute angle error
+    # grows with |z|, so uniform [0, 1] rows of this length (|z| ~ sqrt(n / 3) ~ 200) would sit at the
+    # fp32 floor of the 1e-5 bar whatever the kernel (the reference is fp64)
+    x = 20.0 * oracle.gaussian_rows(logn, 3, n_in, unit=True)
+    f = spn.embed(spn.FeatureMap(sp, kk), dev(torch, x)).cpu().numpy()
+    d = tuple(a[0] for a in sp.plan.diagonals())
+    want = oracle.embed(*d, n, n, k, math.sqrt(n), 0 if kind == "gaussian" else 1, 3.0, x, n_in=n_in)
+    if kind == "gaussian":
+        assert row_rel(f, want).max() <= RTOL
+    else:  # signs: exact except where |z| is at rounding level
+        assert np.mean(f == want) > 0.9999
