@@ -143,6 +143,21 @@ SPN_API spn_status spn_embed_f32_host(const spn_plan* plan, int32_t kind, double
                                       const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
                                       float* out, int64_t ld_out);
 
+/* fwht_normalized (transforms.hpp:13; transforms.cpp:52-71) of every row: y_b = H_n x_b with the
+ * orthonormal Walsh-Hadamard H_n; n a power of two <= 2^20 (n = 1: a copy).  Runs the spinner
+ * kernels with unit diagonals (H H H = H) on a plan cached per (device, n); x may equal y. */
+SPN_API spn_status spn_fwht_f32(int64_t n, const float* x, int64_t batch, int64_t ld_x, float* y,
+                                int64_t ld_y, int32_t device, void* stream);
+SPN_API spn_status spn_fwht_f32_host(int64_t n, const float* x, int64_t batch, int64_t ld_x, float* y,
+                                     int64_t ld_y, int32_t device);
+
+/* diag_matvec (transforms.hpp:59; transforms.cpp:228-235) of every row: y_b = d (.) x_b.  The
+ * reference's finiteness checks stay in the C++ drop-in; the device does not scan. */
+SPN_API spn_status spn_diag_f32(int64_t n, const float* d, const float* x, int64_t batch, int64_t ld_x,
+                                float* y, int64_t ld_y, void* stream);
+SPN_API spn_status spn_diag_f32_host(int64_t n, const float* d, const float* x, int64_t batch, int64_t ld_x,
+                                     float* y, int64_t ld_y, int32_t device);
+
 /* Builder-defined coordinate sampler P (BASELINE config 4): m distinct indices of
  * [0, N) via a partial Fisher-Yates driven by Rng(mix_seed(seed, 0x5a3b)), sorted. */
 SPN_API spn_status spn_sample_rows(int64_t N, int64_t m, uint64_t seed, int64_t* out);

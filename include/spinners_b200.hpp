@@ -58,6 +58,32 @@ inline void check_finite(const Vec64& x, const char* what) {  // common.hpp:37-4
     if (!std::isfinite(v)) throw DomainError(std::string(what) + ": non-finite entry");
 }
 
+// transforms.hpp:13 / transforms.cpp:52-71 — the orthonormal Walsh-Hadamard transform, on the device
+inline Vec64 fwht_normalized(Vec64 x) {
+  const std::size_t n = x.size();
+  if (n == 0 || (n & (n - 1)) != 0)
+    throw DimensionError("fwht_normalized: length must be a power of two, got " + std::to_string(n));
+  check_finite(x, "fwht_normalized");
+  std::vector<float> xf(x.begin(), x.end()), yf(n);
+  check(spn_fwht_f32_host(static_cast<int64_t>(n), xf.data(), 1, static_cast<int64_t>(n), yf.data(),
+                          static_cast<int64_t>(n), 0));
+  return Vec64(yf.begin(), yf.end());
+}
+
+// transforms.hpp:59 / transforms.cpp:228-235 — y = d (.) x, on the device
+inline Vec64 diag_matvec(const Vec64& d, const Vec64& x) {
+  if (d.size() != x.size())
+    throw DimensionError("diag_matvec: length mismatch (" + std::to_string(d.size()) + " vs " +
+                         std::to_string(x.size()) + ")");
+  check_finite(d, "diag_matvec.d");
+  check_finite(x, "diag_matvec.x");
+  if (x.empty()) return Vec64();
+  std::vector<float> df(d.begin(), d.end()), xf(x.begin(), x.end()), yf(x.size());
+  const auto n = static_cast<int64_t>(x.size());
+  check(spn_diag_f32_host(n, df.data(), xf.data(), 1, n, yf.data(), n, 0));
+  return Vec64(yf.begin(), yf.end());
+}
+
 enum class SpinnerVariant {  // spinner.hpp:18-25
   hd3_hd2_hd1 = SPN_HD3_HD2_HD1,
   hdg_hd2_hd1 = SPN_HDG_HD2_HD1,

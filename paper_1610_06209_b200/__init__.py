@@ -81,6 +81,10 @@ _embed_host = _sig("spn_embed_f32_host", C.c_int, [_vp, _i32, _dbl, _vp, _i64, _
 _sample_rows = _sig("spn_sample_rows", C.c_int, [_i64, _i64, _u64, _vp])
 _mix_seed = _sig("spn_mix_seed", _u64, [_u64, _u64])
 _check_rows = _sig("spn_check_rows_f32", C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp])
+_fwht = _sig("spn_fwht_f32", C.c_int, [_i64, _vp, _i64, _i64, _vp, _i64, _i32, _vp])
+_fwht_host = _sig("spn_fwht_f32_host", C.c_int, [_i64, _vp, _i64, _i64, _vp, _i64, _i32])
+_diag = _sig("spn_diag_f32", C.c_int, [_i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp])
+_diag_host = _sig("spn_diag_f32_host", C.c_int, [_i64, _vp, _vp, _i64, _i64, _vp, _i64, _i32])
 
 SPN_OK, SPN_EDIM, SPN_EDOMAIN, SPN_ECUDA, SPN_ENOMEM, SPN_EUNSUPPORTED, SPN_EINVAL, SPN_ESINGULAR = range(8)
 ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_create",
@@ -92,7 +96,8 @@ ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_c
                "spn_ar1_problem", "spn_newton_set_problem", "spn_logistic_eval_host", "spn_hessian_sqrt_host",
                "spn_sketched_step_host", "spn_logistic_line_host", "spn_collision_hits_f32", "spn_gram_exact_f32",
                "spn_gram_approx_f32", "spn_gram_error", "spn_gram_exact_host", "spn_gram_approx_host",
-               "spn_gram_error_host", "spn_hash_f32_peers")
+               "spn_gram_error_host", "spn_hash_f32_peers", "spn_fwht_f32", "spn_fwht_f32_host", "spn_diag_f32",
+               "spn_diag_f32_host")
 
 
 # ----------------------------------------------------------------------- errors
@@ -458,6 +463,72 @@ def signed_argmax(y) -> tuple[int, int]:
     return i, (-1 if y[i] < 0.0 else 1)
 
 
+def _host_rows(x):
+    """fp64 host values -> contiguous fp32 rows (the reference's checks on the fp64 input first)."""
+    xv = np.asarray(x, dtype=np.float64)
+    one = xv.ndim == 1
+    xv = xv.reshape(1, -1) if one else xv
+    if xv.ndim != 2:
+        raise DimensionError("expected a vector or a [batch, n] matrix")
+    return np.ascontiguousarray(xv, dtype=np.float32), one
+
+
+def fwht_normalized(x, out=None, stream=None, device=0):
+    """transforms.hpp:13 / transforms.cpp:52-71: H_n x with the orthonormal Walsh-Hadamard H_n, for a
+    vector or every row of a [batch, n] array.  Host input follows the reference (fp64 values,
+    DimensionError for a non-power-of-two length, DomainError for a non-finite entry) and returns fp64;
+    a CUDA tensor is transformed on the device on `stream` (fp32)."""
+    if _is_cuda(x):
+        torch = _torch()
+        x2, one = _rows2d(x)
+        if x2.dtype != torch.float32 or x2.stride(-1) != 1:
+            x2 = x2.to(torch.float32).contiguous()
+        o = out if out is not None else torch.empty_like(x2)
+        _check(_fwht(x2.shape[1], x2.data_ptr(), x2.shape[0], x2.stride(0), o.data_ptr(), o.stride(0),
+                     x2.device.index or 0, _stream_ptr(stream)))
+        return o[0] if one else o
+    xf, one = _host_rows(x)
+    n = xf.shape[1]
+    if n == 0 or n & (n - 1):
+        raise DimensionError(f"fwht_normalized: length must be a power of two, got {n}")
+    if not np.all(np.isfinite(np.asarray(x, dtype=np.float64))):
+        raise DomainError("fwht_normalized: non-finite entry")
+    o = np.empty_like(xf)
+    _check(_fwht_host(n, xf.ctypes.data, xf.shape[0], n, o.ctypes.data, n, device))
+    o = o.astype(np.float64)
+    return o[0] if one else o
+
+
+def diag_matvec(d, x, out=None, stream=None, device=0):
+    """transforms.hpp:59 / transforms.cpp:228-235: d (.) x for a vector or every row of x.  Host input
+    keeps the reference's length and finiteness checks; CUDA tensors run on the device."""
+    if _is_cuda(x):
+        torch = _torch()
+        x2, one = _rows2d(x)
+        if x2.dtype != torch.float32 or x2.stride(-1) != 1:
+            x2 = x2.to(torch.float32).contiguous()
+        dv = d.to(device=x2.device, dtype=torch.float32).contiguous() if _is_cuda(d) else \
+            torch.from_numpy(np.ascontiguousarray(d, dtype=np.float32)).to(x2.device)
+        if dv.numel() != x2.shape[1]:
+            raise DimensionError("diag_matvec: length mismatch")
+        o = out if out is not None else torch.empty_like(x2)
+        _check(_diag(x2.shape[1], dv.data_ptr(), x2.data_ptr(), x2.shape[0], x2.stride(0), o.data_ptr(),
+                     o.stride(0), _stream_ptr(stream)))
+        return o[0] if one else o
+    dv = np.asarray(d, dtype=np.float64).reshape(-1)
+    xf, one = _host_rows(x)
+    if dv.size != xf.shape[1]:
+        raise DimensionError("diag_matvec: length mismatch")
+    if not np.all(np.isfinite(dv)) or not np.all(np.isfinite(np.asarray(x, dtype=np.float64))):
+        raise DomainError("diag_matvec: non-finite entry")
+    df = np.ascontiguousarray(dv, dtype=np.float32)
+    o = np.empty_like(xf)
+    _check(_diag_host(xf.shape[1], df.ctypes.data, xf.ctypes.data, xf.shape[0], xf.shape[1], o.ctypes.data,
+                      xf.shape[1], device))
+    o = o.astype(np.float64)
+    return o[0] if one else o
+
+
 def decode_id(bucket: int, k: int) -> tuple[int, int]:
     """int32 bucket id -> (index, sign): id = index + (sign < 0 ? k : 0)."""
     return (int(bucket) - k, -1) if bucket >= k else (int(bucket), 1)
@@ -660,6 +731,7 @@ __all__ = [
     "SpinnerVariant", "SpinnerSpec", "StructuredSpinner", "StackedSpinner", "CrossPolytopeHasher",
     "MultiTableHasher", "make_hasher_factory", "signed_argmax", "decode_id", "KernelKind", "FeatureMap",
     "embed", "SketchOperator", "mix_seed", "sample_rows", "realize_block", "check_rows", "DimensionError", "DomainError",
+    "fwht_normalized", "diag_matvec",
     "SpinnerError", "SingularSystemError", "variant_from_string", "version", "LIB_PATH", "ABI_SYMBOLS",
     "LogisticProblem", "SketchConfig", "NewtonTrace", "loss", "gradient", "hessian_sqrt", "sketched_step", "solve",
     "generate_ar1_problem", "variant_to_string", "HashedPair", "CollisionCurve", "FamilyComparison", "collision_curve",

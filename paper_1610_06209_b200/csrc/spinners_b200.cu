@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -798,6 +799,118 @@ spn_status spn_embed_f32_host(const spn_plan* cp, int32_t kind, double sigma, co
                        [&](const float* dx, int64_t rows, int64_t nin, char* dout, cudaStream_t s) {
                          return spn_embed_f32(p, kind, sigma, dx, rows, nin, nin, reinterpret_cast<float*>(dout), w, s);
                        });
+}
+
+// ------------------------------------------------ standalone transforms (transforms.hpp:13,59)
+
+}  // extern "C"
+
+namespace {
+
+// unit-diagonal plans for spn_fwht_f32, one per (device, n), alive for the process
+spn_plan* fwht_plan(int64_t n, int32_t device, spn_status* st) {
+  static std::mutex mu;
+  static std::map<std::pair<int32_t, int64_t>, spn_plan*> plans;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = plans.find({device, n});
+  if (it != plans.end()) return it->second;
+  std::vector<double> ones(static_cast<size_t>(n), 1.0);
+  spn_plan* p = nullptr;
+  *st = spn_plan_create_explicit(&p, n, n, n, 1, ones.data(), ones.data(), ones.data(), 1.0, device);
+  if (*st != SPN_OK) return nullptr;
+  plans[{device, n}] = p;
+  return p;
+}
+
+spn_status fwht_args(int64_t n, const void* x, int64_t batch, int64_t ld_x, const void* y, int64_t ld_y) {
+  if (n < 1 || (n & (n - 1)) != 0)
+    return fail(SPN_EDIM, "fwht_normalized: length must be a power of two, got " + std::to_string(n));
+  if (n > (int64_t(1) << kMaxLogN)) return fail(SPN_EUNSUPPORTED, "n > 2^20 not supported");
+  if (batch < 0 || ld_x < n || ld_y < n) return fail(SPN_EINVAL, "bad batch or leading dimension");
+  if (batch > 0 && (!x || !y)) return fail(SPN_EINVAL, "null pointer");
+  return SPN_OK;
+}
+
+__global__ void diag_rows_kernel(int64_t n, const float* __restrict__ d, const float* x, int64_t batch, int64_t ld_x,
+                                 float* y, int64_t ld_y) {
+  const int64_t total = n * batch;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / n, i = e - b * n;
+    y[b * ld_y + i] = d[i] * x[b * ld_x + i];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+spn_status spn_fwht_f32(int64_t n, const float* x, int64_t batch, int64_t ld_x, float* y, int64_t ld_y,
+                        int32_t device, void* stream) {
+  if (spn_status s = fwht_args(n, x, batch, ld_x, y, ld_y)) return s;
+  if (batch == 0) return SPN_OK;
+  DeviceGuard g(device);
+  if (n == 1) {  // H_1 = [1]
+    if (x != y)
+      SPN_CUDA(cudaMemcpy2DAsync(y, ld_y * 4, x, ld_x * 4, 4, batch, cudaMemcpyDeviceToDevice,
+                                 static_cast<cudaStream_t>(stream)));
+    return SPN_OK;
+  }
+  spn_status st = SPN_OK;
+  spn_plan* p = fwht_plan(n, device, &st);
+  if (!p) return st;
+  return spn_apply_f32(p, x, batch, ld_x, n, y, ld_y, 0, stream);
+}
+
+spn_status spn_fwht_f32_host(int64_t n, const float* x, int64_t batch, int64_t ld_x, float* y, int64_t ld_y,
+                             int32_t device) {
+  if (spn_status s = fwht_args(n, x, batch, ld_x, y, ld_y)) return s;
+  if (batch == 0) return SPN_OK;
+  if (n == 1) {
+    for (int64_t b = 0; b < batch; ++b) y[b * ld_y] = x[b * ld_x];
+    return SPN_OK;
+  }
+  spn_status st = SPN_OK;
+  spn_plan* p = fwht_plan(n, device, &st);
+  if (!p) return st;
+  return spn_apply_f32_host(p, x, batch, ld_x, n, y, ld_y, 0);
+}
+
+spn_status spn_diag_f32(int64_t n, const float* d, const float* x, int64_t batch, int64_t ld_x, float* y,
+                        int64_t ld_y, void* stream) {
+  if (n < 1 || batch < 0 || ld_x < n || ld_y < n) return fail(SPN_EDIM, "diag_matvec: length mismatch");
+  if (batch == 0) return SPN_OK;
+  if (!d || !x || !y) return fail(SPN_EINVAL, "null pointer");
+  int dev = 0;
+  SPN_CUDA(cudaGetDevice(&dev));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n * batch + 255) / 256, int64_t(sms) * 8));
+  diag_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, d, x, batch, ld_x,
+                                                                                                  y, ld_y);
+  SPN_CUDA(cudaGetLastError());
+  return SPN_OK;
+}
+
+spn_status spn_diag_f32_host(int64_t n, const float* d, const float* x, int64_t batch, int64_t ld_x, float* y,
+                             int64_t ld_y, int32_t device) {
+  if (n < 1 || batch < 0 || ld_x < n || ld_y < n) return fail(SPN_EDIM, "diag_matvec: length mismatch");
+  if (batch == 0) return SPN_OK;
+  if (!d || !x || !y) return fail(SPN_EINVAL, "null pointer");
+  DeviceGuard g(device);
+  float *dd = nullptr, *dx = nullptr;
+  const size_t row = static_cast<size_t>(n) * 4;
+  cudaError_t e = cudaMalloc(&dd, row);
+  if (e == cudaSuccess) e = cudaMalloc(&dx, row * static_cast<size_t>(batch));
+  if (e == cudaSuccess) e = cudaMemcpy(dd, d, row, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy2D(dx, row, x, ld_x * 4, row, batch, cudaMemcpyHostToDevice);
+  spn_status st = e == cudaSuccess ? spn_diag_f32(n, dd, dx, batch, n, dx, n, nullptr) : cuda_fail(e, "diag_matvec");
+  if (st == SPN_OK) {
+    e = cudaMemcpy2D(y, ld_y * 4, dx, row, row, batch, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = cuda_fail(e, "diag_matvec");
+  }
+  cudaFree(dd);
+  cudaFree(dx);
+  return st;
 }
 
 }  // extern "C"

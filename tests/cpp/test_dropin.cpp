@@ -59,6 +59,36 @@ static double max_abs_diff(const Vec64& a, const Vec64& b) {
 }
 
 int main() {
+  test_case("fwht_normalized KATs, involution and norm; diag_matvec (test_transforms.cpp:11-42,109-114)", [] {
+    Vec64 h2 = fwht_normalized({1.0, 0.0});
+    CHECK(std::abs(h2[0] - 1.0 / std::sqrt(2.0)) < 1e-6 && std::abs(h2[1] - 1.0 / std::sqrt(2.0)) < 1e-6);
+    Vec64 h4 = fwht_normalized({1.0, 2.0, 3.0, 4.0});  // Sylvester H_4 / 2
+    const Vec64 w4 = {5.0, -1.0, -2.0, 0.0};
+    CHECK(max_abs_diff(h4, w4) < 1e-6);
+    for (std::size_t n : {1u, 2u, 8u, 64u, 1024u, 16384u, 65536u}) {
+      Vec64 x = random_vec(n, 900 + n), want = x;
+      orc_fwht_normalized(want.data(), static_cast<int64_t>(n));
+      Vec64 y = fwht_normalized(x);
+      double nx = 0, ny = 0, err = 0;
+      for (std::size_t i = 0; i < n; ++i) {
+        nx += x[i] * x[i];
+        ny += y[i] * y[i];
+        err += (y[i] - want[i]) * (y[i] - want[i]);
+      }
+      CHECK(std::sqrt(err / nx) < 1e-5);         // against the fp64 restatement
+      CHECK(std::abs(std::sqrt(ny / nx) - 1.0) < 1e-5);  // orthonormal
+      Vec64 back = fwht_normalized(y);            // involution
+      CHECK(max_abs_diff(back, x) < 1e-5 * std::sqrt(nx));
+    }
+    CHECK(throws<DimensionError>([] { fwht_normalized(Vec64(3, 1.0)); }));
+    CHECK(throws<DimensionError>([] { fwht_normalized(Vec64()); }));
+    CHECK(throws<DomainError>([] { fwht_normalized({1.0, NAN}); }));
+    Vec64 dm = diag_matvec({2.0, -1.0, 0.5}, {1.0, 3.0, -4.0});
+    CHECK((dm == Vec64{2.0, -3.0, -2.0}));
+    CHECK(throws<DimensionError>([] { diag_matvec({1.0, 2.0}, {1.0}); }));
+    CHECK(throws<DomainError>([] { diag_matvec({1.0, INFINITY}, {1.0, 2.0}); }));
+  });
+
   test_case("signed_argmax: direct example, ties, sign at zero", [] {
     SignedIndex h = signed_argmax({0.1, -0.9, 0.3});
     CHECK(h.index == 1 && h.sign == -1);

@@ -98,6 +98,18 @@ def test_raw_abi_null_and_bad_arguments(spn):
     assert lib.spn_plan_destroy(None) == spn.SPN_OK
     assert spn._apply(None, None, 0, 0, 1, None, 0, 0, None) == spn.SPN_EINVAL
     assert spn._realize_block(7, 8, 0, None, None, None) == spn.SPN_EINVAL
+    # fwht_normalized / diag_matvec (transforms.cpp:52-71,228-235): shape errors before any device work
+    assert spn._fwht(3, None, 1, 3, None, 3, 0, None) == spn.SPN_EDIM
+    assert spn._fwht(0, None, 1, 0, None, 0, 0, None) == spn.SPN_EDIM
+    assert spn._fwht_host(6, None, 1, 6, None, 6, 0) == spn.SPN_EDIM
+    assert spn._fwht(8, None, 1, 4, None, 8, 0, None) == spn.SPN_EINVAL
+    assert spn._diag_host(4, None, None, 1, 2, None, 4, 0) == spn.SPN_EDIM
+    with pytest.raises(spn.DimensionError):
+        spn.fwht_normalized([1.0, 2.0, 3.0])
+    with pytest.raises(spn.DomainError):
+        spn.fwht_normalized([1.0, float("inf")])
+    with pytest.raises(spn.DimensionError):
+        spn.diag_matvec([1.0], [1.0, 2.0])
 
 
 def test_signed_argmax_host_helper(spn):

@@ -86,3 +86,29 @@ def test_hash_scale_and_negation(spn, torch, n):
     neg = sp.plan.hash(-x).cpu().numpy()[:, 0]
     assert np.array_equal(neg % n, ids % n) and np.all((neg >= n) != (ids >= n))
     assert np.array_equal(sp.plan.hash(x).cpu().numpy()[:, 0], ids)  # determinism
+
+
+@pytest.mark.parametrize("logn", [0, 1, 2, 5, 10, 13, 14, 15, 17, 20])
+def test_fwht_normalized_matches_oracle(spn, oracle, torch, logn):
+    """fwht_normalized (transforms.cpp:52-71) on the device, batch and single-vector host calls."""
+    n = 1 << logn
+    x = oracle.gaussian_rows(logn + 1, 3, n)
+    want = np.stack([oracle.fwht(r.astype(np.float64)) for r in x.astype(np.float32)])
+    got = spn.fwht_normalized(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel(got, want).max() <= RTOL
+    assert rel(spn.fwht_normalized(x[:1].astype(np.float64)), want[:1]).max() <= RTOL
+    if n >= 2:  # involution, in place on the device
+        t = torch.from_numpy(x).cuda()
+        spn.fwht_normalized(t, out=t)
+        spn.fwht_normalized(t, out=t)
+        assert rel(t.cpu().numpy(), x.astype(np.float64)).max() <= RTOL
+
+
+def test_fwht_kats_and_diag(spn, torch):
+    h2 = spn.fwht_normalized(np.array([1.0, 0.0]))
+    assert np.allclose(h2, [1 / math.sqrt(2), 1 / math.sqrt(2)], atol=1e-6)  # test_transforms.cpp:11-15
+    assert np.allclose(spn.fwht_normalized(np.array([1.0, 2.0, 3.0, 4.0])), [5.0, -1.0, -2.0, 0.0], atol=1e-6)
+    assert np.array_equal(spn.diag_matvec([2.0, -1.0, 0.5], [1.0, 3.0, -4.0]), [2.0, -3.0, -2.0])
+    d = torch.tensor([2.0, -1.0, 0.5], device="cuda")
+    x = torch.tensor([[1.0, 3.0, -4.0], [0.0, 1.0, 2.0]], device="cuda")
+    assert torch.equal(spn.diag_matvec(d, x), torch.tensor([[2.0, -3.0, -2.0], [0.0, -1.0, 1.0]], device="cuda"))
