@@ -158,6 +158,21 @@ SPN_API spn_status spn_diag_f32(int64_t n, const float* d, const float* x, int64
 SPN_API spn_status spn_diag_f32_host(int64_t n, const float* d, const float* x, int64_t batch, int64_t ld_x,
                                      float* y, int64_t ld_y, int32_t device);
 
+/* CirculantOperator (transforms.hpp:37-51; transforms.cpp:112-208): kind 0 circulant
+ * (C[i][j] = r[(j-i) mod n]), 1 Toeplitz (T[i][j] = t[i-j]: first_col for i >= j, first_row
+ * for i < j; first_col[0] == first_row[0]), 2 skew-circulant (negacyclic).  Any n >= 1 whose
+ * FFT length (n, 2 next_pow2(n) for Toeplitz, next_pow2(2n) otherwise) is <= 2^13; the spectrum is
+ * built on the host as the reference builds it, the correlation runs on the device in fp64.
+ * apply: y_b = M x_b for every row (x may equal y). */
+typedef struct spn_circulant spn_circulant;
+SPN_API spn_status spn_circulant_create(spn_circulant** out, int32_t kind, int64_t n, const double* first_row,
+                                        const double* first_col, int32_t device);
+SPN_API spn_status spn_circulant_destroy(spn_circulant* op);
+SPN_API spn_status spn_circulant_apply_f32(const spn_circulant* op, const float* x, int64_t batch, int64_t ld_x,
+                                           float* y, int64_t ld_y, void* stream);
+SPN_API spn_status spn_circulant_apply_f32_host(const spn_circulant* op, const float* x, int64_t batch,
+                                                int64_t ld_x, float* y, int64_t ld_y);
+
 /* Builder-defined coordinate sampler P (BASELINE config 4): m distinct indices of
  * [0, N) via a partial Fisher-Yates driven by Rng(mix_seed(seed, 0x5a3b)), sorted. */
 SPN_API spn_status spn_sample_rows(int64_t N, int64_t m, uint64_t seed, int64_t* out);

@@ -84,6 +84,99 @@ inline Vec64 diag_matvec(const Vec64& d, const Vec64& x) {
   return Vec64(yf.begin(), yf.end());
 }
 
+// transforms.hpp:15-56 — circulant-family operators; spectrum on the host (as the reference builds
+// it), the fp64 correlation on the device
+enum class CirculantKind { circulant = 0, toeplitz = 1, skew_circulant = 2 };
+
+struct CirculantSpec {  // transforms.hpp:22-35
+  CirculantKind kind = CirculantKind::circulant;
+  Vec64 first_row;
+  Vec64 first_col;  // toeplitz only; first_col[0] must equal first_row[0]
+
+  static CirculantSpec circulant(Vec64 r) {
+    CirculantSpec s;
+    s.first_row = std::move(r);
+    s.validate();
+    return s;
+  }
+  static CirculantSpec toeplitz(Vec64 col, Vec64 row) {
+    CirculantSpec s;
+    s.kind = CirculantKind::toeplitz;
+    s.first_col = std::move(col);
+    s.first_row = std::move(row);
+    s.validate();
+    return s;
+  }
+  static CirculantSpec skew_circulant(Vec64 r) {
+    CirculantSpec s;
+    s.kind = CirculantKind::skew_circulant;
+    s.first_row = std::move(r);
+    s.validate();
+    return s;
+  }
+  std::size_t dim() const { return first_row.size(); }
+  void validate() const {  // transforms.cpp:98-110
+    if (first_row.empty()) throw DimensionError("CirculantSpec: n must be >= 1");
+    check_finite(first_row, "CirculantSpec.first_row");
+    if (kind == CirculantKind::toeplitz) {
+      if (first_col.size() != first_row.size())
+        throw DimensionError("CirculantSpec: toeplitz first_col/first_row length mismatch");
+      check_finite(first_col, "CirculantSpec.first_col");
+      if (first_col[0] != first_row[0]) throw DomainError("CirculantSpec: toeplitz corner entry mismatch");
+    } else if (!first_col.empty()) {
+      throw DimensionError("CirculantSpec: first_col only valid for toeplitz");
+    }
+  }
+};
+
+class CirculantOperator {  // transforms.hpp:37-51
+ public:
+  explicit CirculantOperator(CirculantSpec spec, int device = 0) : spec_(std::move(spec)) {
+    spec_.validate();
+    spn_circulant* h = nullptr;
+    check(spn_circulant_create(&h, static_cast<int32_t>(spec_.kind), static_cast<int64_t>(spec_.dim()),
+                               spec_.first_row.data(),
+                               spec_.kind == CirculantKind::toeplitz ? spec_.first_col.data() : nullptr, device));
+    op_.reset(h, [](spn_circulant* q) { spn_circulant_destroy(q); });
+  }
+  Vec64 apply(const Vec64& x) const {
+    const std::size_t n = spec_.dim();
+    if (x.size() != n)
+      throw DimensionError("CirculantOperator::apply: expected length " + std::to_string(n) + ", got " +
+                           std::to_string(x.size()));
+    check_finite(x, "CirculantOperator::apply");
+    std::vector<float> xf(x.begin(), x.end()), yf(n);
+    check(spn_circulant_apply_f32_host(op_.get(), xf.data(), 1, static_cast<int64_t>(n), yf.data(),
+                                       static_cast<int64_t>(n)));
+    return Vec64(yf.begin(), yf.end());
+  }
+  // new: device buffers, [batch][ld] rows, stream-ordered
+  void apply_device(const float* x, std::size_t batch, std::size_t ld_x, float* y, std::size_t ld_y,
+                    void* stream = nullptr) const {
+    check(spn_circulant_apply_f32(op_.get(), x, static_cast<int64_t>(batch), static_cast<int64_t>(ld_x), y,
+                                  static_cast<int64_t>(ld_y), stream));
+  }
+  const CirculantSpec& spec() const { return spec_; }
+
+ private:
+  CirculantSpec spec_;
+  std::shared_ptr<spn_circulant> op_;
+};
+
+inline Vec64 circulant_matvec(const CirculantSpec& spec, const Vec64& x) {  // transforms.cpp:210-214
+  if (spec.kind != CirculantKind::circulant) throw DomainError("circulant_matvec: spec is not circulant");
+  return CirculantOperator(spec).apply(x);
+}
+inline Vec64 toeplitz_matvec(const CirculantSpec& spec, const Vec64& x) {  // transforms.cpp:216-220
+  if (spec.kind != CirculantKind::toeplitz) throw DomainError("toeplitz_matvec: spec is not toeplitz");
+  return CirculantOperator(spec).apply(x);
+}
+inline Vec64 skew_circulant_matvec(const CirculantSpec& spec, const Vec64& x) {  // transforms.cpp:222-226
+  if (spec.kind != CirculantKind::skew_circulant)
+    throw DomainError("skew_circulant_matvec: spec is not skew-circulant");
+  return CirculantOperator(spec).apply(x);
+}
+
 enum class SpinnerVariant {  // spinner.hpp:18-25
   hd3_hd2_hd1 = SPN_HD3_HD2_HD1,
   hdg_hd2_hd1 = SPN_HDG_HD2_HD1,

@@ -85,6 +85,10 @@ _fwht = _sig("spn_fwht_f32", C.c_int, [_i64, _vp, _i64, _i64, _vp, _i64, _i32, _
 _fwht_host = _sig("spn_fwht_f32_host", C.c_int, [_i64, _vp, _i64, _i64, _vp, _i64, _i32])
 _diag = _sig("spn_diag_f32", C.c_int, [_i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp])
 _diag_host = _sig("spn_diag_f32_host", C.c_int, [_i64, _vp, _vp, _i64, _i64, _vp, _i64, _i32])
+_circ_create = _sig("spn_circulant_create", C.c_int, [C.POINTER(_vp), _i32, _i64, _vp, _vp, _i32])
+_circ_destroy = _sig("spn_circulant_destroy", C.c_int, [_vp])
+_circ_apply = _sig("spn_circulant_apply_f32", C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp])
+_circ_apply_host = _sig("spn_circulant_apply_f32_host", C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64])
 
 SPN_OK, SPN_EDIM, SPN_EDOMAIN, SPN_ECUDA, SPN_ENOMEM, SPN_EUNSUPPORTED, SPN_EINVAL, SPN_ESINGULAR = range(8)
 ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_create",
@@ -97,7 +101,8 @@ ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_c
                "spn_sketched_step_host", "spn_logistic_line_host", "spn_collision_hits_f32", "spn_gram_exact_f32",
                "spn_gram_approx_f32", "spn_gram_error", "spn_gram_exact_host", "spn_gram_approx_host",
                "spn_gram_error_host", "spn_hash_f32_peers", "spn_fwht_f32", "spn_fwht_f32_host", "spn_diag_f32",
-               "spn_diag_f32_host")
+               "spn_diag_f32_host", "spn_circulant_create", "spn_circulant_destroy", "spn_circulant_apply_f32",
+               "spn_circulant_apply_f32_host")
 
 
 # ----------------------------------------------------------------------- errors
@@ -529,6 +534,126 @@ def diag_matvec(d, x, out=None, stream=None, device=0):
     return o[0] if one else o
 
 
+class CirculantKind(enum.IntEnum):
+    """transforms.hpp:15."""
+    circulant = 0
+    toeplitz = 1
+    skew_circulant = 2
+
+
+class CirculantSpec:
+    """transforms.hpp:22-35: generating data of a circulant-family matrix (validated like
+    CirculantSpec::validate, transforms.cpp:98-110)."""
+
+    def __init__(self, kind, first_row, first_col=None):
+        self.kind = CirculantKind(kind)
+        self.first_row = np.asarray(first_row, dtype=np.float64).reshape(-1)
+        self.first_col = None if first_col is None else np.asarray(first_col, dtype=np.float64).reshape(-1)
+        self.validate()
+
+    @staticmethod
+    def circulant(r):
+        return CirculantSpec(CirculantKind.circulant, r)
+
+    @staticmethod
+    def toeplitz(col, row):
+        return CirculantSpec(CirculantKind.toeplitz, row, col)
+
+    @staticmethod
+    def skew_circulant(r):
+        return CirculantSpec(CirculantKind.skew_circulant, r)
+
+    def dim(self):
+        return self.first_row.size
+
+    def validate(self):
+        if self.first_row.size == 0:
+            raise DimensionError("CirculantSpec: n must be >= 1")
+        if not np.all(np.isfinite(self.first_row)):
+            raise DomainError("CirculantSpec.first_row: non-finite entry")
+        if self.kind == CirculantKind.toeplitz:
+            if self.first_col is None or self.first_col.size != self.first_row.size:
+                raise DimensionError("CirculantSpec: toeplitz first_col/first_row length mismatch")
+            if not np.all(np.isfinite(self.first_col)):
+                raise DomainError("CirculantSpec.first_col: non-finite entry")
+            if self.first_col[0] != self.first_row[0]:
+                raise DomainError("CirculantSpec: toeplitz corner entry mismatch")
+        elif self.first_col is not None and self.first_col.size:
+            raise DimensionError("CirculantSpec: first_col only valid for toeplitz")
+
+
+class CirculantOperator:
+    """transforms.hpp:37-51: the spectrum is computed once (on the host, as the reference does) and
+    apply runs the fp64 correlation on the device.  apply(x): one vector (fp64 in / out, the
+    reference's checks) or a [batch, n] CUDA tensor (fp32, stream-ordered)."""
+
+    def __init__(self, spec: CirculantSpec, device=0):
+        self._h = None
+        spec.validate()
+        self._spec, self.device = spec, device
+        row = np.ascontiguousarray(spec.first_row)
+        col = None if spec.kind != CirculantKind.toeplitz else np.ascontiguousarray(spec.first_col)
+        h = _vp()
+        _check(_circ_create(C.byref(h), int(spec.kind), row.size, row.ctypes.data,
+                            None if col is None else col.ctypes.data, device))
+        self._h = h
+
+    def spec(self):
+        return self._spec
+
+    def apply(self, x, out=None, stream=None):
+        n = self._spec.dim()
+        if _is_cuda(x):
+            torch = _torch()
+            x2, one = _rows2d(x)
+            if x2.shape[1] != n:
+                raise DimensionError(f"CirculantOperator::apply: expected length {n}, got {x2.shape[1]}")
+            if x2.dtype != torch.float32 or x2.stride(-1) != 1:
+                x2 = x2.to(torch.float32).contiguous()
+            o = out if out is not None else torch.empty_like(x2)
+            _check(_circ_apply(self._h, x2.data_ptr(), x2.shape[0], x2.stride(0), o.data_ptr(), o.stride(0),
+                               _stream_ptr(stream)))
+            return o[0] if one else o
+        xv = np.asarray(x, dtype=np.float64)
+        xf, one = _host_rows(xv)
+        if xf.shape[1] != n:
+            raise DimensionError(f"CirculantOperator::apply: expected length {n}, got {xf.shape[1]}")
+        if not np.all(np.isfinite(xv)):
+            raise DomainError("CirculantOperator::apply: non-finite entry")
+        o = np.empty_like(xf)
+        _check(_circ_apply_host(self._h, xf.ctypes.data, xf.shape[0], n, o.ctypes.data, n))
+        o = o.astype(np.float64)
+        return o[0] if one else o
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        destroy = _circ_destroy
+        if h is not None and h.value and destroy is not None:
+            destroy(h)
+            self._h = None
+
+
+def circulant_matvec(spec: CirculantSpec, x):
+    """transforms.cpp:210-214."""
+    if spec.kind != CirculantKind.circulant:
+        raise DomainError("circulant_matvec: spec is not circulant")
+    return CirculantOperator(spec).apply(x)
+
+
+def toeplitz_matvec(spec: CirculantSpec, x):
+    """transforms.cpp:216-220."""
+    if spec.kind != CirculantKind.toeplitz:
+        raise DomainError("toeplitz_matvec: spec is not toeplitz")
+    return CirculantOperator(spec).apply(x)
+
+
+def skew_circulant_matvec(spec: CirculantSpec, x):
+    """transforms.cpp:222-226."""
+    if spec.kind != CirculantKind.skew_circulant:
+        raise DomainError("skew_circulant_matvec: spec is not skew-circulant")
+    return CirculantOperator(spec).apply(x)
+
+
 def decode_id(bucket: int, k: int) -> tuple[int, int]:
     """int32 bucket id -> (index, sign): id = index + (sign < 0 ? k : 0)."""
     return (int(bucket) - k, -1) if bucket >= k else (int(bucket), 1)
@@ -731,7 +856,8 @@ __all__ = [
     "SpinnerVariant", "SpinnerSpec", "StructuredSpinner", "StackedSpinner", "CrossPolytopeHasher",
     "MultiTableHasher", "make_hasher_factory", "signed_argmax", "decode_id", "KernelKind", "FeatureMap",
     "embed", "SketchOperator", "mix_seed", "sample_rows", "realize_block", "check_rows", "DimensionError", "DomainError",
-    "fwht_normalized", "diag_matvec",
+    "fwht_normalized", "diag_matvec", "CirculantKind", "CirculantSpec", "CirculantOperator", "circulant_matvec",
+    "toeplitz_matvec", "skew_circulant_matvec",
     "SpinnerError", "SingularSystemError", "variant_from_string", "version", "LIB_PATH", "ABI_SYMBOLS",
     "LogisticProblem", "SketchConfig", "NewtonTrace", "loss", "gradient", "hessian_sqrt", "sketched_step", "solve",
     "generate_ar1_problem", "variant_to_string", "HashedPair", "CollisionCurve", "FamilyComparison", "collision_curve",

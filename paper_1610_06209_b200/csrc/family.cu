@@ -499,3 +499,239 @@ spn_status family_run(const FamilyPlan* f, int op, const float* x, int64_t batch
 }
 
 }  // namespace spn
+
+// ------------------------------------------------------- standalone circulant operators
+// CirculantOperator / circulant_matvec / toeplitz_matvec / skew_circulant_matvec
+// (transforms.hpp:15-56, transforms.cpp:64-220) on the device: the spectrum is built on the host
+// exactly as the reference does (same FFT length choice, Toeplitz embedding and skew half-root
+// weights, fp64), then one CTA per vector runs the correlation with the family kernel's FFT
+// (complex fp64 in shared memory: FFT length <= 2^13).
+
+namespace spn {
+
+namespace {
+
+struct CircParams {
+  const float* x;
+  int64_t ld_x, batch;
+  float* y;
+  int64_t ld_y;
+  int n, N, kind, direct;  // kind: 0 circulant, 1 toeplitz, 2 skew-circulant
+  const double2* spec;     // [N] conj(FFT(.)), bit-reversed
+  const double2* tw;       // [N/2] e^{-2 pi i t / N}
+  const double2* skw;      // [n] e^{i pi t / n} (skew, direct)
+};
+
+__global__ void __launch_bounds__(kFT) circulant_kernel(const CircParams p) {
+  extern __shared__ double2 c[];  // [N]
+  const int tid = threadIdx.x;
+  const bool skew_direct = p.kind == 2 && p.direct;
+  const bool wrap = (p.kind == 0 || p.kind == 2) && !p.direct;  // periodic / negacyclic extension
+  for (int64_t v = blockIdx.x; v < p.batch; v += gridDim.x) {
+    const float* xr = p.x + v * p.ld_x;
+    // input layouts of CirculantOperator::apply (transforms.cpp:178-199)
+    for (int i = tid; i < p.N; i += kFT) {
+      double val = 0.0;
+      if (i < p.n) {
+        val = (double)xr[i];
+      } else if (wrap && i - p.n < p.n - 1) {
+        val = (p.kind == 2 ? -1.0 : 1.0) * (double)xr[i - p.n];
+      }
+      c[i] = skew_direct ? make_double2(val * p.skw[i].x, val * p.skw[i].y) : make_double2(val, 0.0);
+    }
+    __syncthreads();
+    for (int len = p.N; len >= 2; len >>= 1) {  // forward DIF: natural -> bit-reversed
+      const int half = len >> 1, stride = p.N / len;
+      for (int q = tid; q < p.N / 2; q += kFT) {
+        const int blk = q / half, kk = q - blk * half, i = blk * len + kk;
+        const double2 u = c[i], w = c[i + half];
+        c[i] = make_double2(u.x + w.x, u.y + w.y);
+        c[i + half] = cmul(make_double2(u.x - w.x, u.y - w.y), p.tw[kk * stride]);
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < p.N; i += kFT) c[i] = cmul(c[i], p.spec[i]);
+    __syncthreads();
+    for (int len = 2; len <= p.N; len <<= 1) {  // inverse DIT: bit-reversed -> natural
+      const int half = len >> 1, stride = p.N / len;
+      for (int q = tid; q < p.N / 2; q += kFT) {
+        const int blk = q / half, kk = q - blk * half, i = blk * len + kk;
+        const double2 u = c[i], w = cmulc(c[i + half], p.tw[kk * stride]);
+        c[i] = make_double2(u.x + w.x, u.y + w.y);
+        c[i + half] = make_double2(u.x - w.x, u.y - w.y);
+      }
+      __syncthreads();
+    }
+    const double invN = 1.0 / (double)p.N;
+    float* yr = p.y + v * p.ld_y;
+    for (int i = tid; i < p.n; i += kFT) {
+      const double2 z = c[i];
+      const double yd = skew_direct ? (z.x * p.skw[i].x + z.y * p.skw[i].y) : z.x;  // real(z * conj(w^i))
+      yr[i] = (float)(yd * invN);
+    }
+    __syncthreads();
+  }
+}
+
+int64_t next_pow2(int64_t v) {
+  int64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+struct CirculantPlan {
+  int kind = 0, direct = 0, n = 0, N = 0, logN = 0, device = 0, sms = 148;
+  double2 *spec = nullptr, *tw = nullptr, *skw = nullptr;
+  ~CirculantPlan() {
+    for (void* q : {(void*)spec, (void*)tw, (void*)skw})
+      if (q) cudaFree(q);
+  }
+};
+
+}  // namespace spn
+
+struct spn_circulant {
+  spn::CirculantPlan plan;
+};
+
+extern "C" {
+
+spn_status spn_circulant_create(spn_circulant** out, int32_t kind, int64_t n, const double* first_row,
+                                const double* first_col, int32_t device) {
+  using spn::set_error;
+  if (!out) return set_error(SPN_EINVAL, "null output");
+  *out = nullptr;
+  if (kind < 0 || kind > 2) return set_error(SPN_EDOMAIN, "CirculantSpec: unknown kind");
+  if (n < 1) return set_error(SPN_EDIM, "CirculantSpec: n must be >= 1");
+  if (!first_row) return set_error(SPN_EINVAL, "null first_row");
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(first_row[i])) return set_error(SPN_EDOMAIN, "CirculantSpec.first_row: non-finite entry");
+  if (kind == 1) {  // CirculantSpec::validate (transforms.cpp:98-110)
+    if (!first_col) return set_error(SPN_EDIM, "CirculantSpec: toeplitz first_col/first_row length mismatch");
+    for (int64_t i = 0; i < n; ++i)
+      if (!std::isfinite(first_col[i])) return set_error(SPN_EDOMAIN, "CirculantSpec.first_col: non-finite entry");
+    if (first_col[0] != first_row[0]) return set_error(SPN_EDOMAIN, "CirculantSpec: toeplitz corner entry mismatch");
+  } else if (first_col) {
+    return set_error(SPN_EDIM, "CirculantSpec: first_col only valid for toeplitz");
+  }
+  // CirculantOperator::CirculantOperator (transforms.cpp:112-170)
+  const bool pow2 = (n & (n - 1)) == 0;
+  int direct = 0;
+  int64_t N = 0;
+  if (kind == 1) {
+    direct = 1;
+    N = 2 * spn::next_pow2(n);
+  } else {
+    direct = pow2 ? 1 : 0;
+    N = pow2 ? n : spn::next_pow2(2 * n);
+  }
+  if (N > 8192) return set_error(SPN_EUNSUPPORTED, "circulant operator: FFT length > 2^13 (fp64 FFT in smem)");
+  using cd = std::complex<double>;
+  std::vector<cd> z(static_cast<size_t>(N), cd(0.0, 0.0));
+  std::vector<double2> skw(static_cast<size_t>(n));
+  for (int64_t t = 0; t < n; ++t) {
+    const double ang = M_PI * static_cast<double>(t) / static_cast<double>(n);
+    skw[t] = make_double2(std::cos(ang), std::sin(ang));
+  }
+  if (kind == 1) {
+    for (int64_t k = 0; k < n; ++k) z[k] = cd(first_row[k], 0.0);
+    for (int64_t k = 1; k < n; ++k) z[N - k] = cd(first_col[k], 0.0);
+  } else if (kind == 2 && direct) {
+    for (int64_t k = 0; k < n; ++k) z[k] = first_row[k] * cd(skw[k].x, skw[k].y);
+  } else {
+    for (int64_t k = 0; k < n; ++k) z[k] = cd(first_row[k], 0.0);
+  }
+  spn::fft_fp64(z);
+  int logN = 0;
+  while ((int64_t(1) << logN) < N) ++logN;
+  std::vector<double2> spec(static_cast<size_t>(N));
+  for (int64_t j = 0; j < N; ++j) {
+    const cd s = std::conj(z[spn::bitrev(static_cast<size_t>(j), logN)]);
+    spec[static_cast<size_t>(j)] = make_double2(s.real(), s.imag());
+  }
+  std::vector<double2> tw(static_cast<size_t>(N / 2 > 0 ? N / 2 : 1));
+  for (int64_t t = 0; t < N / 2; ++t) {
+    const double ang = -2.0 * M_PI * static_cast<double>(t) / static_cast<double>(N);
+    tw[t] = make_double2(std::cos(ang), std::sin(ang));
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) return spn::cuda_error(cudaGetLastError(), "cudaSetDevice");
+  auto* op = new spn_circulant();
+  spn::CirculantPlan& p = op->plan;
+  p.kind = kind;
+  p.direct = direct;
+  p.n = static_cast<int>(n);
+  p.N = static_cast<int>(N);
+  p.logN = logN;
+  p.device = device;
+  cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = spn::upload(spec, &p.spec);
+  if (e == cudaSuccess) e = spn::upload(tw, &p.tw);
+  if (e == cudaSuccess) e = spn::upload(skw, &p.skw);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    delete op;
+    return spn::cuda_error(e, "circulant operator upload");
+  }
+  *out = op;
+  return SPN_OK;
+}
+
+spn_status spn_circulant_destroy(spn_circulant* op) {
+  delete op;
+  return SPN_OK;
+}
+
+spn_status spn_circulant_apply_f32(const spn_circulant* op, const float* x, int64_t batch, int64_t ld_x, float* y,
+                                   int64_t ld_y, void* stream) {
+  using spn::set_error;
+  if (!op) return set_error(SPN_EINVAL, "null operator");
+  const spn::CirculantPlan& p = op->plan;
+  if (batch < 0 || ld_x < p.n || ld_y < p.n)
+    return set_error(SPN_EDIM, "CirculantOperator::apply: expected length " + std::to_string(p.n));
+  if (batch == 0) return SPN_OK;
+  if (!x || !y) return set_error(SPN_EINVAL, "null pointer");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(spn::circulant_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 136 * 1024);
+    attr = true;
+  }
+  spn::CircParams cp{x, ld_x, batch, y, ld_y, p.n, p.N, p.kind, p.direct, p.spec, p.tw, p.skw};
+  const int64_t grid = std::min<int64_t>(batch, int64_t(p.sms) * 4);
+  spn::circulant_kernel<<<static_cast<unsigned>(grid), spn::kFT, sizeof(double2) * static_cast<size_t>(p.N),
+                          static_cast<cudaStream_t>(stream)>>>(cp);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SPN_OK : spn::cuda_error(e, "circulant operator");
+}
+
+spn_status spn_circulant_apply_f32_host(const spn_circulant* op, const float* x, int64_t batch, int64_t ld_x,
+                                        float* y, int64_t ld_y) {
+  using spn::set_error;
+  if (!op) return set_error(SPN_EINVAL, "null operator");
+  const spn::CirculantPlan& p = op->plan;
+  if (batch < 0 || ld_x < p.n || ld_y < p.n)
+    return set_error(SPN_EDIM, "CirculantOperator::apply: expected length " + std::to_string(p.n));
+  if (batch == 0) return SPN_OK;
+  if (!x || !y) return set_error(SPN_EINVAL, "null pointer");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p.device);
+  const size_t row = static_cast<size_t>(p.n) * 4;
+  float* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, row * static_cast<size_t>(batch));
+  if (e == cudaSuccess) e = cudaMemcpy2D(d, row, x, ld_x * 4, row, batch, cudaMemcpyHostToDevice);
+  spn_status st = e == cudaSuccess ? spn_circulant_apply_f32(op, d, batch, p.n, d, p.n, nullptr)
+                                   : spn::cuda_error(e, "circulant operator");
+  if (st == SPN_OK) {
+    e = cudaMemcpy2D(y, ld_y * 4, d, row, row, batch, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = spn::cuda_error(e, "circulant operator");
+  }
+  cudaFree(d);
+  cudaSetDevice(prev);
+  return st;
+}
+
+}  // extern "C"

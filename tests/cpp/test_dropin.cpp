@@ -89,6 +89,29 @@ int main() {
     CHECK(throws<DomainError>([] { diag_matvec({1.0, INFINITY}, {1.0, 2.0}); }));
   });
 
+  test_case("circulant / Toeplitz / skew-circulant operators vs explicit matrices (oracles.hpp:35-58)", [] {
+    for (std::size_t n : {1u, 3u, 8u, 100u, 256u}) {
+      Vec64 r = random_vec(n, 70 + n), c = random_vec(n, 90 + n), x = random_vec(n, 110 + n);
+      c[0] = r[0];
+      Vec64 yc(n, 0.0), yt(n, 0.0), ys(n, 0.0);
+      for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < n; ++j) {
+          yc[i] += r[(j + n - i) % n] * x[j];
+          yt[i] += (i >= j ? c[i - j] : r[j - i]) * x[j];
+          ys[i] += (j >= i ? r[j - i] : -r[n + j - i]) * x[j];
+        }
+      double sx = 0;
+      for (double v : x) sx += v * v;
+      const double tol = 1e-5 * std::sqrt(sx) * std::sqrt(static_cast<double>(n));
+      CHECK(max_abs_diff(circulant_matvec(CirculantSpec::circulant(r), x), yc) < tol);
+      CHECK(max_abs_diff(toeplitz_matvec(CirculantSpec::toeplitz(c, r), x), yt) < tol);
+      CHECK(max_abs_diff(skew_circulant_matvec(CirculantSpec::skew_circulant(r), x), ys) < tol);
+    }
+    CHECK(throws<DomainError>([] { CirculantSpec::toeplitz({1.0, 2.0}, {2.0, 2.0}); }));
+    CHECK(throws<DimensionError>([] { CirculantSpec::circulant({}); }));
+    CHECK(throws<DomainError>([] { toeplitz_matvec(CirculantSpec::circulant({1.0, 2.0}), {1.0, 2.0}); }));
+  });
+
   test_case("signed_argmax: direct example, ties, sign at zero", [] {
     SignedIndex h = signed_argmax({0.1, -0.9, 0.3});
     CHECK(h.index == 1 && h.sign == -1);

@@ -110,6 +110,19 @@ def test_raw_abi_null_and_bad_arguments(spn):
         spn.fwht_normalized([1.0, float("inf")])
     with pytest.raises(spn.DimensionError):
         spn.diag_matvec([1.0], [1.0, 2.0])
+    # CirculantSpec::validate (transforms.cpp:98-110) before any device work
+    import ctypes
+    h = spn._vp()
+    row = np.array([1.0, 2.0]); bad = np.array([3.0, 2.0]); nan = np.array([np.nan, 1.0])
+    assert spn._circ_create(ctypes.byref(h), 0, 0, row.ctypes.data, None, 0) == spn.SPN_EDIM
+    assert spn._circ_create(ctypes.byref(h), 1, 2, row.ctypes.data, bad.ctypes.data, 0) == spn.SPN_EDOMAIN
+    assert spn._circ_create(ctypes.byref(h), 0, 2, nan.ctypes.data, None, 0) == spn.SPN_EDOMAIN
+    assert spn._circ_create(ctypes.byref(h), 0, 2, row.ctypes.data, row.ctypes.data, 0) == spn.SPN_EDIM
+    assert spn._circ_create(ctypes.byref(h), 7, 2, row.ctypes.data, None, 0) == spn.SPN_EDOMAIN
+    with pytest.raises(spn.DomainError):
+        spn.CirculantSpec.toeplitz([1.0, 2.0], [2.0, 3.0])
+    with pytest.raises(spn.DimensionError):
+        spn.CirculantSpec(spn.CirculantKind.circulant, [1.0, 2.0], [1.0, 2.0])
 
 
 def test_signed_argmax_host_helper(spn):

@@ -112,3 +112,39 @@ def test_fwht_kats_and_diag(spn, torch):
     d = torch.tensor([2.0, -1.0, 0.5], device="cuda")
     x = torch.tensor([[1.0, 3.0, -4.0], [0.0, 1.0, 2.0]], device="cuda")
     assert torch.equal(spn.diag_matvec(d, x), torch.tensor([[2.0, -3.0, -2.0], [0.0, -1.0, 1.0]], device="cuda"))
+
+
+# -------------------------------------------- circulant-family operators (transforms.cpp:64-226)
+def dense_circulant(kind, row, col=None):
+    """oracles.hpp:35-58: the explicit matrices."""
+    n = row.size
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    if kind == 0:
+        return row[(j - i) % n]
+    if kind == 1:
+        return np.where(i >= j, col[np.abs(i - j)], row[np.abs(j - i)])
+    return np.where(j >= i, row[(j - i) % n], -row[(n + j - i) % n])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 64, 100, 1000, 1024, 4096, 8192])
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_circulant_operator_matches_dense(spn, torch, n, kind):
+    if kind == 1 and n > 4096 or kind != 1 and n & (n - 1) and n > 4096:
+        pytest.skip("FFT length > 2^13")
+    rng = np.random.default_rng(n * 3 + kind)
+    row = rng.standard_normal(n)
+    col = rng.standard_normal(n) if kind == 1 else None
+    if kind == 1:
+        col[0] = row[0]
+    spec = spn.CirculantSpec(kind, row, col)
+    op = spn.CirculantOperator(spec)
+    x = rng.standard_normal((4, n)).astype(np.float32)
+    want = x.astype(np.float64) @ dense_circulant(kind, row, col).T
+    got = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel(got, want).max() <= RTOL, (n, kind)
+    one = op.apply(x[0].astype(np.float64))  # single host vector, fp64 in / out
+    assert rel(one[None], want[:1]).max() <= RTOL
+    fn = [spn.circulant_matvec, spn.toeplitz_matvec, spn.skew_circulant_matvec][kind]
+    assert rel(fn(spec, x[1].astype(np.float64))[None], want[1:2]).max() <= RTOL
+    with pytest.raises(spn.DomainError):
+        [spn.toeplitz_matvec, spn.skew_circulant_matvec, spn.circulant_matvec][kind](spec, x[0])
