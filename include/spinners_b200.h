@@ -91,8 +91,13 @@ SPN_API const char* spn_version(void);
 /* Realise the diagonals with the reference's seeded generator on the host
  * (mix_seed + mt19937_64 + Box-Muller, common.hpp:51-92) and upload them. */
 SPN_API spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* desc);
+/* One m x n block realised from its spec seed directly (StructuredSpinner::build(spec),
+ * spinner.cpp:137-151): any variant, k = m, one table; scale 0 => default_scale. */
+SPN_API spn_status spn_plan_create_block(spn_plan** out, int32_t variant, int64_t n, int64_t m,
+                                         uint64_t spec_seed, double scale, int32_t device);
 /* Same, with caller-provided diagonals [tables][blocks][n] (e.g. a fitted tail
  * vector, StructuredSpinner::with_tail_vector, spinner.hpp:80). */
+
 SPN_API spn_status spn_plan_create_explicit(spn_plan** out, int64_t n, int64_t m, int64_t k,
                                             int64_t tables, const double* d1, const double* d2,
                                             const double* d3, double scale, int32_t device);

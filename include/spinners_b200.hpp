@@ -283,17 +283,33 @@ class StructuredSpinner : public StackedSpinner {
     s.spec_ = spec;
     s.n_ = spec.n;
     s.k_ = spec.m;
+    spn_plan* p = nullptr;  // every variant, drawn from spec.seed itself (spinner.cpp:137-151)
+    check(spn_plan_create_block(&p, static_cast<int32_t>(spec.variant), static_cast<int64_t>(spec.n),
+                                static_cast<int64_t>(spec.m), spec.seed, spec.scale, device));
+    s.plan_ = detail::Plan(p, detail::PlanDeleter{});
     s.d1_.resize(spec.n);
     s.d2_.resize(spec.n);
     s.d3_.resize(spec.n);
-    check(spn_realize_block(static_cast<int32_t>(spec.variant), static_cast<int64_t>(spec.n), spec.seed,
-                            s.d1_.data(), s.d2_.data(), s.d3_.data()));
-    spn_plan* p = nullptr;
-    check(spn_plan_create_explicit(&p, static_cast<int64_t>(spec.n), static_cast<int64_t>(spec.m),
-                                   static_cast<int64_t>(spec.m), 1, s.d1_.data(), s.d2_.data(), s.d3_.data(),
-                                   spec.scale, device));
-    s.plan_ = detail::Plan(p, detail::PlanDeleter{});
+    check(spn_plan_diagonals(p, s.d1_.data(), s.d2_.data(), s.d3_.data()));
     return s;
+  }
+  // M2 M1 x (spinner.cpp:186-198): H D2 H D1 x for the Hadamard-only variants, D2 H D1 x for the
+  // circulant family — on the device (the D2 H D1 chain, plus one normalised FWHT)
+  Vec64 apply_front_blocks(const Vec64& x) const {
+    if (!has_hadamard(spec_.variant)) throw DomainError("apply_front_blocks: dense baseline has no block structure");
+    if (x.size() != spec_.n) throw DimensionError("apply_front_blocks: length mismatch");
+    check_finite(x, "apply_front_blocks");
+    const auto n = static_cast<int64_t>(spec_.n);
+    Vec64 ones(spec_.n, 1.0);
+    spn_plan* p = nullptr;  // H (1) H D2 H D1 = D2 H D1 (H H = I), scale 1
+    check(spn_plan_create_explicit(&p, n, n, n, 1, d1_.data(), d2_.data(), ones.data(), 1.0, 0));
+    detail::Plan front(p, detail::PlanDeleter{});
+    std::vector<float> xf = detail::to_f32(x), y(spec_.n);
+    check(spn_apply_f32_host(front.get(), xf.data(), 1, n, n, y.data(), n, 0));
+    const bool hadamard_only = spec_.variant == SpinnerVariant::hd3_hd2_hd1 ||
+                               spec_.variant == SpinnerVariant::hdg_hd2_hd1 || spec_.variant == SpinnerVariant::gauss3;
+    if (hadamard_only) check(spn_fwht_f32_host(n, y.data(), 1, n, y.data(), n, 0));
+    return Vec64(y.begin(), y.end());
   }
   const SpinnerSpec& spec() const { return spec_; }
   const Vec64& d1() const { return d1_; }

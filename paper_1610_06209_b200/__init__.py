@@ -65,6 +65,7 @@ _status_string = _sig("spn_status_string", C.c_char_p, [C.c_int])
 _last_error = _sig("spn_last_error", C.c_char_p, [])
 _version = _sig("spn_version", C.c_char_p, [])
 _plan_create = _sig("spn_plan_create", C.c_int, [C.POINTER(_vp), C.POINTER(_Desc)])
+_plan_create_block = _sig("spn_plan_create_block", C.c_int, [C.POINTER(_vp), _i32, _i64, _i64, _u64, _dbl, _i32])
 _plan_create_explicit = _sig("spn_plan_create_explicit", C.c_int,
                              [C.POINTER(_vp), _i64, _i64, _i64, _i64, _vp, _vp, _vp, _dbl, _i32])
 _plan_destroy = _sig("spn_plan_destroy", C.c_int, [_vp])
@@ -91,7 +92,7 @@ _circ_apply = _sig("spn_circulant_apply_f32", C.c_int, [_vp, _vp, _i64, _i64, _v
 _circ_apply_host = _sig("spn_circulant_apply_f32_host", C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64])
 
 SPN_OK, SPN_EDIM, SPN_EDOMAIN, SPN_ECUDA, SPN_ENOMEM, SPN_EUNSUPPORTED, SPN_EINVAL, SPN_ESINGULAR = range(8)
-ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_create",
+ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_create", "spn_plan_create_block",
                "spn_plan_create_explicit", "spn_plan_destroy", "spn_plan_query", "spn_plan_diagonals",
                "spn_apply_f32", "spn_hash_f32", "spn_embed_f32", "spn_sketch_f32", "spn_apply_f32_host",
                "spn_hash_f32_host", "spn_embed_f32_host", "spn_sample_rows", "spn_mix_seed",
@@ -439,12 +440,34 @@ class StructuredSpinner(StackedSpinner):
     @classmethod
     def build(cls, spec: SpinnerSpec, device=0):
         spec.validate()
-        d = realize_block(spec.variant, spec.n, spec.seed)
-        p = _Plan.create_explicit(*d, spec.n, spec.m, spec.m, 1, spec.scale, device)
-        obj = cls(None, spec.n, spec.m, spec.m, spec.seed, _plan=p)
+        h = _vp()  # every variant, drawn from spec.seed itself (spinner.cpp:137-151)
+        _check(_plan_create_block(C.byref(h), int(spec.variant), spec.n, spec.m, int(spec.seed) & (2**64 - 1),
+                                  float(spec.scale), device))
+        obj = cls(None, spec.n, spec.m, spec.m, spec.seed, _plan=_Plan(h.value, device))
         obj.variant = spec.variant
         obj.spec = spec
         return obj
+
+    def apply_front_blocks(self, x):
+        """M2 M1 x (spinner.cpp:186-198): H D2 H D1 x for the Hadamard-only variants, D2 H D1 x for the
+        circulant family (on the device: the D2 H D1 chain, plus one normalised FWHT)."""
+        if self.variant == SpinnerVariant.gaussian_dense:
+            raise DomainError("apply_front_blocks: dense baseline has no block structure")
+        d1, d2, _ = (a[0, 0] for a in self._p.diagonals())
+        n = self.spec.n
+        front = StackedSpinner.from_diagonals(d1, d2, np.ones(n), n, n, n, scale=1.0)
+        if _is_cuda(x):
+            y = front.apply(x)
+        else:
+            xv = np.asarray(x, dtype=np.float64)
+            if xv.shape[-1] != n:
+                raise DimensionError("apply_front_blocks: length mismatch")
+            if not np.all(np.isfinite(xv)):
+                raise DomainError("apply_front_blocks: non-finite entry")
+            y = front.apply(xv)
+        if self.variant in (SpinnerVariant.hd3_hd2_hd1, SpinnerVariant.hdg_hd2_hd1, SpinnerVariant.gauss3):
+            y = fwht_normalized(y)
+        return y if _is_cuda(y) else np.asarray(y, dtype=np.float64)
 
 
 _realize_block = _sig("spn_realize_block", C.c_int, [_i32, _i64, _u64, _vp, _vp, _vp])

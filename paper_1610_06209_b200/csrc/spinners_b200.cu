@@ -366,7 +366,28 @@ spn_status spn_realize_block(int32_t variant, int64_t n, uint64_t spec_seed, dou
   return SPN_OK;
 }
 
-spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) {
+}  // extern "C"
+
+namespace {
+// raw_spec_seed: d->seed is the single block's spec seed itself (StructuredSpinner::build,
+// spinner.cpp:137-151) instead of the stacked seed whose block b draws from mix_seed(seed, b)
+spn_status plan_create_impl(spn_plan** out, const spn_plan_desc* d, bool raw_spec_seed);
+}  // namespace
+
+extern "C" {
+
+spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) { return plan_create_impl(out, d, false); }
+
+spn_status spn_plan_create_block(spn_plan** out, int32_t variant, int64_t n, int64_t m, uint64_t spec_seed,
+                                 double scale, int32_t device) {
+  const spn_plan_desc d{variant, n, m, m, 1, nullptr, spec_seed, scale, device};
+  return plan_create_impl(out, &d, true);
+}
+
+}  // extern "C"
+
+namespace {
+spn_status plan_create_impl(spn_plan** out, const spn_plan_desc* d, bool raw_spec_seed) {
   if (!out || !d) return fail(SPN_EINVAL, "null argument");
   *out = nullptr;
   const bool fam = spn::family_variant(d->variant);
@@ -396,7 +417,7 @@ spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) {
   const int64_t per = p->blocks * p->n;
   if (d->variant == SPN_HD3_HD2_HD1 && p->tables == 1 && p->blocks == 1 && ilog2(p->n) > kMaxLogNVec) {
     p->lazy_d = true;
-    p->spec_seed = spn::mix_seed(d->table_seeds ? d->table_seeds[0] : d->seed, 0);
+    p->spec_seed = raw_spec_seed ? d->seed : spn::mix_seed(d->table_seeds ? d->table_seeds[0] : d->seed, 0);
     for (int di = 0; di < 3; ++di) p->dsign[di] = 1;
     if (spn_status s = finish_plan(p)) {
       delete p;
@@ -422,7 +443,7 @@ spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) {
     const int64_t t = tb / p->blocks, b = tb - t * p->blocks;
     const uint64_t seed = d->table_seeds ? d->table_seeds[t] : d->seed;
     const int64_t off = t * per + b * p->n;
-    const uint64_t spec_seed = spn::mix_seed(seed, static_cast<uint64_t>(b));
+    const uint64_t spec_seed = raw_spec_seed ? seed : spn::mix_seed(seed, static_cast<uint64_t>(b));
     if (fam)
       spn::family_realize(d->variant, p->n, p->m, spec_seed, p->d[0].data() + off, p->d[1].data() + off,
                           p->d[2].data() + off, p->trow.empty() ? nullptr : p->trow.data() + off,
@@ -443,6 +464,9 @@ spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) {
   *out = p;
   return SPN_OK;
 }
+}  // namespace
+
+extern "C" {
 
 spn_status spn_plan_create_explicit(spn_plan** out, int64_t n, int64_t m, int64_t k,
                                     int64_t tables, const double* d1, const double* d2,

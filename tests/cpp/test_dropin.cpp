@@ -163,6 +163,27 @@ int main() {
     CHECK(a.d1() == b.d1() && a.d3() == b.d3());
   });
 
+  test_case("build(spec) for every variant equals the stacked plan's block 0; apply_front_blocks", [] {
+    for (SpinnerVariant v : {SpinnerVariant::hd3_hd2_hd1, SpinnerVariant::hdg_hd2_hd1, SpinnerVariant::gcirc_d2_hd1,
+                             SpinnerVariant::gtoeplitz_d2_hd1, SpinnerVariant::gskew_circ_d2_hd1,
+                             SpinnerVariant::gaussian_dense}) {
+      auto sp = StructuredSpinner::build(SpinnerSpec::make(v, 32, 24, mix_seed(99, 0)));
+      StackedSpinner st(v, 32, 24, 24, 99);
+      Vec64 x = random_vec(32, 5);
+      CHECK(sp.apply(x) == st.apply(x));
+      if (v == SpinnerVariant::gaussian_dense) {
+        CHECK(throws<DomainError>([&] { sp.apply_front_blocks(x); }));
+        continue;
+      }
+      Vec64 f(32);
+      for (std::size_t i = 0; i < 32; ++i) f[i] = static_cast<double>(static_cast<float>(sp.d1()[i])) * x[i];
+      orc_fwht_normalized(f.data(), 32);
+      for (std::size_t i = 0; i < 32; ++i) f[i] *= static_cast<double>(static_cast<float>(sp.d2()[i]));
+      if (v == SpinnerVariant::hd3_hd2_hd1 || v == SpinnerVariant::hdg_hd2_hd1) orc_fwht_normalized(f.data(), 32);
+      CHECK(max_abs_diff(sp.apply_front_blocks(x), f) < 1e-5);
+    }
+  });
+
   test_case("HD3HD2HD1 with scale 1 is an isometry at m=n", [] {
     auto spec = SpinnerSpec::make(SpinnerVariant::hd3_hd2_hd1, 64, 64, 3);
     spec.scale = 1.0;

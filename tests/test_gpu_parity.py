@@ -414,3 +414,34 @@ def test_big_embed(spn, oracle, torch, logn, kind):
         assert row_rel(f, want).max() <= RTOL
     else:  # signs: exact except where |z| is at rounding level
         assert np.mean(f == want) > 0.9999
+
+
+@pytest.mark.parametrize("variant", ["hd3_hd2_hd1", "hdg_hd2_hd1", "gcirc_d2_hd1", "gtoeplitz_d2_hd1",
+                                     "gskew_circ_d2_hd1", "gaussian_dense"])
+def test_structured_spinner_build_all_variants(spn, oracle, torch, variant):
+    """StructuredSpinner::build(spec) draws block 0 from spec.seed itself (spinner.cpp:137-151) for
+    every variant: it must equal, bit for bit, the stacked plan whose block 0 spec seed is
+    mix_seed(S, 0) (spinner.cpp:255); apply_front_blocks (spinner.cpp:186-198) against the
+    diagonals composed in fp64."""
+    v = getattr(spn.SpinnerVariant, variant)
+    n, m, S = 64, 48, 1234
+    spec = spn.SpinnerSpec.make(v, n, m, spn.mix_seed(S, 0))
+    sp = spn.StructuredSpinner.build(spec)
+    stacked = spn.StackedSpinner(v, n, m, m, S)
+    x = oracle.gaussian_rows(77, 6, n)
+    a = sp.apply(dev(torch, x)).cpu().numpy()
+    b = stacked.apply(dev(torch, x)).cpu().numpy()
+    assert a.shape == (6, m) and np.array_equal(a, b)
+    if variant == "gaussian_dense":
+        with pytest.raises(spn.DomainError):
+            sp.apply_front_blocks(x[0])
+        return
+    d1, d2, _ = (t[0, 0] for t in sp.plan.diagonals())
+    d1, d2 = (t.astype(np.float32).astype(np.float64) for t in (d1, d2))
+    xd = x.astype(np.float64)
+    front = np.stack([oracle.fwht(r * d1) * d2 for r in xd])
+    if variant in ("hd3_hd2_hd1", "hdg_hd2_hd1"):
+        front = np.stack([oracle.fwht(r) for r in front])
+    got = sp.apply_front_blocks(dev(torch, x)).cpu().numpy()
+    assert row_rel(got, front).max() <= RTOL
+    assert row_rel(sp.apply_front_blocks(xd[0])[None], front[:1]).max() <= RTOL
