@@ -189,6 +189,36 @@ enum class SpinnerVariant {  // spinner.hpp:18-25
 
 inline bool has_hadamard(SpinnerVariant v) { return v != SpinnerVariant::gaussian_dense; }  // spinner.cpp:38
 
+inline const char* to_string(SpinnerVariant v) {  // spinner.cpp:9-19
+  switch (v) {
+    case SpinnerVariant::hd3_hd2_hd1: return "HD3HD2HD1";
+    case SpinnerVariant::hdg_hd2_hd1: return "HDgHD2HD1";
+    case SpinnerVariant::gcirc_d2_hd1: return "GcircD2HD1";
+    case SpinnerVariant::gtoeplitz_d2_hd1: return "GToeplitzD2HD1";
+    case SpinnerVariant::gskew_circ_d2_hd1: return "GSkewCircD2HD1";
+    case SpinnerVariant::gaussian_dense: return "GaussianDense";
+    case SpinnerVariant::gauss3: return "Gauss3";
+  }
+  throw DomainError("to_string: unknown variant");
+}
+
+inline std::vector<SpinnerVariant> all_variants() {  // spinner.cpp:27-31
+  return {SpinnerVariant::hd3_hd2_hd1,       SpinnerVariant::hdg_hd2_hd1,       SpinnerVariant::gcirc_d2_hd1,
+          SpinnerVariant::gtoeplitz_d2_hd1, SpinnerVariant::gskew_circ_d2_hd1, SpinnerVariant::gaussian_dense};
+}
+
+inline std::vector<SpinnerVariant> structured_variants() {  // spinner.cpp:33-37
+  std::vector<SpinnerVariant> v = all_variants();
+  v.pop_back();
+  return v;
+}
+
+inline SpinnerVariant variant_from_string(const std::string& s) {  // spinner.cpp:21-25
+  for (SpinnerVariant v : all_variants())
+    if (s == to_string(v)) return v;
+  throw DomainError("unknown spinner variant: " + s);
+}
+
 inline double default_scale(SpinnerVariant v, std::size_t n) {  // spinner.cpp:40-45
   if (v == SpinnerVariant::hd3_hd2_hd1 || v == SpinnerVariant::hdg_hd2_hd1 || v == SpinnerVariant::gauss3)
     return std::sqrt(static_cast<double>(n));

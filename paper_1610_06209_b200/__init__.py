@@ -185,6 +185,22 @@ def variant_from_string(s: str) -> SpinnerVariant:
         raise DomainError(f"unknown spinner variant: {s}") from None
 
 
+def all_variants():
+    """spinner.cpp:27-31 (the reference's six; the builder-defined gauss3 is not listed)."""
+    return [SpinnerVariant.hd3_hd2_hd1, SpinnerVariant.hdg_hd2_hd1, SpinnerVariant.gcirc_d2_hd1,
+            SpinnerVariant.gtoeplitz_d2_hd1, SpinnerVariant.gskew_circ_d2_hd1, SpinnerVariant.gaussian_dense]
+
+
+def structured_variants():
+    """spinner.cpp:33-37."""
+    return all_variants()[:5]
+
+
+def has_hadamard(v) -> bool:
+    """spinner.cpp:38."""
+    return SpinnerVariant(v) != SpinnerVariant.gaussian_dense
+
+
 # ------------------------------------------------------------------ buffers
 def _torch():
     import torch
@@ -881,7 +897,8 @@ __all__ = [
     "embed", "SketchOperator", "mix_seed", "sample_rows", "realize_block", "check_rows", "DimensionError", "DomainError",
     "fwht_normalized", "diag_matvec", "CirculantKind", "CirculantSpec", "CirculantOperator", "circulant_matvec",
     "toeplitz_matvec", "skew_circulant_matvec",
-    "SpinnerError", "SingularSystemError", "variant_from_string", "version", "LIB_PATH", "ABI_SYMBOLS",
+    "SpinnerError", "SingularSystemError", "variant_from_string", "all_variants", "structured_variants",
+    "has_hadamard", "version", "LIB_PATH", "ABI_SYMBOLS",
     "LogisticProblem", "SketchConfig", "NewtonTrace", "loss", "gradient", "hessian_sqrt", "sketched_step", "solve",
     "generate_ar1_problem", "variant_to_string", "HashedPair", "CollisionCurve", "FamilyComparison", "collision_curve",
     "compare_families", "gram_exact", "gram_approx", "gram_error",
