@@ -445,3 +445,15 @@ def test_structured_spinner_build_all_variants(spn, oracle, torch, variant):
     got = sp.apply_front_blocks(dev(torch, x)).cpu().numpy()
     assert row_rel(got, front).max() <= RTOL
     assert row_rel(sp.apply_front_blocks(xd[0])[None], front[:1]).max() <= RTOL
+
+
+def test_big_hash_stacked_blocks(spn, oracle, torch):
+    """signed argmax over the k rows of a stacked (k > m) plan at n > 2^14, truncated last block."""
+    n = 1 << 15
+    k = n + n // 2 + 7
+    sp = spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, n, n, k, 61)
+    x = oracle.gaussian_rows(8, 4, n, unit=True)
+    ids = sp.plan.hash(dev(torch, x)).cpu().numpy()[:, 0]
+    d = tuple(a[0] for a in sp.plan.diagonals())
+    want, gaps = oracle.hash(*d, n, n, k, 1, math.sqrt(n), x)
+    assert_ids(ids, want[:, 0], gaps[:, 0])
