@@ -67,7 +67,14 @@ __device__ __forceinline__ double warp_sum(double v) {
 // sigmoid(m) and sigmoid(y m) (bit-identical to evaluating both, y = +-1),
 //   loss += log1p_exp(-y m), w = (sigmoid(y m) - 1) y, h = sqrt(s (1 - s)), s = sigmoid(m),
 // then g += w a (lane-parallel over columns).  Per-CTA partials [grid][d+1] (loss last).
-constexpr int kRPI = 8;
+#ifndef SPN_PASS_RPI
+#define SPN_PASS_RPI 8
+#endif
+#ifndef SPN_PASS_MINB  // resident CTAs per SM the pass kernels are compiled for
+#define SPN_PASS_MINB 2  // <= 128 registers: the 2 x SMs grid resident at once (at 177 registers one CTA/SM
+                         // fit, so it ran as two rounds of 8 warps/SM): pass over A 67 -> 51 us at the c6 shape
+#endif
+constexpr int kRPI = SPN_PASS_RPI;
 
 __device__ __forceinline__ double sigmoid_e(double t, double e) {  // e = exp(-|t|)
   return t >= 0.0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
@@ -79,7 +86,7 @@ struct PassCfg {  // rows per warp iteration: 8 KB of loads in flight, <= 64 dat
 };
 
 template <int DCH>
-__global__ void __launch_bounds__(kPassThreads) logistic_pass_kernel(const float* __restrict__ a, int64_t ld,
+__global__ void __launch_bounds__(kPassThreads, SPN_PASS_MINB) logistic_pass_kernel(const float* __restrict__ a, int64_t ld,
                                                                      const float* __restrict__ labels,
                                                                      const double* __restrict__ x, int64_t n, int d,
                                                                      double* __restrict__ part,
@@ -495,7 +502,7 @@ __global__ void ridge_kernel(double* __restrict__ normal, int d) {
 // 8 per warp iteration; lane (q, k) = row q, candidate k when count <= 4 (one transcendental
 // per lane per 8 rows), otherwise lane k (and k + 32) for every row.
 template <int DCH>
-__global__ void __launch_bounds__(kPassThreads) line_kernel(const float* __restrict__ a, int64_t ld,
+__global__ void __launch_bounds__(kPassThreads, SPN_PASS_MINB) line_kernel(const float* __restrict__ a, int64_t ld,
                                                             const float* __restrict__ labels,
                                                             const double* __restrict__ x,
                                                             const double* __restrict__ step, int64_t n, int d,
