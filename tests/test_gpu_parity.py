@@ -457,3 +457,29 @@ def test_big_hash_stacked_blocks(spn, oracle, torch):
     d = tuple(a[0] for a in sp.plan.diagonals())
     want, gaps = oracle.hash(*d, n, n, k, 1, math.sqrt(n), x)
     assert_ids(ids, want[:, 0], gaps[:, 0])
+
+
+def test_concurrent_host_and_stream_calls(spn, oracle, torch):
+    """Plans are immutable and reentrant (spinner.hpp:55): host-buffer calls from several
+    threads on one plan (serialised per plan) and device calls on several streams give the same bits
+    as one call."""
+    import concurrent.futures
+    n, k = 1024, 2048
+    sp = spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, n, n, k, 17)
+    fm = spn.FeatureMap(sp, spn.KernelKind.gaussian(4.0))
+    xs = [oracle.uniform_rows(100 + i, 300, n) for i in range(6)]
+    want = [spn.embed(fm, dev(torch, x)).cpu().numpy() for x in xs]
+    with concurrent.futures.ThreadPoolExecutor(6) as ex:
+        got = list(ex.map(lambda x: spn.embed(fm, x), xs))  # host arrays -> spn_embed_f32_host
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    xd = [dev(torch, x) for x in xs[:3]]
+    torch.cuda.synchronize()
+    outs = []
+    for s, x in zip(streams, xd):
+        with torch.cuda.stream(s):
+            outs.append(spn.embed(fm, x, stream=s))
+    torch.cuda.synchronize()
+    for o, w in zip(outs, want[:3]):
+        assert np.array_equal(o.cpu().numpy(), w)
