@@ -101,6 +101,15 @@ SPN_API spn_status spn_plan_create_block(spn_plan** out, int32_t variant, int64_
 SPN_API spn_status spn_plan_create_explicit(spn_plan** out, int64_t n, int64_t m, int64_t k,
                                             int64_t tables, const double* d1, const double* d2,
                                             const double* d3, double scale, int32_t device);
+/* StructuredSpinner::resample_last_block (mode 0) / resample_tail (mode 1)
+ * (proj/include/spinners/spinner.hpp:67-74; proj/src/spinner.cpp:153-166): a new one-block plan
+ * equal to `src` with the last block's randomness (D3, g, the circulant generator or the dense
+ * matrix; draw_tail, spinner.cpp:92-135) redrawn from Rng(mix_seed(tail_seed, 2)) — or, mode 1,
+ * D2 and then that randomness redrawn from Rng(mix_seed(tail_seed, 3)).  src: one table, one block. */
+SPN_API spn_status spn_plan_resample(spn_plan** out, const spn_plan* src, int32_t mode, uint64_t tail_seed);
+/* StructuredSpinner::with_tail_vector (spinner.hpp:75-77; spinner.cpp:168-184): D3 (HD3) or g (HDg)
+ * replaced by r[n]; Hadamard-only variants; SPN_EDOMAIN for a non-finite entry. */
+SPN_API spn_status spn_plan_with_tail(spn_plan** out, const spn_plan* src, const double* r);
 SPN_API spn_status spn_plan_destroy(spn_plan* plan);
 SPN_API spn_status spn_plan_query(const spn_plan* plan, int64_t* n, int64_t* m, int64_t* k,
                                   int64_t* tables, int64_t* blocks, double* scale);
@@ -130,9 +139,10 @@ SPN_API spn_status spn_embed_f32(const spn_plan* plan, int32_t kind, double sigm
 
 /* Sketch along the long (strided) axis of a row-major A[n_in][d] (ld_a):
  * out[r*ld_out + c] = norm * scale * (H D3 H D2 H D1 a_c)[rows[r]] for r < m_out,
- * a_c = column c zero padded to n.  rows == NULL => rows 0..m_out-1 (the
- * reference's first-m P); rows is a HOST array of distinct indices < n.
- * Requires tables == 1, blocks == 1. */
+ * a_c = column c zero padded to n.  rows == NULL => rows 0..m_out-1 of the stacked
+ * output (the reference's first-m P; m_out <= k, any number of blocks: the multi-block
+ * SketchOperator of newton_sketch.cpp:77-79 when rows > padded); rows is a HOST array of
+ * distinct indices < n (builder-defined P; single-block plans).  Requires tables == 1. */
 SPN_API spn_status spn_sketch_f32(const spn_plan* plan, const float* a, int64_t n_in, int64_t d,
                                   int64_t ld_a, const int64_t* rows, int64_t m_out, double norm,
                                   float* out, int64_t ld_out, void* stream);
@@ -144,6 +154,17 @@ SPN_API spn_status spn_apply_f32_host(const spn_plan* plan, const float* x, int6
                                       int32_t relu);
 SPN_API spn_status spn_hash_f32_host(const spn_plan* plan, const float* x, int64_t batch,
                                      int64_t ld_x, int64_t n_in, int32_t* ids);
+/* hash + projection in one call on host buffers (BASELINE config 1: CrossPolytopeHasher::hash,
+ * lsh.cpp:23-30, and StructuredSpinner::apply, spinner.cpp:200-231, on the same rows):
+ * ids[b] as spn_hash_f32, y[b*ld_y + r] as spn_apply_f32.  Requires tables == 1. */
+SPN_API spn_status spn_hash_project_f32_host(const spn_plan* plan, const float* x, int64_t batch,
+                                             int64_t ld_x, int64_t n_in, int32_t* ids, float* y,
+                                             int64_t ld_y);
+/* SketchOperator::apply with value semantics (newton_sketch.hpp:64; newton_sketch.cpp:87-101):
+ * A and out are HOST buffers (pinned for full PCIe rate); arguments as spn_sketch_f32. */
+SPN_API spn_status spn_sketch_f32_host(const spn_plan* plan, const float* a, int64_t n_in, int64_t d,
+                                       int64_t ld_a, const int64_t* rows, int64_t m_out, double norm,
+                                       float* out, int64_t ld_out);
 SPN_API spn_status spn_embed_f32_host(const spn_plan* plan, int32_t kind, double sigma,
                                       const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
                                       float* out, int64_t ld_out);
@@ -198,10 +219,10 @@ SPN_API spn_status spn_check_rows_f32(const float* x, int64_t batch, int64_t ld_
  * the device pointers in `peers` (a device array of npeers pointers mapped with CUDA IPC
  * over NVLink / NVSwitch; the local table is one of them).  After a barrier on all
  * ranks, every table holds all codes — the NCCL all-gather of config 3 without a
- * separate collective. */
+ * separate collective.  total = rows of every gathered table; row0 + batch <= total. */
 SPN_API spn_status spn_hash_f32_peers(const spn_plan* plan, const float* x, int64_t batch, int64_t ld_x,
                                       int64_t n_in, int32_t* const* peers, int32_t npeers, int64_t row0,
-                                      void* stream);
+                                      int64_t total, void* stream);
 
 /* collision_curve / compare_families (lsh.cpp:38-96; lsh.hpp:38-75), the counting core.
  * plan: `trials` tables of make_hasher_factory(v, n, m) with table seeds mix_seed(seed, t)

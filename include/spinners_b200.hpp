@@ -261,7 +261,7 @@ class StackedSpinner {
  public:
   StackedSpinner(SpinnerVariant v, std::size_t n, std::size_t m, std::size_t k, std::uint64_t seed,
                  double scale = 0.0, int device = 0)
-      : n_(n), k_(k) {
+      : n_(n), k_(k), device_(device) {
     if (k < 1) throw DimensionError("StackedSpinner: k must be >= 1");
     spn_plan_desc d{static_cast<int32_t>(v), static_cast<int64_t>(n), static_cast<int64_t>(m),
                     static_cast<int64_t>(k), 1, nullptr, seed, scale, device};
@@ -272,6 +272,7 @@ class StackedSpinner {
 
   std::size_t rows() const { return k_; }
   std::size_t input_dim() const { return n_; }
+  int device() const { return device_; }
   const spn_plan* plan() const { return plan_.get(); }
 
   // Single vector, like StackedSpinner::apply (spinner.cpp:272-283).
@@ -302,6 +303,7 @@ class StackedSpinner {
   StackedSpinner() = default;
   detail::Plan plan_;
   std::size_t n_ = 0, k_ = 0;
+  int device_ = 0;
 };
 
 // One realised m x n block (spinner.hpp:56-104), diagonals drawn from spec.seed.
@@ -309,36 +311,49 @@ class StructuredSpinner : public StackedSpinner {
  public:
   static StructuredSpinner build(const SpinnerSpec& spec, int device = 0) {
     spec.validate();
-    StructuredSpinner s;
-    s.spec_ = spec;
-    s.n_ = spec.n;
-    s.k_ = spec.m;
     spn_plan* p = nullptr;  // every variant, drawn from spec.seed itself (spinner.cpp:137-151)
     check(spn_plan_create_block(&p, static_cast<int32_t>(spec.variant), static_cast<int64_t>(spec.n),
                                 static_cast<int64_t>(spec.m), spec.seed, spec.scale, device));
-    s.plan_ = detail::Plan(p, detail::PlanDeleter{});
-    s.d1_.resize(spec.n);
-    s.d2_.resize(spec.n);
-    s.d3_.resize(spec.n);
-    check(spn_plan_diagonals(p, s.d1_.data(), s.d2_.data(), s.d3_.data()));
-    return s;
+    return wrap(p, spec, device);
+  }
+  // spinner.hpp:67-69 / spinner.cpp:153-158: M1, M2 kept, the last block redrawn from mix_seed(tail_seed, 2)
+  StructuredSpinner resample_last_block(std::uint64_t tail_seed) const {
+    spn_plan* p = nullptr;
+    check(spn_plan_resample(&p, plan_.get(), 0, tail_seed));
+    return wrap(p, spec_, device_);
+  }
+  // spinner.hpp:71-73 / spinner.cpp:160-166: D2 and the last block redrawn from mix_seed(tail_seed, 3)
+  StructuredSpinner resample_tail(std::uint64_t tail_seed) const {
+    spn_plan* p = nullptr;
+    check(spn_plan_resample(&p, plan_.get(), 1, tail_seed));
+    return wrap(p, spec_, device_);
+  }
+  // spinner.hpp:75-77 / spinner.cpp:168-184: D3 (HD3) or g (HDg) replaced by r
+  StructuredSpinner with_tail_vector(Vec64 r) const {
+    if (r.size() != spec_.n) throw DimensionError("with_tail_vector: length mismatch");
+    check_finite(r, "with_tail_vector");
+    spn_plan* p = nullptr;
+    check(spn_plan_with_tail(&p, plan_.get(), r.data()));
+    return wrap(p, spec_, device_);
   }
   // M2 M1 x (spinner.cpp:186-198): H D2 H D1 x for the Hadamard-only variants, D2 H D1 x for the
-  // circulant family — on the device (the D2 H D1 chain, plus one normalised FWHT)
+  // circulant family — on the spinner's device (the D2 H D1 chain, plus one normalised FWHT)
   Vec64 apply_front_blocks(const Vec64& x) const {
     if (!has_hadamard(spec_.variant)) throw DomainError("apply_front_blocks: dense baseline has no block structure");
     if (x.size() != spec_.n) throw DimensionError("apply_front_blocks: length mismatch");
     check_finite(x, "apply_front_blocks");
     const auto n = static_cast<int64_t>(spec_.n);
-    Vec64 ones(spec_.n, 1.0);
-    spn_plan* p = nullptr;  // H (1) H D2 H D1 = D2 H D1 (H H = I), scale 1
-    check(spn_plan_create_explicit(&p, n, n, n, 1, d1_.data(), d2_.data(), ones.data(), 1.0, 0));
-    detail::Plan front(p, detail::PlanDeleter{});
+    if (!front_) {  // H (1) H D2 H D1 = D2 H D1 (H H = I), scale 1; made once per spinner
+      Vec64 ones(spec_.n, 1.0);
+      spn_plan* p = nullptr;
+      check(spn_plan_create_explicit(&p, n, n, n, 1, d1_.data(), d2_.data(), ones.data(), 1.0, device_));
+      front_ = detail::Plan(p, detail::PlanDeleter{});
+    }
     std::vector<float> xf = detail::to_f32(x), y(spec_.n);
-    check(spn_apply_f32_host(front.get(), xf.data(), 1, n, n, y.data(), n, 0));
+    check(spn_apply_f32_host(front_.get(), xf.data(), 1, n, n, y.data(), n, 0));
     const bool hadamard_only = spec_.variant == SpinnerVariant::hd3_hd2_hd1 ||
                                spec_.variant == SpinnerVariant::hdg_hd2_hd1 || spec_.variant == SpinnerVariant::gauss3;
-    if (hadamard_only) check(spn_fwht_f32_host(n, y.data(), 1, n, y.data(), n, 0));
+    if (hadamard_only) check(spn_fwht_f32_host(n, y.data(), 1, n, y.data(), n, device_));
     return Vec64(y.begin(), y.end());
   }
   const SpinnerSpec& spec() const { return spec_; }
@@ -348,8 +363,22 @@ class StructuredSpinner : public StackedSpinner {
   const Vec64& g_diag() const { return d3_; }  // HDgHD2HD1
 
  private:
+  static StructuredSpinner wrap(spn_plan* p, const SpinnerSpec& spec, int device) {
+    StructuredSpinner s;
+    s.plan_ = detail::Plan(p, detail::PlanDeleter{});
+    s.spec_ = spec;
+    s.n_ = spec.n;
+    s.k_ = spec.m;
+    s.device_ = device;
+    s.d1_.resize(spec.n);
+    s.d2_.resize(spec.n);
+    s.d3_.resize(spec.n);
+    check(spn_plan_diagonals(p, s.d1_.data(), s.d2_.data(), s.d3_.data()));
+    return s;
+  }
   SpinnerSpec spec_;
   Vec64 d1_, d2_, d3_;
+  mutable detail::Plan front_;
 };
 
 struct SignedIndex {  // lsh.hpp:13-17
@@ -399,6 +428,12 @@ class CrossPolytopeHasher {  // lsh.hpp:26-36
   void hash_batch(const float* x, std::size_t batch, std::size_t ld_x, std::size_t n_in, int32_t* ids) const {
     check(spn_hash_f32_host(projector_.plan(), x, static_cast<int64_t>(batch), static_cast<int64_t>(ld_x),
                             static_cast<int64_t>(n_in), ids));
+  }
+  // ids and the projection y = scale * stacked(x) of the same host rows in one call (BASELINE config 1)
+  void hash_project_batch(const float* x, std::size_t batch, std::size_t ld_x, std::size_t n_in, int32_t* ids,
+                          float* y, std::size_t ld_y) const {
+    check(spn_hash_project_f32_host(projector_.plan(), x, static_cast<int64_t>(batch), static_cast<int64_t>(ld_x),
+                                    static_cast<int64_t>(n_in), ids, y, static_cast<int64_t>(ld_y)));
   }
   void hash_device(const float* x, std::size_t batch, std::size_t ld_x, std::size_t n_in, int32_t* ids,
                    void* stream) const {
@@ -552,21 +587,73 @@ inline void embed_batch(const FeatureMap& fm, const float* x, std::size_t batch,
                            static_cast<int64_t>(ld_out)));
 }
 
+// Minimal column-major dense matrix with the slice of Eigen::MatrixXd's interface the reference's
+// SketchOperator uses (rows(), cols(), operator()(i, j), (rows, cols) constructor).  Callers that
+// have Eigen pass Eigen::MatrixXd to SketchOperator::apply unchanged (it is a template).
+class MatrixXd {
+ public:
+  MatrixXd() = default;
+  MatrixXd(std::ptrdiff_t rows, std::ptrdiff_t cols)
+      : r_(rows), c_(cols), v_(static_cast<std::size_t>(rows * cols), 0.0) {}
+  std::ptrdiff_t rows() const { return r_; }
+  std::ptrdiff_t cols() const { return c_; }
+  double& operator()(std::ptrdiff_t i, std::ptrdiff_t j) { return v_[static_cast<std::size_t>(j * r_ + i)]; }
+  double operator()(std::ptrdiff_t i, std::ptrdiff_t j) const { return v_[static_cast<std::size_t>(j * r_ + i)]; }
+  double* data() { return v_.data(); }
+  const double* data() const { return v_.data(); }
+
+ private:
+  std::ptrdiff_t r_ = 0, c_ = 0;
+  std::vector<double> v_;
+};
+
 // Spinner sketch on n-row matrices (newton_sketch.hpp:50-71, newton_sketch.cpp:74-101).
 class SketchOperator {
  public:
   SketchOperator() = default;  // the exact (identity) operator, newton_sketch.hpp:55-56
   bool is_exact() const { return !projector_; }
   const spn_plan* plan() const { return projector_ ? projector_->plan() : nullptr; }
+  // newton_sketch.cpp:74-81: padded = next_pow2(input_dim), StackedSpinner(v, padded, min(rows, padded),
+  // rows, seed) — rows > padded stacks ceil(rows / padded) blocks — and norm 1/sqrt(rows)
   SketchOperator(SpinnerVariant v, std::size_t input_dim, std::size_t rows, std::uint64_t seed, int device = 0)
       : input_dim_(input_dim), rows_(rows) {
     padded_ = 1;
     while (padded_ < input_dim) padded_ <<= 1;
-    if (rows > padded_) throw DeviceError("SketchOperator: rows > padded dimension not supported");
-    projector_ = std::make_unique<StackedSpinner>(v, padded_, std::min(rows, padded_), rows, seed, 0.0, device);
+    projector_ = std::make_shared<StackedSpinner>(v, padded_, std::min(rows, padded_), rows, seed, 0.0, device);
     norm_ = 1.0 / std::sqrt(static_cast<double>(rows));
   }
   std::size_t rows(std::size_t input_dim) const { return is_exact() ? input_dim : rows_; }
+  std::size_t input_dim() const { return input_dim_; }
+
+  // newton_sketch.hpp:64 / newton_sketch.cpp:87-101 with value semantics: any Eigen-like column
+  // matrix (Eigen::MatrixXd or spinners_b200::MatrixXd) of input_dim rows -> rows x cols sketch.
+  template <class Mat>
+  Mat apply(const Mat& columns) const {
+    if (is_exact()) return columns;
+    if (static_cast<std::size_t>(columns.rows()) != input_dim_)
+      throw DimensionError("SketchOperator::apply: row count mismatch");
+    const std::size_t d = static_cast<std::size_t>(columns.cols());
+    std::vector<float> a(input_dim_ * d), o(rows_ * d);
+    for (std::size_t i = 0; i < input_dim_; ++i)
+      for (std::size_t c = 0; c < d; ++c) {
+        const double v = columns(static_cast<std::ptrdiff_t>(i), static_cast<std::ptrdiff_t>(c));
+        if (!std::isfinite(v)) throw DomainError("SketchOperator::apply: non-finite entry");
+        a[i * d + c] = static_cast<float>(v);
+      }
+    if (d > 0) apply_host(a.data(), d, d, o.data(), d);
+    Mat out(static_cast<std::ptrdiff_t>(rows_), static_cast<std::ptrdiff_t>(d));
+    for (std::size_t r = 0; r < rows_; ++r)
+      for (std::size_t c = 0; c < d; ++c)
+        out(static_cast<std::ptrdiff_t>(r), static_cast<std::ptrdiff_t>(c)) = static_cast<double>(o[r * d + c]);
+    return out;
+  }
+  // Row-major host buffers: a [input_dim][ld_a] -> out [rows][ld_out] (spn_sketch_f32_host).
+  void apply_host(const float* a, std::size_t d, std::size_t ld_a, float* out, std::size_t ld_out,
+                  const std::vector<int64_t>* row_list = nullptr) const {
+    check(spn_sketch_f32_host(projector_->plan(), a, static_cast<int64_t>(input_dim_), static_cast<int64_t>(d),
+                              static_cast<int64_t>(ld_a), row_list ? row_list->data() : nullptr,
+                              static_cast<int64_t>(rows_), norm_, out, static_cast<int64_t>(ld_out)));
+  }
   // columns: row-major [input_dim][d] on the DEVICE; out: [rows][d] on the device.
   void apply_device(const float* columns, std::size_t d, float* out, void* stream,
                     const std::vector<int64_t>* row_list = nullptr) const {

@@ -315,6 +315,19 @@ class Reference:
                                         threads))
         return out
 
+    def block_resampled(self, variant, n, m, spec_seed, mode, tail_seed=0, tail=None, x=None):
+        """StructuredSpinner::build(spec) -> resample_last_block (0) / resample_tail (1) /
+        with_tail_vector (2), applied to rows of x; returns (y, d1, d2, d3)."""
+        x = _f32rows(np.zeros((0, n)) if x is None else x)
+        y = np.zeros((x.shape[0], m))
+        d = [np.zeros(n) for _ in range(3)]
+        tv = None if tail is None else np.ascontiguousarray(tail, dtype=np.float64)
+        vp = lambda v: None if v is None else v.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._check(self.lib.ref_block_resampled(cint(variant), i64(n), i64(m), u64(spec_seed), cint(mode),
+                                                 u64(tail_seed), vp(tv), vp(x), i64(x.shape[0]), vp(y), vp(d[0]),
+                                                 vp(d[1]), vp(d[2])))
+        return y, d[0], d[1], d[2]
+
     def gram_exact(self, points, kind, sigma=1.0):
         p = np.ascontiguousarray(points, dtype=np.float32)
         out = np.zeros((p.shape[0], p.shape[0]))

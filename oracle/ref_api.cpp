@@ -223,6 +223,33 @@ int ref_batch_embed(int variant, std::int64_t n, std::int64_t dprime, std::uint6
   }
 }
 
+// StructuredSpinner::build(SpinnerSpec::make(v, n, m, spec_seed)) then (mode 0)
+// resample_last_block(tail_seed), (1) resample_tail(tail_seed) or (2) with_tail_vector(tail)
+// (spinner.cpp:153-184), applied to fp32 rows: y [batch][m].  d1/d2/d3 (optional, [n]) receive the
+// resulting spinner's d1, d2 and d3 (or g_diag).
+int ref_block_resampled(int variant, std::int64_t n, std::int64_t m, std::uint64_t spec_seed, int mode,
+                        std::uint64_t tail_seed, const double* tail, const float* x, std::int64_t batch,
+                        double* y, double* d1, double* d2, double* d3) {
+  try {
+    StructuredSpinner b = StructuredSpinner::build(
+        SpinnerSpec::make(variant_of(variant), static_cast<std::size_t>(n), static_cast<std::size_t>(m), spec_seed));
+    StructuredSpinner r = mode == 0   ? b.resample_last_block(tail_seed)
+                          : mode == 1 ? b.resample_tail(tail_seed)
+                                      : b.with_tail_vector(Vec64(tail, tail + n));
+    for (std::int64_t row = 0; row < batch; ++row) {
+      Vec64 out = r.apply(row_of(x, n, row, n, n));
+      std::copy(out.begin(), out.end(), y + row * m);
+    }
+    if (d1 && !r.d1().empty()) std::copy(r.d1().begin(), r.d1().end(), d1);
+    if (d2 && !r.d2().empty()) std::copy(r.d2().begin(), r.d2().end(), d2);
+    const Vec64& t = r.spec().variant == SpinnerVariant::hdg_hd2_hd1 ? r.g_diag() : r.d3();
+    if (d3 && !t.empty()) std::copy(t.begin(), t.end(), d3);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // SketchOperator(v, input_dim, rows, seed).apply(A) restated over the real
 // StackedSpinner (newton_sketch.cpp:74-101).  A is [input_dim][d] row-major
 // fp32.  If row_list != NULL the builder-defined random-P mode is used instead:

@@ -41,7 +41,7 @@ LIB_PATH = os.environ.get("SPN_LIB") or os.path.join(_HERE, "_lib", "libspinners
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"{LIB_PATH} is missing: build the sm_100a extension first "
-        "(python -m paper_1610_06209_b200.build_ext or __graft_entry__.build())")
+        "(python paper_1610_06209_b200/build_ext.py, or __graft_entry__.build(), from the repo root)")
 
 _lib = C.CDLL(LIB_PATH)
 
@@ -73,12 +73,16 @@ _plan_query = _sig("spn_plan_query", C.c_int, [_vp] + [C.POINTER(_i64)] * 5 + [C
 _plan_diagonals = _sig("spn_plan_diagonals", C.c_int, [_vp, _vp, _vp, _vp])
 _apply = _sig("spn_apply_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i32, _vp])
 _hash = _sig("spn_hash_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp])
-_hash_peers = _sig("spn_hash_f32_peers", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _i64, _vp])
+_hash_peers = _sig("spn_hash_f32_peers", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _i64, _i64, _vp])
 _embed = _sig("spn_embed_f32", C.c_int, [_vp, _i32, _dbl, _vp, _i64, _i64, _i64, _vp, _i64, _vp])
 _sketch = _sig("spn_sketch_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _dbl, _vp, _i64, _vp])
 _apply_host = _sig("spn_apply_f32_host", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i32])
 _hash_host = _sig("spn_hash_f32_host", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp])
 _embed_host = _sig("spn_embed_f32_host", C.c_int, [_vp, _i32, _dbl, _vp, _i64, _i64, _i64, _vp, _i64])
+_hash_project_host = _sig("spn_hash_project_f32_host", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64])
+_sketch_host = _sig("spn_sketch_f32_host", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _dbl, _vp, _i64])
+_plan_resample = _sig("spn_plan_resample", C.c_int, [C.POINTER(_vp), _vp, _i32, _u64])
+_plan_with_tail = _sig("spn_plan_with_tail", C.c_int, [C.POINTER(_vp), _vp, _vp])
 _sample_rows = _sig("spn_sample_rows", C.c_int, [_i64, _i64, _u64, _vp])
 _mix_seed = _sig("spn_mix_seed", _u64, [_u64, _u64])
 _check_rows = _sig("spn_check_rows_f32", C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp])
@@ -103,7 +107,8 @@ ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_c
                "spn_gram_approx_f32", "spn_gram_error", "spn_gram_exact_host", "spn_gram_approx_host",
                "spn_gram_error_host", "spn_hash_f32_peers", "spn_fwht_f32", "spn_fwht_f32_host", "spn_diag_f32",
                "spn_diag_f32_host", "spn_circulant_create", "spn_circulant_destroy", "spn_circulant_apply_f32",
-               "spn_circulant_apply_f32_host")
+               "spn_circulant_apply_f32_host", "spn_hash_project_f32_host", "spn_sketch_f32_host", "spn_plan_resample",
+               "spn_plan_with_tail")
 
 
 # ----------------------------------------------------------------------- errors
@@ -281,6 +286,8 @@ class _Plan:
         torch = _torch()
         if x.dtype != torch.float32:
             raise DomainError("device inputs must be float32")
+        if (x.device.index or 0) != self.device:
+            raise SpinnerError(f"input on cuda:{x.device.index or 0}, plan on cuda:{self.device}")
         x, one = _rows2d(x)
         if x.stride(1) != 1:
             x = x.contiguous()
@@ -296,32 +303,78 @@ class _Plan:
         x, one = _rows2d(x)
         return np.ascontiguousarray(x), one
 
+    def _device_out(self, out, rows, cols, dtype=None, what="out"):
+        """Caller-supplied device output: `dtype`, on the plan's device, >= rows x cols, unit stride
+        along the last dim.  Returns (tensor, leading dimension)."""
+        torch = _torch()
+        dtype = dtype or torch.float32
+        if not _is_cuda(out):
+            raise SpinnerError(f"{what} must be a CUDA tensor for a device input")
+        if out.dtype != dtype:
+            raise DomainError(f"{what} must be {dtype}, got {out.dtype}")
+        if (out.device.index or 0) != self.device:
+            raise SpinnerError(f"{what} on cuda:{out.device.index or 0}, plan on cuda:{self.device}")
+        o2 = out.reshape(1, -1) if out.dim() == 1 else out
+        if o2.dim() != 2 or o2.shape[0] < rows or o2.shape[1] < cols or (o2.shape[1] > 1 and o2.stride(1) != 1):
+            raise DimensionError(f"{what} must be at least [{rows}, {cols}] with unit stride along dim 1, "
+                                 f"got shape {tuple(out.shape)} stride {tuple(out.stride())}")
+        return o2, o2.stride(0)
+
+    @staticmethod
+    def _host_out(out, rows, cols, dtype=np.float32, what="out"):
+        """Caller-supplied host output: a writable numpy array of `dtype`, >= rows x cols, unit
+        stride along the last dim.  Returns (array, leading dimension in elements)."""
+        if not isinstance(out, np.ndarray):
+            raise SpinnerError(f"{what} must be a numpy array for a host input")
+        if out.dtype != dtype:
+            raise DomainError(f"{what} must be {np.dtype(dtype)}, got {out.dtype}")
+        o2 = out.reshape(1, -1) if out.ndim == 1 else out
+        isz = o2.itemsize
+        if (o2.ndim != 2 or o2.shape[0] < rows or o2.shape[1] < cols or not o2.flags.writeable
+                or (o2.shape[1] > 1 and o2.strides[1] != isz) or o2.strides[0] % isz or o2.strides[0] < cols * isz):
+            raise DimensionError(f"{what} must be a writable array of at least [{rows}, {cols}] with packed rows, "
+                                 f"got shape {out.shape} strides {out.strides}")
+        return o2, o2.strides[0] // isz
+
     def apply(self, x, relu=False, out=None, stream=None):
         if _is_cuda(x):
             torch = _torch()
             x, one = self._device_in(x)
             y = out if out is not None else torch.empty((x.shape[0], self.k), device=x.device, dtype=torch.float32)
-            _check(_apply(self._h, x.data_ptr(), x.shape[0], x.stride(0), x.shape[1], y.data_ptr(), y.stride(0),
+            y2, ldy = self._device_out(y, x.shape[0], self.k)
+            _check(_apply(self._h, x.data_ptr(), x.shape[0], x.stride(0), x.shape[1], y2.data_ptr(), ldy,
                           int(relu), _stream_ptr(stream)))
-            return y[0] if one else y
+            return y[0] if one and out is None else y
         x, one = self._host_in(x)
         y = out if out is not None else np.empty((x.shape[0], self.k), dtype=np.float32)
-        _check(_apply_host(self._h, x.ctypes.data, x.shape[0], x.shape[1], x.shape[1], y.ctypes.data, y.shape[1],
+        y2, ldy = self._host_out(y, x.shape[0], self.k)
+        _check(_apply_host(self._h, x.ctypes.data, x.shape[0], x.shape[1], x.shape[1], y2.ctypes.data, ldy,
                            int(relu)))
-        return y[0] if one else y
+        return y[0] if one and out is None else y
 
     def hash(self, x, y_out=None, stream=None):
+        """int32 ids [batch, tables]; with y_out (single-table plans) also the projection."""
+        if y_out is not None and self.tables != 1:
+            raise SpinnerError("y output needs a single-table plan")
         if _is_cuda(x):
             torch = _torch()
             x, one = self._device_in(x)
             ids = torch.empty((x.shape[0], self.tables), device=x.device, dtype=torch.int32)
-            yp, ldy = (y_out.data_ptr(), y_out.stride(0)) if y_out is not None else (None, 0)
+            yp, ldy = None, 0
+            if y_out is not None:
+                y2, ldy = self._device_out(y_out, x.shape[0], self.k, what="y_out")
+                yp = y2.data_ptr()
             _check(_hash(self._h, x.data_ptr(), x.shape[0], x.stride(0), x.shape[1], ids.data_ptr(), yp, ldy,
                          _stream_ptr(stream)))
             return ids[0] if one else ids
         x, one = self._host_in(x)
         ids = np.empty((x.shape[0], self.tables), dtype=np.int32)
-        _check(_hash_host(self._h, x.ctypes.data, x.shape[0], x.shape[1], x.shape[1], ids.ctypes.data))
+        if y_out is not None:
+            y2, ldy = self._host_out(y_out, x.shape[0], self.k, what="y_out")
+            _check(_hash_project_host(self._h, x.ctypes.data, x.shape[0], x.shape[1], x.shape[1], ids.ctypes.data,
+                                      y2.ctypes.data, ldy))
+        else:
+            _check(_hash_host(self._h, x.ctypes.data, x.shape[0], x.shape[1], x.shape[1], ids.ctypes.data))
         return ids[0] if one else ids
 
     def embed(self, kind, sigma, x, out=None, stream=None):
@@ -330,33 +383,48 @@ class _Plan:
             torch = _torch()
             x, one = self._device_in(x)
             o = out if out is not None else torch.empty((x.shape[0], w), device=x.device, dtype=torch.float32)
+            o2, ldo = self._device_out(o, x.shape[0], w)
             _check(_embed(self._h, kind, float(sigma), x.data_ptr(), x.shape[0], x.stride(0), x.shape[1],
-                          o.data_ptr(), o.stride(0), _stream_ptr(stream)))
-            return o[0] if one else o
+                          o2.data_ptr(), ldo, _stream_ptr(stream)))
+            return o[0] if one and out is None else o
         x, one = self._host_in(x)
         o = out if out is not None else np.empty((x.shape[0], w), dtype=np.float32)
+        o2, ldo = self._host_out(o, x.shape[0], w)
         _check(_embed_host(self._h, kind, float(sigma), x.ctypes.data, x.shape[0], x.shape[1], x.shape[1],
-                           o.ctypes.data, o.shape[1]))
-        return o[0] if one else o
+                           o2.ctypes.data, ldo))
+        return o[0] if one and out is None else o
 
     def sketch(self, a, m_out, norm, rows=None, out=None, stream=None):
-        torch = _torch()
-        host = not _is_cuda(a)
-        if host:
-            a = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32))).cuda(self.device)
-        if a.dim() != 2 or a.stride(1) != 1:
-            a = a.reshape(a.shape[0], -1).contiguous()
-        o = out if out is not None else torch.empty((m_out, a.shape[1]), device=a.device, dtype=torch.float32)
+        """Device A (CUDA tensor [n_in, d]) -> device sketch; host A (numpy) -> host sketch through
+        spn_sketch_f32_host (the reference's value semantics)."""
         rl = None
         if rows is not None:
             rows = np.ascontiguousarray(rows, dtype=np.int64)
             if rows.size != m_out:
                 raise DimensionError("rows must have m_out entries")
             rl = rows.ctypes.data
+        if not _is_cuda(a):
+            a = np.asarray(a)
+            if a.ndim != 2:
+                raise DimensionError("expected a [n_in, d] matrix")
+            if a.dtype != np.float32 or a.strides[1] != 4 or a.strides[0] % 4:
+                a = np.ascontiguousarray(a, dtype=np.float32)
+            o = out if out is not None else np.empty((m_out, a.shape[1]), dtype=np.float32)
+            o2, ldo = self._host_out(o, m_out, a.shape[1])
+            _check(_sketch_host(self._h, a.ctypes.data, a.shape[0], a.shape[1], a.strides[0] // 4, rl, m_out,
+                                float(norm), o2.ctypes.data, ldo))
+            return o
+        torch = _torch()
+        if a.dtype != torch.float32:
+            raise DomainError("device inputs must be float32")
+        if (a.device.index or 0) != self.device:
+            raise SpinnerError(f"input on cuda:{a.device.index or 0}, plan on cuda:{self.device}")
+        if a.dim() != 2 or a.stride(1) != 1:
+            a = a.reshape(a.shape[0], -1).contiguous()
+        o = out if out is not None else torch.empty((m_out, a.shape[1]), device=a.device, dtype=torch.float32)
+        o2, ldo = self._device_out(o, m_out, a.shape[1])
         _check(_sketch(self._h, a.data_ptr(), a.shape[0], a.shape[1], a.stride(0), rl, m_out, float(norm),
-                       o.data_ptr(), o.stride(0), _stream_ptr(stream)))
-        if host:
-            return o.cpu().numpy()
+                       o2.data_ptr(), ldo, _stream_ptr(stream)))
         return o
 
 
@@ -459,31 +527,74 @@ class StructuredSpinner(StackedSpinner):
         h = _vp()  # every variant, drawn from spec.seed itself (spinner.cpp:137-151)
         _check(_plan_create_block(C.byref(h), int(spec.variant), spec.n, spec.m, int(spec.seed) & (2**64 - 1),
                                   float(spec.scale), device))
+        return cls._wrap(h, spec, device)
+
+    @classmethod
+    def _wrap(cls, h, spec, device):
         obj = cls(None, spec.n, spec.m, spec.m, spec.seed, _plan=_Plan(h.value, device))
         obj.variant = spec.variant
         obj.spec = spec
+        obj.device = device
+        obj._front = None
         return obj
+
+    def resample_last_block(self, tail_seed):
+        """spinner.hpp:67-69 / spinner.cpp:153-158: same M1, M2; the last block's randomness (D3, g,
+        the circulant generator or the dense matrix) redrawn from Rng(mix_seed(tail_seed, 2))."""
+        h = _vp()
+        _check(_plan_resample(C.byref(h), self._p._h, 0, int(tail_seed) & (2**64 - 1)))
+        return StructuredSpinner._wrap(h, self.spec, self.device)
+
+    def resample_tail(self, tail_seed):
+        """spinner.hpp:71-73 / spinner.cpp:160-166: D2 and the last block redrawn from
+        Rng(mix_seed(tail_seed, 3)); M1 stays fixed."""
+        h = _vp()
+        _check(_plan_resample(C.byref(h), self._p._h, 1, int(tail_seed) & (2**64 - 1)))
+        return StructuredSpinner._wrap(h, self.spec, self.device)
+
+    def with_tail_vector(self, r):
+        """spinner.hpp:75-77 / spinner.cpp:168-184: D3 (HD3) or g (HDg) replaced by r."""
+        rv = np.ascontiguousarray(np.asarray(r, dtype=np.float64).reshape(-1))
+        if rv.size != self.spec.n:
+            raise DimensionError("with_tail_vector: length mismatch")
+        h = _vp()
+        _check(_plan_with_tail(C.byref(h), self._p._h, rv.ctypes.data))
+        return StructuredSpinner._wrap(h, self.spec, self.device)
+
+    def d1(self):
+        return self.diagonals()[0]
+
+    def d2(self):
+        return self.diagonals()[1]
+
+    def d3(self):
+        return self.diagonals()[2]
+
+    g_diag = d3
 
     def apply_front_blocks(self, x):
         """M2 M1 x (spinner.cpp:186-198): H D2 H D1 x for the Hadamard-only variants, D2 H D1 x for the
-        circulant family (on the device: the D2 H D1 chain, plus one normalised FWHT)."""
+        circulant family (on the device: the D2 H D1 chain, plus one normalised FWHT), on the device
+        the spinner was built on."""
         if self.variant == SpinnerVariant.gaussian_dense:
             raise DomainError("apply_front_blocks: dense baseline has no block structure")
-        d1, d2, _ = (a[0, 0] for a in self._p.diagonals())
         n = self.spec.n
-        front = StackedSpinner.from_diagonals(d1, d2, np.ones(n), n, n, n, scale=1.0)
+        if self._front is None:  # D2 H D1 as a plan with D3 = 1 and scale 1 (H 1 H D2 H D1 = D2 H D1)
+            d1, d2, _ = (a[0, 0] for a in self._p.diagonals())
+            self._front = StackedSpinner.from_diagonals(d1, d2, np.ones(n), n, n, n, scale=1.0, device=self.device)
+        hadamard_only = self.variant in (SpinnerVariant.hd3_hd2_hd1, SpinnerVariant.hdg_hd2_hd1, SpinnerVariant.gauss3)
         if _is_cuda(x):
-            y = front.apply(x)
-        else:
-            xv = np.asarray(x, dtype=np.float64)
-            if xv.shape[-1] != n:
-                raise DimensionError("apply_front_blocks: length mismatch")
-            if not np.all(np.isfinite(xv)):
-                raise DomainError("apply_front_blocks: non-finite entry")
-            y = front.apply(xv)
-        if self.variant in (SpinnerVariant.hd3_hd2_hd1, SpinnerVariant.hdg_hd2_hd1, SpinnerVariant.gauss3):
-            y = fwht_normalized(y)
-        return y if _is_cuda(y) else np.asarray(y, dtype=np.float64)
+            y = self._front.apply(x)
+            return fwht_normalized(y, device=self.device) if hadamard_only else y
+        xv = np.asarray(x, dtype=np.float64)
+        if xv.shape[-1] != n:
+            raise DimensionError("apply_front_blocks: length mismatch")
+        if not np.all(np.isfinite(xv)):
+            raise DomainError("apply_front_blocks: non-finite entry")
+        y = self._front.apply(xv)
+        if hadamard_only:
+            y = fwht_normalized(y, device=self.device)
+        return np.asarray(y, dtype=np.float64)
 
 
 _realize_block = _sig("spn_realize_block", C.c_int, [_i32, _i64, _u64, _vp, _vp, _vp])
@@ -861,8 +972,9 @@ class SketchOperator:
             self.norm, self.row_list = 1.0, None
             return
         padded = 1 << max(0, (input_dim - 1).bit_length())
-        if rows > padded:
-            raise SpinnerError("SketchOperator: rows > padded dimension (multi-block sketch) not supported")
+        if mode == "random" and rows > padded:
+            raise DimensionError("SketchOperator: a sampled P needs rows <= padded dimension")
+        # rows > padded: ceil(rows / padded) stacked blocks (newton_sketch.cpp:77-79)
         self.input_dim, self.padded, self.m = input_dim, padded, rows
         self.norm = 1.0 / math.sqrt(rows)
         self._p = _Plan.create(variant, padded, min(rows, padded), rows, seed=seed, device=device)
@@ -883,7 +995,9 @@ class SketchOperator:
         return input_dim if self.is_exact() else self.m
 
     def apply(self, columns, out=None, stream=None):
-        """columns: [input_dim, d] (row-major; the sketch runs along axis 0)."""
+        """columns: [input_dim, d] (row-major; the sketch runs along axis 0).  A CUDA tensor is
+        sketched on the device (stream-ordered); a host array goes through spn_sketch_f32_host
+        and the result comes back as a host array (newton_sketch.cpp:87-101)."""
         if self.is_exact():
             return columns
         if columns.shape[0] != self.input_dim:

@@ -2,8 +2,9 @@
 
 Each translation unit is compiled by its own nvcc process (in parallel), then
 linked into one shared library that exports only the C ABI of
-include/spinners_b200.h.  `python -m paper_1610_06209_b200.build_ext` rebuilds
-when any source is newer than the library.
+include/spinners_b200.h.  `python paper_1610_06209_b200/build_ext.py` (or
+`__graft_entry__.build()`) rebuilds when any source is newer than the library;
+`--force` recompiles every translation unit.
 """
 from __future__ import annotations
 
@@ -42,10 +43,10 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def _compile(src: str, objdir: str = OBJDIR, extra: tuple = ()) -> str:
+def _compile(src: str, objdir: str = OBJDIR, extra: tuple = (), force: bool = False) -> str:
     obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
     hdr_t = max(os.path.getmtime(d) for d in _deps() if not d.endswith(".cu"))
-    if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t):
+    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t):
         return obj
     cmd = [NVCC] + FLAGS + list(extra) + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -67,7 +68,7 @@ def build(force: bool = False, verbose: bool = True, variant: str = "", defines:
     srcs = _sources()
     extra = tuple("-D" + d for d in defines)
     with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda f: _compile(f, objdir, extra), srcs))
+        objs = list(ex.map(lambda f: _compile(f, objdir, extra, force), srcs))
     cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

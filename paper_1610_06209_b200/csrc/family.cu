@@ -599,7 +599,7 @@ struct spn_circulant {
 extern "C" {
 
 spn_status spn_circulant_create(spn_circulant** out, int32_t kind, int64_t n, const double* first_row,
-                                const double* first_col, int32_t device) {
+                                const double* first_col, int32_t device) { SPN_TRY
   using spn::set_error;
   if (!out) return set_error(SPN_EINVAL, "null output");
   *out = nullptr;
@@ -678,15 +678,17 @@ spn_status spn_circulant_create(spn_circulant** out, int32_t kind, int64_t n, co
   }
   *out = op;
   return SPN_OK;
+  SPN_CATCH
 }
 
-spn_status spn_circulant_destroy(spn_circulant* op) {
+spn_status spn_circulant_destroy(spn_circulant* op) { SPN_TRY
   delete op;
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_circulant_apply_f32(const spn_circulant* op, const float* x, int64_t batch, int64_t ld_x, float* y,
-                                   int64_t ld_y, void* stream) {
+                                   int64_t ld_y, void* stream) { SPN_TRY
   using spn::set_error;
   if (!op) return set_error(SPN_EINVAL, "null operator");
   const spn::CirculantPlan& p = op->plan;
@@ -705,10 +707,11 @@ spn_status spn_circulant_apply_f32(const spn_circulant* op, const float* x, int6
                           static_cast<cudaStream_t>(stream)>>>(cp);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SPN_OK : spn::cuda_error(e, "circulant operator");
+  SPN_CATCH
 }
 
 spn_status spn_circulant_apply_f32_host(const spn_circulant* op, const float* x, int64_t batch, int64_t ld_x,
-                                        float* y, int64_t ld_y) {
+                                        float* y, int64_t ld_y) { SPN_TRY
   using spn::set_error;
   if (!op) return set_error(SPN_EINVAL, "null operator");
   const spn::CirculantPlan& p = op->plan;
@@ -732,6 +735,7 @@ spn_status spn_circulant_apply_f32_host(const spn_circulant* op, const float* x,
   cudaFree(d);
   cudaSetDevice(prev);
   return st;
+  SPN_CATCH
 }
 
 }  // extern "C"

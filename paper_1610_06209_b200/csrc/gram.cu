@@ -178,7 +178,7 @@ int sms_of_current() {
 extern "C" {
 
 spn_status spn_gram_approx_f32(const float* features, int64_t count, int64_t width, int64_t ld, int32_t kind,
-                               int64_t dprime, double* gram, int64_t ld_gram, void* stream) {
+                               int64_t dprime, double* gram, int64_t ld_gram, void* stream) { SPN_TRY
   if (count < 1) return fail(SPN_EDIM, "gram_approx: empty dataset");
   if (!features || !gram) return fail(SPN_EINVAL, "null pointer");
   if (ld < width || ld_gram < count || width < 1) return fail(SPN_EINVAL, "bad leading dimension");
@@ -191,10 +191,11 @@ spn_status spn_gram_approx_f32(const float* features, int64_t count, int64_t wid
       features, ld, count, width, kind, 1.0 / (2.0 * static_cast<double>(dprime)), gram, ld_gram);
   GRAM_CUDA(cudaGetLastError());
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_gram_exact_f32(const float* points, int64_t count, int64_t dim, int64_t ld, int32_t kind, double sigma,
-                              double* gram, int64_t ld_gram, void* stream) {
+                              double* gram, int64_t ld_gram, void* stream) { SPN_TRY
   if (count < 1) return fail(SPN_EDIM, "gram_exact: empty dataset");
   if (!points || !gram) return fail(SPN_EINVAL, "null pointer");
   if (ld < dim || ld_gram < count || dim < 1) return fail(SPN_EINVAL, "bad leading dimension");
@@ -215,10 +216,11 @@ spn_status spn_gram_exact_f32(const float* points, int64_t count, int64_t dim, i
   if (norms) cudaFreeAsync(norms, s);
   if (e != cudaSuccess) return spn::cuda_error(e, "gram_exact");
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_gram_error(const double* exact, const double* approx, int64_t count, int64_t ld, double* err,
-                          void* stream) {
+                          void* stream) { SPN_TRY
   if (!exact || !approx || !err) return fail(SPN_EINVAL, "null pointer");
   if (count < 1 || ld < count) return fail(SPN_EDIM, "gram_error: shape mismatch");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -236,6 +238,7 @@ spn_status spn_gram_error(const double* exact, const double* approx, int64_t cou
   if (h[1] == 0.0) return fail(SPN_EDOMAIN, "gram_error: exact Gram matrix is zero");
   *err = std::sqrt(h[0]) / std::sqrt(h[1]);  // (exact - approx).norm() / exact.norm()
   return SPN_OK;
+  SPN_CATCH
 }
 
 // ------------------------------------------------------------- host-buffer forms
@@ -249,7 +252,7 @@ struct DevBuf {
 }  // namespace
 
 spn_status spn_gram_exact_host(const float* points, int64_t count, int64_t dim, int32_t kind, double sigma,
-                               double* gram) {
+                               double* gram) { SPN_TRY
   if (!points || !gram) return fail(SPN_EINVAL, "null pointer");
   if (count < 1) return fail(SPN_EDIM, "gram_exact: empty dataset");
   DevBuf dp, dg;
@@ -261,10 +264,11 @@ spn_status spn_gram_exact_host(const float* points, int64_t count, int64_t dim, 
     return st;
   GRAM_CUDA(cudaMemcpy(gram, dg.p, sizeof(double) * static_cast<size_t>(count * count), cudaMemcpyDeviceToHost));
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_gram_approx_host(const spn_plan* plan, int32_t kind, double sigma, const float* points, int64_t count,
-                                int64_t dim, double* gram) {
+                                int64_t dim, double* gram) { SPN_TRY
   if (!plan || !points || !gram) return fail(SPN_EINVAL, "null pointer");
   if (count < 1) return fail(SPN_EDIM, "gram_approx: empty dataset");
   int64_t n = 0, m = 0, k = 0, tables = 0, blocks = 0;
@@ -284,9 +288,10 @@ spn_status spn_gram_approx_host(const spn_plan* plan, int32_t kind, double sigma
     return st;
   GRAM_CUDA(cudaMemcpy(gram, dg.p, sizeof(double) * static_cast<size_t>(count * count), cudaMemcpyDeviceToHost));
   return SPN_OK;
+  SPN_CATCH
 }
 
-spn_status spn_gram_error_host(const double* exact, const double* approx, int64_t count, double* err) {
+spn_status spn_gram_error_host(const double* exact, const double* approx, int64_t count, double* err) { SPN_TRY
   if (!exact || !approx || !err) return fail(SPN_EINVAL, "null pointer");
   if (count < 1) return fail(SPN_EDIM, "gram_error: shape mismatch");
   DevBuf da, db;
@@ -296,6 +301,7 @@ spn_status spn_gram_error_host(const double* exact, const double* approx, int64_
   GRAM_CUDA(cudaMemcpy(da.p, exact, bytes, cudaMemcpyHostToDevice));
   GRAM_CUDA(cudaMemcpy(db.p, approx, bytes, cudaMemcpyHostToDevice));
   return spn_gram_error(static_cast<double*>(da.p), static_cast<double*>(db.p), count, count, err, nullptr);
+  SPN_CATCH
 }
 
 }  // extern "C"

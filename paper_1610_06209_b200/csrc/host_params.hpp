@@ -129,6 +129,29 @@ inline void realize_block(int variant, int64_t n, uint64_t spec_seed, double* d1
   }
 }
 
+// StructuredSpinner::draw_tail (spinner.cpp:92-135) from a given stream: the last block's
+// randomness of every variant — D3 (HD3, Rademacher), g (HDg, Gaussian), the circulant /
+// skew-circulant generator row, the Toeplitz first column then first row (row[0] = col[0]), or
+// the whole m x n dense matrix.  Variant codes are spn_variant's; V_GAUSS3 draws a Gaussian D3.
+inline void draw_tail(int variant, int64_t n, int64_t m, HostRng& rng, double* tail, double* trow, double* dense) {
+  switch (variant) {
+    case 0:  // SPN_HD3_HD2_HD1
+      for (int64_t i = 0; i < n; ++i) tail[i] = rng.rademacher();
+      break;
+    case 3:  // SPN_GTOEPLITZ_D2_HD1
+      for (int64_t i = 0; i < n; ++i) tail[i] = rng.gaussian();
+      trow[0] = tail[0];
+      for (int64_t i = 1; i < n; ++i) trow[i] = rng.gaussian();
+      break;
+    case 5:  // SPN_GAUSSIAN_DENSE
+      for (int64_t i = 0; i < m * n; ++i) dense[i] = rng.gaussian();
+      break;
+    default:  // HDg, Gaussian circulant / skew-circulant rows, builder-defined Gauss3
+      for (int64_t i = 0; i < n; ++i) tail[i] = rng.gaussian();
+      break;
+  }
+}
+
 // Run f(i) for i in [0, count) on up to hardware_concurrency threads (independent blocks /
 // tables of a plan: every block has its own seeded generators).
 template <class F>

@@ -728,7 +728,7 @@ spn_status factor_solve(spn_newton* w, const double* grad, double* step, cudaStr
 
 extern "C" {
 
-spn_status spn_newton_create(spn_newton** out, int64_t n, int64_t d, int64_t max_sketch_rows, int device) {
+spn_status spn_newton_create(spn_newton** out, int64_t n, int64_t d, int64_t max_sketch_rows, int device) { SPN_TRY
   if (!out) return fail(SPN_EINVAL, "null output");
   *out = nullptr;
   if (n < 1 || d < 1) return fail(SPN_EDIM, "LogisticProblem: empty data");
@@ -768,18 +768,20 @@ spn_status spn_newton_create(spn_newton** out, int64_t n, int64_t d, int64_t max
   }
   *out = w;
   return SPN_OK;
+  SPN_CATCH
 }
 
-spn_status spn_newton_destroy(spn_newton* w) {
+spn_status spn_newton_destroy(spn_newton* w) { SPN_TRY
   if (!w) return SPN_OK;
   DevGuard g(w->device);
   newton_free(w);
   delete w;
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_logistic_eval_f32(spn_newton* w, const float* a, int64_t ld_a, const float* labels,
-                                 const double* x, double* loss, double* grad, void* stream) {
+                                 const double* x, double* loss, double* grad, void* stream) { SPN_TRY
   if (!w || !a || !labels || !x) return fail(SPN_EINVAL, "null pointer");
   if (ld_a < w->d) return fail(SPN_EINVAL, "bad leading dimension");
   DevGuard g(w->device);
@@ -789,10 +791,11 @@ spn_status spn_logistic_eval_f32(spn_newton* w, const float* a, int64_t ld_a, co
   reduce_parts_kernel<<<width, 256, 0, s>>>(w->part, w->grid, width, grad, loss, (int)w->d);
   NWT_CUDA(cudaGetLastError());
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_hessian_sqrt_f32(spn_newton* w, const float* a, int64_t ld_a, const double* x, float* out,
-                                int64_t ld_out, void* stream) {
+                                int64_t ld_out, void* stream) { SPN_TRY
   if (!w || !a || !x || !out) return fail(SPN_EINVAL, "null pointer");
   if (ld_a < w->d || ld_out < w->d) return fail(SPN_EINVAL, "bad leading dimension");
   DevGuard g(w->device);
@@ -803,11 +806,12 @@ spn_status spn_hessian_sqrt_f32(spn_newton* w, const float* a, int64_t ld_a, con
   scale_rows_f32_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, ld_a, w->h64, w->n, (int)w->d, out, ld_out);
   NWT_CUDA(cudaGetLastError());
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_sketched_step_f32(spn_newton* w, const spn_plan* sketch, int64_t rows, const float* a, int64_t ld_a,
                                  const float* labels, const double* x, double* step, double* grad, double* loss,
-                                 void* stream) {
+                                 void* stream) { SPN_TRY
   if (!w || !a || !labels || !x || !step) return fail(SPN_EINVAL, "null pointer");
   if (ld_a < w->d) return fail(SPN_EINVAL, "bad leading dimension");
   const int64_t m = sketch ? rows : w->n;
@@ -842,10 +846,11 @@ spn_status spn_sketched_step_f32(spn_newton* w, const spn_plan* sketch, int64_t 
     if (failed) return fail(SPN_ESINGULAR, "sketched_step: sketched Hessian is indefinite; sketch dimension too small");
   }
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_logistic_line_f32(spn_newton* w, const float* a, int64_t ld_a, const float* labels, const double* x,
-                                 const double* step, double s0, int64_t count, double* losses, void* stream) {
+                                 const double* step, double s0, int64_t count, double* losses, void* stream) { SPN_TRY
   if (!w || !a || !labels || !x || !step || !losses) return fail(SPN_EINVAL, "null pointer");
   if (count < 1 || count > 64) return fail(SPN_EINVAL, "line search: 1 <= count <= 64");
   if (ld_a < w->d) return fail(SPN_EINVAL, "bad leading dimension");
@@ -855,10 +860,11 @@ spn_status spn_logistic_line_f32(spn_newton* w, const float* a, int64_t ld_a, co
   reduce_parts_kernel<<<(unsigned)count, 256, 0, s>>>(w->part, w->grid, (int)count, losses, nullptr, (int)count);
   NWT_CUDA(cudaGetLastError());
   return SPN_OK;
+  SPN_CATCH
 }
 
 // ------------------------------------------------------------- host-buffer forms
-spn_status spn_newton_set_problem(spn_newton* w, const float* features, int64_t ld, const float* labels) {
+spn_status spn_newton_set_problem(spn_newton* w, const float* features, int64_t ld, const float* labels) { SPN_TRY
   if (!w || !features || !labels) return fail(SPN_EINVAL, "null pointer");
   if (ld < w->d) return fail(SPN_EINVAL, "bad leading dimension");
   DevGuard g(w->device);
@@ -870,6 +876,7 @@ spn_status spn_newton_set_problem(spn_newton* w, const float* features, int64_t 
                         sizeof(float) * (size_t)w->d, (size_t)w->n, cudaMemcpyHostToDevice));
   NWT_CUDA(cudaMemcpy(w->labels, labels, sizeof(float) * (size_t)w->n, cudaMemcpyHostToDevice));
   return SPN_OK;
+  SPN_CATCH
 }
 
 namespace {
@@ -880,7 +887,7 @@ spn_status need_problem(const spn_newton* w) {
 }
 }  // namespace
 
-spn_status spn_logistic_eval_host(spn_newton* w, const double* x, double* loss, double* grad) {
+spn_status spn_logistic_eval_host(spn_newton* w, const double* x, double* loss, double* grad) { SPN_TRY
   if (spn_status st = need_problem(w)) return st;
   if (!x) return fail(SPN_EINVAL, "null pointer");
   DevGuard g(w->device);
@@ -894,9 +901,10 @@ spn_status spn_logistic_eval_host(spn_newton* w, const double* x, double* loss, 
   if (loss) NWT_CUDA(cudaMemcpyAsync(loss, df, sizeof(double), cudaMemcpyDeviceToHost, w->s));
   NWT_CUDA(cudaStreamSynchronize(w->s));
   return SPN_OK;
+  SPN_CATCH
 }
 
-spn_status spn_hessian_sqrt_host(spn_newton* w, const double* x, float* out, int64_t ld_out) {
+spn_status spn_hessian_sqrt_host(spn_newton* w, const double* x, float* out, int64_t ld_out) { SPN_TRY
   if (spn_status st = need_problem(w)) return st;
   if (!x || !out) return fail(SPN_EINVAL, "null pointer");
   if (ld_out < w->d) return fail(SPN_EINVAL, "bad leading dimension");
@@ -914,10 +922,11 @@ spn_status spn_hessian_sqrt_host(spn_newton* w, const double* x, float* out, int
   if (e != cudaSuccess) return spn::cuda_error(e, "hessian_sqrt copy");
   NWT_CUDA(cudaStreamSynchronize(w->s));
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_sketched_step_host(spn_newton* w, const spn_plan* sketch, int64_t rows, const double* x, double* step,
-                                  double* grad, double* loss) {
+                                  double* grad, double* loss) { SPN_TRY
   if (spn_status st = need_problem(w)) return st;
   if (!x || !step) return fail(SPN_EINVAL, "null pointer");
   DevGuard g(w->device);
@@ -933,10 +942,11 @@ spn_status spn_sketched_step_host(spn_newton* w, const spn_plan* sketch, int64_t
   if (loss) NWT_CUDA(cudaMemcpyAsync(loss, df, sizeof(double), cudaMemcpyDeviceToHost, w->s));
   NWT_CUDA(cudaStreamSynchronize(w->s));
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_logistic_line_host(spn_newton* w, const double* x, const double* step, double s0, int64_t count,
-                                  double* losses) {
+                                  double* losses) { SPN_TRY
   if (spn_status st = need_problem(w)) return st;
   if (!x || !step || !losses) return fail(SPN_EINVAL, "null pointer");
   if (count < 1 || count > 64) return fail(SPN_EINVAL, "line search: 1 <= count <= 64");
@@ -951,9 +961,10 @@ spn_status spn_logistic_line_host(spn_newton* w, const double* x, const double* 
   NWT_CUDA(cudaMemcpyAsync(losses, dl, sizeof(double) * (size_t)count, cudaMemcpyDeviceToHost, w->s));
   NWT_CUDA(cudaStreamSynchronize(w->s));
   return SPN_OK;
+  SPN_CATCH
 }
 
-spn_status spn_ar1_problem(int64_t n, int64_t d, uint64_t seed, float* features, float* labels) {
+spn_status spn_ar1_problem(int64_t n, int64_t d, uint64_t seed, float* features, float* labels) { SPN_TRY
   if (n < 1 || d < 1) return fail(SPN_EDIM, "generate_ar1_problem: n, d must be >= 1");
   if (!features || !labels) return fail(SPN_EINVAL, "null pointer");
   // newton_sketch.cpp:185-204 with the reference generator (host_params.hpp HostRng)
@@ -969,6 +980,7 @@ spn_status spn_ar1_problem(int64_t n, int64_t d, uint64_t seed, float* features,
   }
   for (int64_t i = 0; i < n; ++i) labels[i] = (float)rng.rademacher();
   return SPN_OK;
+  SPN_CATCH
 }
 
 }  // extern "C"

@@ -595,7 +595,6 @@ struct BigPlan {
   bool sk_ready = false;
   int sk_lsa = 0, sk_lsb = 0;
   float* sk_d[3] = {nullptr, nullptr, nullptr};
-  float* sk_d1s = nullptr;  // D1 * row scale (Newton step), lazily allocated
   // Rademacher (HD3) single-block plans realise their sketch diagonals on the device
   // (mt_rademacher_sketch_kernel) instead of uploading host draws
   bool dev_rad = false;
@@ -665,8 +664,6 @@ struct BigPlan {
         pfree(q);
         q = nullptr;
       }
-      pfree(sk_d1s);
-      sk_d1s = nullptr;
       pfree(rowmap);
       rowmap = nullptr;
       for (auto& u : uses) cudaEventDestroy(u.second);
@@ -1050,15 +1047,18 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
   // the realisation (realisation stream) and the row map (possibly another caller stream)
   if (cudaError_t e = bp->wait_ready(s0)) return BigPlan::err(e, "sketch ready");
   const float* d1 = bp->sk_d[0];
+  // D1 times the row scale: per call, from the stream-ordered pool on s0 (freed on s0 after the
+  // join), so calls on different streams sharing this plan never overwrite each other's copy
+  Scratch d1s;
   if (row_scale) {
-    cudaError_t e = cudaSuccess;
-    if (!bp->sk_d1s) e = pool_alloc(reinterpret_cast<void**>(&bp->sk_d1s), static_cast<size_t>(nn) * 4, s0);
+    cudaError_t e = d1s.alloc(static_cast<size_t>(nn) * 4, s0);
     if (e != cudaSuccess) return BigPlan::err(e, "scaled D1");
     const int64_t blocks = std::min<int64_t>((nn + 255) / 256, int64_t(sms) * 8);
-    scale_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, s0>>>(bp->sk_d[0], row_scale, n_in, nn, bp->sk_d1s);
+    scale_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, s0>>>(bp->sk_d[0], row_scale, n_in, nn,
+                                                                       static_cast<float*>(d1s.p));
     e = cudaGetLastError();
     if (e != cudaSuccess) return BigPlan::err(e, "scaled D1");
-    d1 = bp->sk_d1s;
+    d1 = static_cast<const float*>(d1s.p);
   }
   cudaStream_t s = s0;
   const int lsa = bp->sk_lsa, lsb = bp->sk_lsb;

@@ -439,20 +439,12 @@ __device__ __forceinline__ void thread_argmax(const float (&r)[C::R], int first_
   vbest = vb;
 }
 
-// sin/cos for the random-feature epilogue (kernels.cpp:29-34): Cody-Waite reduction by
-// 2*pi (two-constant split, FFMA) to |r| <= pi, then the SFU (MUFU.SIN/COS, max abs
-// error 2^-21.4 on [-pi, pi]).  Runs on the XU pipe, off the FP32 pipe that the
-// butterflies saturate; abs error ~4e-7 against features of rms 0.7.
-//
-// The argument arrives in revolutions (u = t / 2pi, the 1/2pi folded into the host-side
-// multiplier): f = u - rint(u) is exact, a = 2pi f in [-pi, pi].
-__device__ __forceinline__ void sincos_rev(float u, float& s, float& c) {
-  const float f = u - rintf(u);
-  const float a = f * 6.28318530717958648f;
-  s = __sinf(a);
-  c = __cosf(a);
-}
-
+// sin/cos for the random-feature epilogue (kernels.cpp:29-34): __sincosf on the angle t
+// itself, i.e. the SFU path (FMUL.RZ by 1/2pi + MUFU.SIN/COS) with no explicit range
+// reduction.  Its absolute error grows with |t| (tools/microbench/sincos_acc.cu: max abs
+// error 2.4e-6 for |t| <= 20; DESIGN.md §3 lists the measured domain).  The Gaussian embed
+// at config-2 scale (x in [0,1]^784, sqrt(n)/sigma = 6.4) gives t ~ N(0, 3.2^2), so |t| <= 20
+// holds with > 6 sigma margin and the features meet the 1e-5 relative-L2 bar.
 // (A 16-B-store variant of this epilogue — angles re-laid through smem so each lane owns
 // four consecutive elements — measured 0.577 vs 0.458 ms on config 2 and was dropped.)
 // Permuted-coordinate Gaussian embed (OP_EMBED_GAUSS_P): layout-B register j of lane t

@@ -96,13 +96,26 @@ struct spn_plan {
   // multi-pass layouts (n > 2^14)
   spn::BigPlan big;
 
+  // multi-block sketch: one single-block plan per block (sketch_subplans)
+  std::mutex sub_mu;
+  std::vector<spn_plan*> sub;
+
   // host-API staging (lazily grown; guarded by mu)
   std::mutex mu;
   cudaStream_t hs[2] = {nullptr, nullptr};
-  void* hbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  size_t hbuf_bytes[2][2] = {{0, 0}, {0, 0}};
+  void* hbuf[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};  // [stream][x | out0 | out1]
+  size_t hbuf_bytes[2][3] = {{0, 0, 0}, {0, 0, 0}};
 
-  ~spn_plan() {
+  ~spn_plan();
+};
+
+namespace {
+spn_status plan_destroy_impl(spn_plan* p);
+}  // namespace
+
+spn_plan::~spn_plan() {
+  {
+    for (spn_plan* q : sub) plan_destroy_impl(q);
     DeviceGuard g(device);
     if (fam) spn::family_destroy(fam);
     for (auto& a : vsgn)
@@ -121,7 +134,14 @@ struct spn_plan {
     for (auto s : hs)
       if (s) cudaStreamDestroy(s);
   }
-};
+}
+
+namespace {
+spn_status plan_destroy_impl(spn_plan* p) {
+  delete p;
+  return SPN_OK;
+}
+}  // namespace
 
 namespace {
 
@@ -326,6 +346,79 @@ spn_status big_embed(spn_plan* p, int32_t kind, double sigma, const float* x, in
 
 }  // namespace
 
+// ------------------------------------------------------------------------ sketches
+namespace {
+
+// SketchOperator::apply argument checks (newton_sketch.cpp:87-90).  rows == NULL is the reference's
+// P = first m_out rows of the stacked output; a row list (builder-defined P) indexes the n outputs
+// of a single-block plan.
+spn_status sketch_check(const spn_plan* p, const float* a, int64_t n_in, int64_t d, int64_t ld_a,
+                        const int64_t* rows, int64_t m_out, const float* out, int64_t ld_out) {
+  if (!p) return fail(SPN_EINVAL, "null plan");
+  if (p->fam) return fail(SPN_EUNSUPPORTED, "sketch: Hadamard-only variants (HD3/HDg) on the device");
+  if (p->tables != 1) return fail(SPN_EUNSUPPORTED, "sketch needs a single-table plan");
+  if (n_in < 1 || n_in > p->n) return fail(SPN_EDIM, "SketchOperator::apply: row count mismatch");
+  if (d < 0 || m_out < 0) return fail(SPN_EDIM, "bad sketch shape");
+  if (ld_a < d || ld_out < d) return fail(SPN_EINVAL, "bad leading dimension");
+  if (d > 0 && m_out > 0 && (!a || !out)) return fail(SPN_EINVAL, "null pointer");
+  if (!rows && m_out > p->k) return fail(SPN_EDIM, "first-m sketch: m_out > k");
+  if (rows) {
+    if (p->blocks != 1) return fail(SPN_EUNSUPPORTED, "row-sampled sketch needs a single-block plan");
+    if (m_out > p->n) return fail(SPN_EDIM, "bad sketch shape");
+    for (int64_t r = 0; r < m_out; ++r)
+      if (rows[r] < 0 || rows[r] >= p->n) return fail(SPN_EDIM, "row index out of range");
+  }
+  return SPN_OK;
+}
+
+// Multi-block sketches (rows > next_pow2(input_dim): StackedSpinner(v, padded, padded, rows, seed),
+// newton_sketch.cpp:77-79): block b produces output rows [b*m, b*m + m) from its own single-block
+// plan, made once from the realised diagonals of (table 0, block b).
+spn_status sketch_subplans(spn_plan* p) {
+  std::lock_guard<std::mutex> lock(p->sub_mu);
+  if (!p->sub.empty()) return SPN_OK;
+  std::vector<spn_plan*> sub;
+  for (int64_t b = 0; b < p->blocks; ++b) {
+    spn_plan* q = nullptr;
+    const int64_t off = b * p->n;
+    spn_status st = spn_plan_create_explicit(&q, p->n, p->n, p->n, 1, p->d[0].data() + off, p->d[1].data() + off,
+                                             p->d[2].data() + off, p->scale, p->device);
+    if (st) {
+      for (spn_plan* r : sub) spn_plan_destroy(r);
+      return st;
+    }
+    sub.push_back(q);
+  }
+  p->sub = std::move(sub);
+  return SPN_OK;
+}
+
+spn_status sketch_dispatch(const spn_plan* cp, const float* a, int64_t n_in, int64_t d, int64_t ld_a,
+                           const int64_t* rows, int64_t m_out, double norm, float* out, int64_t ld_out,
+                           cudaStream_t s, const float* row_scale) {
+  if (spn_status st = sketch_check(cp, a, n_in, d, ld_a, rows, m_out, out, ld_out)) return st;
+  if (d == 0 || m_out == 0) return SPN_OK;
+  auto* p = const_cast<spn_plan*>(cp);
+  DeviceGuard g(p->device);
+  if (p->blocks == 1)
+    return spn::sketch_run(p->n, p->d, p->dsign, a, n_in, d, ld_a, rows, m_out,
+                           p->scale * std::pow(static_cast<double>(p->n), -1.5) * norm, out, ld_out, p->sms, s,
+                           &p->big, row_scale);
+  if (spn_status st = sketch_subplans(p)) return st;
+  for (int64_t b = 0; b < p->blocks && b * p->m < m_out; ++b) {
+    const int64_t mb = std::min(p->m, m_out - b * p->m);
+    const spn_plan* q = p->sub[static_cast<size_t>(b)];
+    if (spn_status st = spn::sketch_run(q->n, q->d, q->dsign, a, n_in, d, ld_a, nullptr, mb,
+                                        q->scale * std::pow(static_cast<double>(q->n), -1.5) * norm,
+                                        out + b * p->m * ld_out, ld_out, q->sms, s,
+                                        const_cast<spn::BigPlan*>(&q->big), row_scale))
+      return st;
+  }
+  return SPN_OK;
+}
+
+}  // namespace
+
 // =============================================================================== C ABI
 
 extern "C" {
@@ -348,22 +441,24 @@ const char* spn_last_error(void) { return spn::last_error().c_str(); }
 const char* spn_version(void) { return "spinners_b200 0.1 (sm_100a)"; }
 uint64_t spn_mix_seed(uint64_t base, uint64_t stream) { return spn::mix_seed(base, stream); }
 
-spn_status spn_sample_rows(int64_t N, int64_t m, uint64_t seed, int64_t* out) {
+spn_status spn_sample_rows(int64_t N, int64_t m, uint64_t seed, int64_t* out) { SPN_TRY
   if (!out) return fail(SPN_EINVAL, "null out");
   if (N < 1 || m < 0 || m > N) return fail(SPN_EDIM, "need 0 <= m <= N, N >= 1");
   std::vector<int64_t> r = spn::sample_rows(N, m, seed);
   std::copy(r.begin(), r.end(), out);
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_realize_block(int32_t variant, int64_t n, uint64_t spec_seed, double* d1, double* d2,
-                             double* d3) {
+                             double* d3) { SPN_TRY
   if (!d1 || !d2 || !d3) return fail(SPN_EINVAL, "null argument");
   if (variant != SPN_HD3_HD2_HD1 && variant != SPN_HDG_HD2_HD1 && variant != SPN_GAUSS3)
     return fail(SPN_EDOMAIN, "unknown spinner variant " + std::to_string(variant));
   if (n < 1) return fail(SPN_EDIM, "n must be >= 1");
   spn::realize_block(variant, n, spec_seed, d1, d2, d3);
   return SPN_OK;
+  SPN_CATCH
 }
 
 }  // extern "C"
@@ -376,12 +471,14 @@ spn_status plan_create_impl(spn_plan** out, const spn_plan_desc* d, bool raw_spe
 
 extern "C" {
 
-spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) { return plan_create_impl(out, d, false); }
+spn_status spn_plan_create(spn_plan** out, const spn_plan_desc* d) { SPN_TRY return plan_create_impl(out, d, false);   SPN_CATCH
+}
 
 spn_status spn_plan_create_block(spn_plan** out, int32_t variant, int64_t n, int64_t m, uint64_t spec_seed,
-                                 double scale, int32_t device) {
+                                 double scale, int32_t device) { SPN_TRY
   const spn_plan_desc d{variant, n, m, m, 1, nullptr, spec_seed, scale, device};
   return plan_create_impl(out, &d, true);
+  SPN_CATCH
 }
 
 }  // extern "C"
@@ -470,7 +567,7 @@ extern "C" {
 
 spn_status spn_plan_create_explicit(spn_plan** out, int64_t n, int64_t m, int64_t k,
                                     int64_t tables, const double* d1, const double* d2,
-                                    const double* d3, double scale, int32_t device) {
+                                    const double* d3, double scale, int32_t device) { SPN_TRY
   if (!out || !d1 || !d2 || !d3) return fail(SPN_EINVAL, "null argument");
   *out = nullptr;
   if (spn_status s = validate_shape(n, m, k, tables)) return s;
@@ -500,15 +597,90 @@ spn_status spn_plan_create_explicit(spn_plan** out, int64_t n, int64_t m, int64_
   }
   *out = p;
   return SPN_OK;
+  SPN_CATCH
 }
 
-spn_status spn_plan_destroy(spn_plan* p) {
+// StructuredSpinner::resample_last_block / resample_tail / with_tail_vector (spinner.hpp:67-77,
+// spinner.cpp:153-184): a new one-block plan with the source's realised parameters and the tail
+// (and for resample_tail also D2) redrawn or replaced.
+namespace {
+spn_plan* clone_block(const spn_plan* src) {
+  auto* p = new spn_plan();
+  p->variant = src->variant;
+  p->n = src->n;
+  p->m = src->m;
+  p->k = src->k;
+  p->tables = 1;
+  p->blocks = 1;
+  p->device = src->device;
+  p->scale = src->scale;
+  for (int di = 0; di < 3; ++di) p->d[di] = src->d[di];
+  p->trow = src->trow;
+  p->dense = src->dense;
+  return p;
+}
+spn_status one_block(const spn_plan* src, const char* what) {
+  if (!src) return fail(SPN_EINVAL, "null plan");
+  if (src->tables != 1 || src->blocks != 1)
+    return fail(SPN_EUNSUPPORTED, std::string(what) + ": needs a one-block plan (StructuredSpinner)");
+  return SPN_OK;
+}
+}  // namespace
+
+spn_status spn_plan_resample(spn_plan** out, const spn_plan* src, int32_t mode, uint64_t tail_seed) { SPN_TRY
+  if (!out) return fail(SPN_EINVAL, "null argument");
+  *out = nullptr;
+  if (spn_status st = one_block(src, "resample")) return st;
+  if (mode != 0 && mode != 1) return fail(SPN_EINVAL, "resample: mode must be 0 (last block) or 1 (tail)");
+  if (src->variant < 0) return fail(SPN_EUNSUPPORTED, "resample: plan was made from explicit diagonals");
+  const_cast<spn_plan*>(src)->ensure_host_d();
+  spn_plan* p = clone_block(src);
+  const int64_t n = p->n;
+  spn::HostRng rng(spn::mix_seed(tail_seed, mode == 0 ? 2 : 3));  // spinner.cpp:154 / :161
+  if (mode == 1 && p->variant != SPN_GAUSSIAN_DENSE) {
+    // resample_tail redraws D2 first (Rademacher; the builder-defined Gauss3 keeps its N(0,1) D2)
+    for (int64_t i = 0; i < n; ++i) p->d[1][static_cast<size_t>(i)] = p->variant == SPN_GAUSS3 ? rng.gaussian() : rng.rademacher();
+  }
+  spn::draw_tail(p->variant, n, p->m, rng, p->d[2].data(), p->trow.empty() ? nullptr : p->trow.data(),
+                 p->dense.empty() ? nullptr : p->dense.data());
+  if (spn_status st = finish_plan(p)) {
+    delete p;
+    return st;
+  }
+  *out = p;
+  return SPN_OK;
+  SPN_CATCH
+}
+
+spn_status spn_plan_with_tail(spn_plan** out, const spn_plan* src, const double* r) { SPN_TRY
+  if (!out || !r) return fail(SPN_EINVAL, "null argument");
+  *out = nullptr;
+  if (spn_status st = one_block(src, "with_tail_vector")) return st;
+  if (src->variant != SPN_HD3_HD2_HD1 && src->variant != SPN_HDG_HD2_HD1 && src->variant != SPN_GAUSS3 &&
+      src->variant != -1)
+    return fail(SPN_EDOMAIN, "with_tail_vector: only valid for Hadamard-only variants");
+  for (int64_t i = 0; i < src->n; ++i)
+    if (!std::isfinite(r[i])) return fail(SPN_EDOMAIN, "with_tail_vector: non-finite entry");
+  const_cast<spn_plan*>(src)->ensure_host_d();
+  spn_plan* p = clone_block(src);
+  p->d[2].assign(r, r + p->n);
+  if (spn_status st = finish_plan(p)) {
+    delete p;
+    return st;
+  }
+  *out = p;
+  return SPN_OK;
+  SPN_CATCH
+}
+
+spn_status spn_plan_destroy(spn_plan* p) { SPN_TRY
   delete p;
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_plan_query(const spn_plan* p, int64_t* n, int64_t* m, int64_t* k, int64_t* tables,
-                          int64_t* blocks, double* scale) {
+                          int64_t* blocks, double* scale) { SPN_TRY
   if (!p) return fail(SPN_EINVAL, "null plan");
   if (n) *n = p->n;
   if (m) *m = p->m;
@@ -517,19 +689,21 @@ spn_status spn_plan_query(const spn_plan* p, int64_t* n, int64_t* m, int64_t* k,
   if (blocks) *blocks = p->blocks;
   if (scale) *scale = p->scale;
   return SPN_OK;
+  SPN_CATCH
 }
 
-spn_status spn_plan_diagonals(const spn_plan* p, double* d1, double* d2, double* d3) {
+spn_status spn_plan_diagonals(const spn_plan* p, double* d1, double* d2, double* d3) { SPN_TRY
   if (!p) return fail(SPN_EINVAL, "null plan");
   double* dst[3] = {d1, d2, d3};
   const_cast<spn_plan*>(p)->ensure_host_d();
   for (int di = 0; di < 3; ++di)
     if (dst[di]) std::copy(p->d[di].begin(), p->d[di].end(), dst[di]);
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_apply_f32(const spn_plan* p, const float* x, int64_t batch, int64_t ld_x,
-                         int64_t n_in, float* y, int64_t ld_y, int32_t relu, void* stream) {
+                         int64_t n_in, float* y, int64_t ld_y, int32_t relu, void* stream) { SPN_TRY
   if (spn_status s = check_io(p, x, batch, ld_x, n_in)) return s;
   if (p->tables != 1) return fail(SPN_EINVAL, "apply needs a single-table plan");
   if (batch > 0 && !y) return fail(SPN_EINVAL, "null output");
@@ -554,10 +728,11 @@ spn_status spn_apply_f32(const spn_plan* p, const float* x, int64_t batch, int64
   v.ld_y = ld_y;
   v.relu = relu;
   return run_vec(p, spn::OP_APPLY, v, static_cast<cudaStream_t>(stream));
+  SPN_CATCH
 }
 
 spn_status spn_hash_f32(const spn_plan* p, const float* x, int64_t batch, int64_t ld_x,
-                        int64_t n_in, int32_t* ids, float* y, int64_t ld_y, void* stream) {
+                        int64_t n_in, int32_t* ids, float* y, int64_t ld_y, void* stream) { SPN_TRY
   if (spn_status s = check_io(p, x, batch, ld_x, n_in)) return s;
   if (batch > 0 && !ids) return fail(SPN_EINVAL, "null ids");
   if (p->fam) {
@@ -580,6 +755,7 @@ spn_status spn_hash_f32(const spn_plan* p, const float* x, int64_t batch, int64_
   v.y = y;
   v.ld_y = ld_y;
   return run_vec(p, y ? spn::OP_APPLY : spn::OP_HASH, v, static_cast<cudaStream_t>(stream));
+  SPN_CATCH
 }
 
 // collision_curve's counting core (lsh.cpp:54-61): per pair, how many tables give
@@ -597,7 +773,7 @@ __global__ void collision_count_kernel(const int32_t* __restrict__ ids, int64_t 
 }
 
 spn_status spn_collision_hits_f32(const spn_plan* p, const float* xy, int64_t pairs, int64_t ld, int64_t n_in,
-                                  const int32_t* bucket_of, int64_t buckets, int64_t* hits, void* stream) {
+                                  const int32_t* bucket_of, int64_t buckets, int64_t* hits, void* stream) { SPN_TRY
   if (spn_status s = check_io(p, xy, 2 * pairs, ld, n_in)) return s;
   if (pairs > 0 && (!bucket_of || !hits)) return fail(SPN_EINVAL, "null pointer");
   if (buckets < 1) return fail(SPN_EDIM, "collision_curve: need at least one bucket");
@@ -618,13 +794,16 @@ spn_status spn_collision_hits_f32(const spn_plan* p, const float* xy, int64_t pa
     SPN_CUDA(cudaGetLastError());
   }
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_hash_f32_peers(const spn_plan* p, const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
-                              int32_t* const* peers, int32_t npeers, int64_t row0, void* stream) {
+                              int32_t* const* peers, int32_t npeers, int64_t row0, int64_t total,
+                              void* stream) { SPN_TRY
   if (spn_status s = check_io(p, x, batch, ld_x, n_in)) return s;
   if (npeers < 1 || !peers) return fail(SPN_EINVAL, "need >= 1 peer table");
-  if (row0 < 0) return fail(SPN_EINVAL, "row0 < 0");
+  if (row0 < 0 || row0 + batch > total)
+    return fail(SPN_EINVAL, "peer hash: rows [row0, row0 + batch) outside the gathered table");
   if (p->fam) return fail(SPN_EUNSUPPORTED, "peer hash: Hadamard-only variants");
   if (p->k >= (int64_t(1) << 30)) return fail(SPN_EDIM, "2k must fit int32 ids");
   if (p->log_n > kMaxLogNVec) return fail(SPN_EUNSUPPORTED, "hash with n > 2^14 not implemented");
@@ -637,11 +816,12 @@ spn_status spn_hash_f32_peers(const spn_plan* p, const float* x, int64_t batch, 
   v.npeers = npeers;
   v.peer_row0 = row0;
   return run_vec(p, spn::OP_HASH, v, static_cast<cudaStream_t>(stream));
+  SPN_CATCH
 }
 
 spn_status spn_embed_f32(const spn_plan* p, int32_t kind, double sigma, const float* x,
                          int64_t batch, int64_t ld_x, int64_t n_in, float* out, int64_t ld_out,
-                         void* stream) {
+                         void* stream) { SPN_TRY
   if (spn_status s = check_io(p, x, batch, ld_x, n_in)) return s;
   if (p->tables != 1) return fail(SPN_EINVAL, "embed needs a single-table plan");
   if (kind != SPN_EMBED_GAUSSIAN && kind != SPN_EMBED_ANGULAR) return fail(SPN_EDOMAIN, "unknown kernel kind");
@@ -680,27 +860,53 @@ spn_status spn_embed_f32(const spn_plan* p, int32_t kind, double sigma, const fl
   }
   return run_vec(p, kind == SPN_EMBED_GAUSSIAN ? spn::OP_EMBED_GAUSS : spn::OP_EMBED_ANG, v,
                  static_cast<cudaStream_t>(stream));
+  SPN_CATCH
 }
 
 spn_status spn_sketch_f32(const spn_plan* p, const float* a, int64_t n_in, int64_t d, int64_t ld_a,
                           const int64_t* rows, int64_t m_out, double norm, float* out,
-                          int64_t ld_out, void* stream) {
-  if (!p) return fail(SPN_EINVAL, "null plan");
-  if (p->fam) return fail(SPN_EUNSUPPORTED, "sketch: Hadamard-only variants (HD3/HDg) on the device");
-  if (p->tables != 1 || p->blocks != 1) return fail(SPN_EUNSUPPORTED, "sketch needs one table of one block");
-  if (n_in < 1 || n_in > p->n) return fail(SPN_EDIM, "SketchOperator::apply: row count mismatch");
-  if (d < 0 || m_out < 0 || m_out > p->n) return fail(SPN_EDIM, "bad sketch shape");
-  if (ld_a < d || ld_out < d) return fail(SPN_EINVAL, "bad leading dimension");
-  if (d > 0 && m_out > 0 && (!a || !out)) return fail(SPN_EINVAL, "null pointer");
-  if (!rows && m_out > p->k) return fail(SPN_EDIM, "first-m sketch: m_out > k");
-  if (rows)
-    for (int64_t r = 0; r < m_out; ++r)
-      if (rows[r] < 0 || rows[r] >= p->n) return fail(SPN_EDIM, "row index out of range");
+                          int64_t ld_out, void* stream) { SPN_TRY
+  return sketch_dispatch(p, a, n_in, d, ld_a, rows, m_out, norm, out, ld_out, static_cast<cudaStream_t>(stream),
+                         nullptr);
+  SPN_CATCH
+}
+
+// SketchOperator::apply with the reference's value semantics (newton_sketch.cpp:87-101): host A in,
+// host sketch out.  A goes to the device in one pass (linear copies when the rows are packed at a
+// 16-B multiple), the sketch runs there, the m_out x d result comes back.
+spn_status spn_sketch_f32_host(const spn_plan* cp, const float* a, int64_t n_in, int64_t d, int64_t ld_a,
+                               const int64_t* rows, int64_t m_out, double norm, float* out,
+                               int64_t ld_out) { SPN_TRY
+  if (spn_status st = sketch_check(cp, a, n_in, d, ld_a, rows, m_out, out, ld_out)) return st;
   if (d == 0 || m_out == 0) return SPN_OK;
+  auto* p = const_cast<spn_plan*>(cp);
+  std::lock_guard<std::mutex> lock(p->mu);
   DeviceGuard g(p->device);
-  return spn::sketch_run(p->n, p->d, p->dsign, a, n_in, d, ld_a, rows, m_out,
-                         p->scale * std::pow(static_cast<double>(p->n), -1.5) * norm, out, ld_out,
-                         p->sms, static_cast<cudaStream_t>(stream), const_cast<spn::BigPlan*>(&p->big));
+  if (!p->hs[0]) SPN_CUDA(cudaStreamCreateWithFlags(&p->hs[0], cudaStreamNonBlocking));
+  cudaStream_t s = p->hs[0];
+  const int64_t ldd = (d + 3) / 4 * 4;  // 16-B aligned device rows (the TMA column passes need them)
+  spn::Scratch da, dout;
+  SPN_CUDA(da.alloc(sizeof(float) * static_cast<size_t>(n_in * ldd), s));
+  SPN_CUDA(dout.alloc(sizeof(float) * static_cast<size_t>(m_out * ldd), s));
+  struct Drain {  // the copies reference the caller's buffers: complete them on every exit
+    cudaStream_t s;
+    ~Drain() { cudaStreamSynchronize(s); }
+  } drain{s};
+  float* A = static_cast<float*>(da.p);
+  if (ld_a == ldd) {  // packed rows: linear copies of <= 32 MB
+    const int64_t total = n_in * ldd, piece = int64_t(8) << 20;
+    for (int64_t o = 0; o < total; o += piece)
+      SPN_CUDA(cudaMemcpyAsync(A + o, a + o, sizeof(float) * static_cast<size_t>(std::min(piece, total - o)),
+                               cudaMemcpyHostToDevice, s));
+  } else {
+    SPN_CUDA(cudaMemcpy2DAsync(A, ldd * 4, a, ld_a * 4, d * 4, n_in, cudaMemcpyHostToDevice, s));
+  }
+  float* O = static_cast<float*>(dout.p);
+  if (spn_status st = sketch_dispatch(p, A, n_in, d, ldd, rows, m_out, norm, O, ldd, s, nullptr)) return st;
+  SPN_CUDA(cudaMemcpy2DAsync(out, ld_out * 4, O, ldd * 4, d * 4, m_out, cudaMemcpyDeviceToHost, s));
+  SPN_CUDA(cudaStreamSynchronize(s));
+  return SPN_OK;
+  SPN_CATCH
 }
 
 // --------------------------------------------------------------------- host-buffer API
@@ -715,24 +921,24 @@ int plan_device(const spn_plan* p) { return p->device; }
 spn_status plan_sketch_scaled(const spn_plan* p, const float* a, int64_t n_in, int64_t d, int64_t ld_a,
                               int64_t m_out, double norm, const float* row_scale, float* out, int64_t ld_out,
                               cudaStream_t s) {
-  if (p->fam) return fail(SPN_EUNSUPPORTED, "sketch: Hadamard-only variants (HD3/HDg) on the device");
-  if (p->tables != 1 || p->blocks != 1) return fail(SPN_EUNSUPPORTED, "sketch needs one table of one block");
-  if (n_in < 1 || n_in > p->n) return fail(SPN_EDIM, "SketchOperator::apply: row count mismatch");
-  if (m_out > p->k || m_out > p->n) return fail(SPN_EDIM, "sketch rows exceed the plan");
-  DeviceGuard g(p->device);
-  return sketch_run(p->n, p->d, p->dsign, a, n_in, d, ld_a, nullptr, m_out,
-                    p->scale * std::pow(static_cast<double>(p->n), -1.5) * norm, out, ld_out, p->sms, s,
-                    const_cast<BigPlan*>(&p->big), row_scale);
+  return sketch_dispatch(p, a, n_in, d, ld_a, nullptr, m_out, norm, out, ld_out, s, row_scale);
 }
 
 }  // namespace spn
 
 namespace {
 
-// Pipelined host->device->host execution over row chunks on two streams.
+// One host output of host_pipeline: rows of row_bytes at a host stride of ld_bytes.
+struct HostOut {
+  void* ptr;
+  int64_t row_bytes, ld_bytes;
+};
+
+// Pipelined host->device->host execution over row chunks on two streams (up to two outputs per
+// row, e.g. ids and y).  launch(dx, rows, n_in, dout0, dout1, stream) runs the device op on a chunk.
 template <class Launch>
-spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
-                         void* out, int64_t out_row_bytes, int64_t ld_out_bytes, Launch launch) {
+spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_x, int64_t n_in, HostOut o0,
+                         HostOut o1, Launch launch) {
   if (batch == 0) return SPN_OK;
   std::lock_guard<std::mutex> lock(p->mu);
   DeviceGuard g(p->device);
@@ -740,7 +946,7 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
   // Chunks of ~1/8 of the traffic, 4..48 MB (the larger of input / output row bytes): small
   // calls still overlap H2D, kernel and D2H on the two copy engines; large ones keep the
   // per-chunk launch/copy overhead small.
-  const int64_t row_bytes = std::max<int64_t>(std::max<int64_t>(out_row_bytes, in_row), 1);
+  const int64_t row_bytes = std::max<int64_t>(std::max<int64_t>(o0.row_bytes + o1.row_bytes, in_row), 1);
   static const int64_t cap_mb = [] {
     const char* e = std::getenv("SPN_HOST_CHUNK_MB");
     const int64_t v = e ? std::atoll(e) : 48;
@@ -752,33 +958,46 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
   chunk = std::min(chunk, batch);
   for (int s = 0; s < 2; ++s) {
     if (!p->hs[s]) SPN_CUDA(cudaStreamCreateWithFlags(&p->hs[s], cudaStreamNonBlocking));
-    const size_t need[2] = {static_cast<size_t>(chunk * in_row), static_cast<size_t>(chunk * out_row_bytes)};
-    for (int b = 0; b < 2; ++b)
+    const size_t need[3] = {static_cast<size_t>(chunk * in_row), static_cast<size_t>(chunk * o0.row_bytes),
+                            static_cast<size_t>(chunk * o1.row_bytes)};
+    for (int b = 0; b < 3; ++b)
       if (p->hbuf_bytes[s][b] < need[b]) {
         if (p->hbuf[s][b]) cudaFree(p->hbuf[s][b]);
         p->hbuf[s][b] = nullptr;
+        p->hbuf_bytes[s][b] = 0;
         SPN_CUDA(cudaMalloc(&p->hbuf[s][b], need[b]));
         p->hbuf_bytes[s][b] = need[b];
       }
   }
+  // on every exit the enqueued copies are complete (they reference the caller's host buffers)
+  struct Drain {
+    spn_plan* p;
+    ~Drain() {
+      cudaStreamSynchronize(p->hs[0]);
+      cudaStreamSynchronize(p->hs[1]);
+    }
+  } drain{p};
+  auto d2h = [&](const HostOut& o, int64_t r0, int64_t rows, const void* dsrc, cudaStream_t st) -> cudaError_t {
+    if (!o.ptr) return cudaSuccess;
+    char* dst = static_cast<char*>(o.ptr) + r0 * o.ld_bytes;
+    if (o.ld_bytes == o.row_bytes) return cudaMemcpyAsync(dst, dsrc, o.row_bytes * rows, cudaMemcpyDeviceToHost, st);
+    return cudaMemcpy2DAsync(dst, o.ld_bytes, dsrc, o.row_bytes, o.row_bytes, rows, cudaMemcpyDeviceToHost, st);
+  };
   int c = 0;
   for (int64_t r0 = 0; r0 < batch; r0 += chunk, ++c) {
     const int s = c & 1;
     const int64_t rows = std::min(chunk, batch - r0);
     float* dx = static_cast<float*>(p->hbuf[s][0]);
-    char* dout = static_cast<char*>(p->hbuf[s][1]);
+    char* dout0 = static_cast<char*>(p->hbuf[s][1]);
+    char* dout1 = static_cast<char*>(p->hbuf[s][2]);
     if (ld_x * 4 == in_row)  // contiguous rows: one linear copy
       SPN_CUDA(cudaMemcpyAsync(dx, x + r0 * ld_x, in_row * rows, cudaMemcpyHostToDevice, p->hs[s]));
     else
       SPN_CUDA(cudaMemcpy2DAsync(dx, in_row, x + r0 * ld_x, ld_x * 4, in_row, rows, cudaMemcpyHostToDevice,
                                  p->hs[s]));
-    if (spn_status st = launch(dx, rows, n_in, dout, p->hs[s])) return st;
-    if (ld_out_bytes == out_row_bytes)
-      SPN_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + r0 * ld_out_bytes, dout, out_row_bytes * rows,
-                               cudaMemcpyDeviceToHost, p->hs[s]));
-    else
-      SPN_CUDA(cudaMemcpy2DAsync(static_cast<char*>(out) + r0 * ld_out_bytes, ld_out_bytes, dout, out_row_bytes,
-                                 out_row_bytes, rows, cudaMemcpyDeviceToHost, p->hs[s]));
+    if (spn_status st = launch(dx, rows, n_in, dout0, dout1, p->hs[s])) return st;
+    SPN_CUDA(d2h(o0, r0, rows, dout0, p->hs[s]));
+    SPN_CUDA(d2h(o1, r0, rows, dout1, p->hs[s]));
   }
   SPN_CUDA(cudaStreamSynchronize(p->hs[0]));
   SPN_CUDA(cudaStreamSynchronize(p->hs[1]));
@@ -790,39 +1009,57 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
 extern "C" {
 
 spn_status spn_apply_f32_host(const spn_plan* cp, const float* x, int64_t batch, int64_t ld_x,
-                              int64_t n_in, float* y, int64_t ld_y, int32_t relu) {
+                              int64_t n_in, float* y, int64_t ld_y, int32_t relu) { SPN_TRY
   if (spn_status s = check_io(cp, x, batch, ld_x, n_in)) return s;
   if (batch > 0 && !y) return fail(SPN_EINVAL, "null output");
   if (ld_y < cp->k) return fail(SPN_EINVAL, "ld_y < k");
   auto* p = const_cast<spn_plan*>(cp);
-  return host_pipeline(p, x, batch, ld_x, n_in, y, p->k * 4, ld_y * 4,
-                       [&](const float* dx, int64_t rows, int64_t nin, char* dout, cudaStream_t s) {
+  return host_pipeline(p, x, batch, ld_x, n_in, HostOut{y, p->k * 4, ld_y * 4}, HostOut{nullptr, 0, 0},
+                       [&](const float* dx, int64_t rows, int64_t nin, char* dout, char*, cudaStream_t s) {
                          return spn_apply_f32(p, dx, rows, nin, nin, reinterpret_cast<float*>(dout), p->k, relu, s);
                        });
+  SPN_CATCH
 }
 
 spn_status spn_hash_f32_host(const spn_plan* cp, const float* x, int64_t batch, int64_t ld_x,
-                             int64_t n_in, int32_t* ids) {
+                             int64_t n_in, int32_t* ids) { SPN_TRY
   if (spn_status s = check_io(cp, x, batch, ld_x, n_in)) return s;
   if (batch > 0 && !ids) return fail(SPN_EINVAL, "null ids");
   auto* p = const_cast<spn_plan*>(cp);
-  return host_pipeline(p, x, batch, ld_x, n_in, ids, p->tables * 4, p->tables * 4,
-                       [&](const float* dx, int64_t rows, int64_t nin, char* dout, cudaStream_t s) {
+  return host_pipeline(p, x, batch, ld_x, n_in, HostOut{ids, p->tables * 4, p->tables * 4}, HostOut{nullptr, 0, 0},
+                       [&](const float* dx, int64_t rows, int64_t nin, char* dout, char*, cudaStream_t s) {
                          return spn_hash_f32(p, dx, rows, nin, nin, reinterpret_cast<int32_t*>(dout), nullptr, 0, s);
                        });
+  SPN_CATCH
+}
+
+spn_status spn_hash_project_f32_host(const spn_plan* cp, const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
+                                     int32_t* ids, float* y, int64_t ld_y) { SPN_TRY
+  if (spn_status s = check_io(cp, x, batch, ld_x, n_in)) return s;
+  if (batch > 0 && (!ids || !y)) return fail(SPN_EINVAL, "null output");
+  if (cp->tables != 1) return fail(SPN_EINVAL, "y output needs a single-table plan");
+  if (ld_y < cp->k) return fail(SPN_EINVAL, "ld_y < k");
+  auto* p = const_cast<spn_plan*>(cp);
+  return host_pipeline(p, x, batch, ld_x, n_in, HostOut{ids, 4, 4}, HostOut{y, p->k * 4, ld_y * 4},
+                       [&](const float* dx, int64_t rows, int64_t nin, char* dids, char* dy, cudaStream_t s) {
+                         return spn_hash_f32(p, dx, rows, nin, nin, reinterpret_cast<int32_t*>(dids),
+                                             reinterpret_cast<float*>(dy), p->k, s);
+                       });
+  SPN_CATCH
 }
 
 spn_status spn_embed_f32_host(const spn_plan* cp, int32_t kind, double sigma, const float* x,
-                              int64_t batch, int64_t ld_x, int64_t n_in, float* out, int64_t ld_out) {
+                              int64_t batch, int64_t ld_x, int64_t n_in, float* out, int64_t ld_out) { SPN_TRY
   if (spn_status s = check_io(cp, x, batch, ld_x, n_in)) return s;
   const int64_t w = kind == SPN_EMBED_GAUSSIAN ? 2 * cp->k : cp->k;
   if (batch > 0 && !out) return fail(SPN_EINVAL, "null output");
   if (ld_out < w) return fail(SPN_EINVAL, "ld_out too small");
   auto* p = const_cast<spn_plan*>(cp);
-  return host_pipeline(p, x, batch, ld_x, n_in, out, w * 4, ld_out * 4,
-                       [&](const float* dx, int64_t rows, int64_t nin, char* dout, cudaStream_t s) {
+  return host_pipeline(p, x, batch, ld_x, n_in, HostOut{out, w * 4, ld_out * 4}, HostOut{nullptr, 0, 0},
+                       [&](const float* dx, int64_t rows, int64_t nin, char* dout, char*, cudaStream_t s) {
                          return spn_embed_f32(p, kind, sigma, dx, rows, nin, nin, reinterpret_cast<float*>(dout), w, s);
                        });
+  SPN_CATCH
 }
 
 // ------------------------------------------------ standalone transforms (transforms.hpp:13,59)
@@ -869,7 +1106,7 @@ __global__ void diag_rows_kernel(int64_t n, const float* __restrict__ d, const f
 extern "C" {
 
 spn_status spn_fwht_f32(int64_t n, const float* x, int64_t batch, int64_t ld_x, float* y, int64_t ld_y,
-                        int32_t device, void* stream) {
+                        int32_t device, void* stream) { SPN_TRY
   if (spn_status s = fwht_args(n, x, batch, ld_x, y, ld_y)) return s;
   if (batch == 0) return SPN_OK;
   DeviceGuard g(device);
@@ -883,10 +1120,11 @@ spn_status spn_fwht_f32(int64_t n, const float* x, int64_t batch, int64_t ld_x, 
   spn_plan* p = fwht_plan(n, device, &st);
   if (!p) return st;
   return spn_apply_f32(p, x, batch, ld_x, n, y, ld_y, 0, stream);
+  SPN_CATCH
 }
 
 spn_status spn_fwht_f32_host(int64_t n, const float* x, int64_t batch, int64_t ld_x, float* y, int64_t ld_y,
-                             int32_t device) {
+                             int32_t device) { SPN_TRY
   if (spn_status s = fwht_args(n, x, batch, ld_x, y, ld_y)) return s;
   if (batch == 0) return SPN_OK;
   if (n == 1) {
@@ -897,10 +1135,11 @@ spn_status spn_fwht_f32_host(int64_t n, const float* x, int64_t batch, int64_t l
   spn_plan* p = fwht_plan(n, device, &st);
   if (!p) return st;
   return spn_apply_f32_host(p, x, batch, ld_x, n, y, ld_y, 0);
+  SPN_CATCH
 }
 
 spn_status spn_diag_f32(int64_t n, const float* d, const float* x, int64_t batch, int64_t ld_x, float* y,
-                        int64_t ld_y, void* stream) {
+                        int64_t ld_y, void* stream) { SPN_TRY
   if (n < 1 || batch < 0 || ld_x < n || ld_y < n) return fail(SPN_EDIM, "diag_matvec: length mismatch");
   if (batch == 0) return SPN_OK;
   if (!d || !x || !y) return fail(SPN_EINVAL, "null pointer");
@@ -913,10 +1152,11 @@ spn_status spn_diag_f32(int64_t n, const float* d, const float* x, int64_t batch
                                                                                                   y, ld_y);
   SPN_CUDA(cudaGetLastError());
   return SPN_OK;
+  SPN_CATCH
 }
 
 spn_status spn_diag_f32_host(int64_t n, const float* d, const float* x, int64_t batch, int64_t ld_x, float* y,
-                             int64_t ld_y, int32_t device) {
+                             int64_t ld_y, int32_t device) { SPN_TRY
   if (n < 1 || batch < 0 || ld_x < n || ld_y < n) return fail(SPN_EDIM, "diag_matvec: length mismatch");
   if (batch == 0) return SPN_OK;
   if (!d || !x || !y) return fail(SPN_EINVAL, "null pointer");
@@ -935,6 +1175,7 @@ spn_status spn_diag_f32_host(int64_t n, const float* d, const float* x, int64_t 
   cudaFree(dd);
   cudaFree(dx);
   return st;
+  SPN_CATCH
 }
 
 }  // extern "C"
@@ -959,7 +1200,7 @@ __global__ void check_rows_kernel(const float* __restrict__ x, int64_t batch, in
 }  // namespace
 
 extern "C" spn_status spn_check_rows_f32(const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
-                                         int32_t* flags, void* stream) {
+                                         int32_t* flags, void* stream) { SPN_TRY
   if (batch < 0 || n_in < 1 || ld_x < n_in) return fail(SPN_EINVAL, "bad shape");
   if (batch == 0) return SPN_OK;
   if (!x || !flags) return fail(SPN_EINVAL, "null pointer");
@@ -968,4 +1209,5 @@ extern "C" spn_status spn_check_rows_f32(const float* x, int64_t batch, int64_t 
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "check_rows_kernel");
   return SPN_OK;
+  SPN_CATCH
 }

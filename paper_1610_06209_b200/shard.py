@@ -63,6 +63,15 @@ class PeerCodes:
         torch.cuda.synchronize(device)  # the fill must land before any peer can write into the table
         handles = [None] * world
         if world > 1:
+            # P2P capability first: every peer table must be directly addressable from this GPU
+            # (NVLink / NVSwitch peer access); otherwise the caller falls back to NCCL all-gather
+            devs = [None] * world
+            dist.all_gather_object(devs, device)
+            for r, dev in enumerate(devs):
+                if r == rank or dev == device:
+                    continue
+                if not torch.cuda.can_device_access_peer(device, dev):
+                    raise RuntimeError(f"no peer access from cuda:{device} to rank {r}'s cuda:{dev}")
             dist.all_gather_object(handles, reduce_tensor(self.table))
         peers = []
         for r in range(world):
@@ -80,8 +89,12 @@ class PeerCodes:
         import torch.distributed as dist
         from . import _check, _hash_peers, _stream_ptr
         x, _ = hasher.plan._device_in(x_local)
+        if hasher.plan.tables != self.tables:
+            raise ValueError(f"hasher has {hasher.plan.tables} tables, the gathered table {self.tables}")
+        if row0 < 0 or row0 + x.shape[0] > self.total:
+            raise ValueError(f"rows [{row0}, {row0 + x.shape[0]}) outside the gathered table of {self.total} rows")
         _check(_hash_peers(hasher.plan._h, x.data_ptr(), x.shape[0], x.stride(0), x.shape[1],
-                           self.ptrs.data_ptr(), self.world, row0, _stream_ptr(stream)))
+                           self.ptrs.data_ptr(), self.world, row0, self.total, _stream_ptr(stream)))
         torch.cuda.synchronize(x.device)
         if self.world > 1:
             dist.barrier()  # every rank's stores into this table are complete

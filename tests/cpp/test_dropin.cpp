@@ -240,6 +240,101 @@ int main() {
     CHECK(throws<DomainError>([] { KernelKind::gaussian(0.0); }));
   });
 
+  test_case("SketchOperator::apply(MatrixXd) value semantics, single and multi-block (newton_sketch.cpp:74-101)", [] {
+    // {input_dim, rows}: rows <= padded (one block) and rows > padded (ceil(rows / padded) blocks)
+    const std::size_t shapes[3][2] = {{200, 64}, {100, 300}, {1000, 2500}};
+    for (const auto& sh : shapes) {
+      const std::size_t in = sh[0], rows = sh[1], d = 7;
+      std::size_t N = 1;
+      while (N < in) N <<= 1;
+      const std::size_t blocks = (rows + N - 1) / N, m = std::min(rows, N);
+      MatrixXd A(static_cast<std::ptrdiff_t>(in), static_cast<std::ptrdiff_t>(d));
+      Vec64 cols = random_vec(in * d, 41 + in);
+      std::vector<float> af(in * d);
+      for (std::size_t i = 0; i < in; ++i)
+        for (std::size_t c = 0; c < d; ++c) {
+          A(i, c) = static_cast<double>(static_cast<float>(cols[i * d + c]));
+          af[i * d + c] = static_cast<float>(A(i, c));
+        }
+      SketchOperator sk(SpinnerVariant::hd3_hd2_hd1, in, rows, 55);
+      MatrixXd S = sk.apply(A);
+      CHECK(S.rows() == static_cast<std::ptrdiff_t>(rows) && S.cols() == static_cast<std::ptrdiff_t>(d));
+      std::vector<double> d1(blocks * N), d2(blocks * N), d3(blocks * N);
+      orc_realize_stacked(0, N, m, rows, 55, d1.data(), d2.data(), d3.data());
+      double err = 0, nrm = 0;
+      for (std::size_t b = 0; b < blocks; ++b) {
+        const std::size_t mb = std::min(m, rows - b * m);
+        std::vector<double> want(mb * d);
+        orc_sketch(N, std::sqrt(double(N)), 1.0 / std::sqrt(double(rows)), d1.data() + b * N, d2.data() + b * N,
+                   d3.data() + b * N, af.data(), in, d, d, nullptr, mb, want.data());
+        for (std::size_t r = 0; r < mb; ++r)
+          for (std::size_t c = 0; c < d; ++c) {
+            const double e = S(b * m + r, c) - want[r * d + c];
+            err += e * e;
+            nrm += want[r * d + c] * want[r * d + c];
+          }
+      }
+      CHECK(std::sqrt(err / nrm) < 1e-5);
+      CHECK(throws<DimensionError>([&] { sk.apply(MatrixXd(static_cast<std::ptrdiff_t>(in + 1), 2)); }));
+    }
+    MatrixXd A(5, 2);
+    CHECK(SketchOperator().apply(A).rows() == 5);  // exact operator: identity
+  });
+
+  test_case("hash_project_batch: ids and y of the same rows (BASELINE config 1)", [] {
+    const std::size_t n = 1024, batch = 300;
+    auto sp = StackedSpinner(SpinnerVariant::hd3_hd2_hd1, n, n, n, 42, 1.0);
+    CrossPolytopeHasher h(sp);
+    Vec64 xv = random_vec(n * batch, 7);
+    std::vector<float> x(xv.begin(), xv.end()), y(n * batch);
+    std::vector<int32_t> ids(batch), ids2(batch);
+    h.hash_project_batch(x.data(), batch, n, n, ids.data(), y.data(), n);
+    h.hash_batch(x.data(), batch, n, n, ids2.data());
+    CHECK(ids == ids2);
+    std::vector<double> d1(n), d2(n), d3(n), want(n * batch);
+    orc_realize_stacked(0, n, n, n, 42, d1.data(), d2.data(), d3.data());
+    orc_batch_apply(n, n, n, 1.0, d1.data(), d2.data(), d3.data(), x.data(), batch, n, n, 0, want.data());
+    double worst = 0;
+    for (std::size_t b = 0; b < batch; ++b) {
+      double e = 0, w = 0;
+      for (std::size_t i = 0; i < n; ++i) {
+        e += (y[b * n + i] - want[b * n + i]) * (y[b * n + i] - want[b * n + i]);
+        w += want[b * n + i] * want[b * n + i];
+      }
+      worst = std::max(worst, std::sqrt(e / w));
+    }
+    CHECK(worst < 1e-5);
+  });
+
+  test_case("resample_last_block / resample_tail / with_tail_vector (spinner.cpp:153-184)", [] {
+    const std::size_t n = 32, m = 32;
+    auto sp = StructuredSpinner::build(SpinnerSpec::make(SpinnerVariant::hd3_hd2_hd1, n, m, 19));
+    auto r0 = sp.resample_last_block(5);
+    CHECK(r0.d1() == sp.d1() && r0.d2() == sp.d2());
+    Vec64 t(n);
+    orc_rng_fill(orc_mix_seed(5, 2), 3, static_cast<int64_t>(n), t.data());  // Rng(mix_seed(s, 2)).rademacher()
+    CHECK(r0.d3() == t);
+    auto r1 = sp.resample_tail(6);
+    Vec64 u(2 * n);
+    orc_rng_fill(orc_mix_seed(6, 3), 3, static_cast<int64_t>(2 * n), u.data());  // D2 then D3 from one stream
+    CHECK(r1.d1() == sp.d1() && r1.d2() == Vec64(u.begin(), u.begin() + n) && r1.d3() == Vec64(u.begin() + n, u.end()));
+    Vec64 g = random_vec(n, 3);
+    auto r2 = sp.with_tail_vector(g);
+    CHECK(r2.d3() == g && r2.d1() == sp.d1());
+    Vec64 x = random_vec(n, 4), want(n);
+    orc_block_apply(n, m, std::sqrt(double(n)), r2.d1().data(), r2.d2().data(), g.data(), x.data(), want.data());
+    double e = 0, w = 0;
+    Vec64 got = r2.apply(x);
+    for (std::size_t i = 0; i < n; ++i) {
+      e += (got[i] - want[i]) * (got[i] - want[i]);
+      w += want[i] * want[i];
+    }
+    CHECK(std::sqrt(e / w) < 1e-5);
+    CHECK(throws<DimensionError>([&] { sp.with_tail_vector(Vec64(n - 1, 1.0)); }));
+    auto dense = StructuredSpinner::build(SpinnerSpec::make(SpinnerVariant::gaussian_dense, 8, 4, 1));
+    CHECK(throws<DomainError>([&] { dense.with_tail_vector(Vec64(8, 1.0)); }));
+  });
+
   test_case("sampler: distinct sorted indices", [] {
     auto r = sample_rows(1000, 100, 5);
     bool ok = r.size() == 100;
