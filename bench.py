@@ -669,8 +669,9 @@ def cpu_reference(config, budget_s=10.0, threads=None):
         fn = lambda c: r.chain(d[0], d[1], d[2], 1.0, x[:c], relu=True, threads=threads)  # noqa: E731
         total = cfg["batch"]
         what = "fwht_normalized/diag_matvec chain + ReLU, Gaussian D's"
-    if x.shape[0] < total:  # fewer distinct rows than the batch: process them cyclically
-        rows, base = x.shape[0], fn
+    avail = a.shape[1] if config == "c4" else x.shape[0]
+    if avail < total:  # fewer distinct rows than the batch: process them cyclically
+        rows, base = avail, fn
         fn = lambda c: [base(min(rows, c - i)) for i in range(0, c, rows)]  # noqa: E731
     # size the sample: a probe of one row per thread, then up to `budget_s` of work
     probe = max(1, min(total, threads))
