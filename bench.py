@@ -544,6 +544,50 @@ def timed_steps(w, steps, warmup, world, clk):
     return [a.elapsed_time(b) for a, b in evs]
 
 
+def c1_steady_state(w, steps, peak):
+    """Config 1 back to back (SURVEY §7 hard part 7): the one-wave hash + y launch is latency-bound
+    when timed alone, so also report the throughput of many consecutive steps captured in one CUDA
+    graph, over 8 distinct input/output batch buffers (8 x 32 MB > 126 MB L2: every step streams
+    its 16 MB of x from HBM and its 16 MB of y back).  Not the headline number for c1 (that is the
+    cold single launch above); this is the sustained rate of a stream of config-1 batches."""
+    torch = w.torch
+    nb, reps = 8, 4
+    xs = [w.x.clone() for _ in range(nb)]
+    ys = [torch.empty_like(w.y) for _ in range(nb)]
+    ids = [None] * nb
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm (plan layouts, occupancy caches) before capture
+        for b in range(nb):
+            ids[b] = w.sp.plan.hash(xs[b], y_out=ys[b], stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(reps):
+            for b in range(nb):
+                w.sp.plan.hash(xs[b], y_out=ys[b], stream=s)
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rounds = max(3, steps // 4)
+    e0.record()
+    for _ in range(rounds):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = rounds * reps * nb
+    per_ms = ms / launches
+    ach = BYTES_PER_UNIT["c1"] * w.units / (per_ms / 1e3) / 1e9
+    # the graph's outputs equal a plain launch's (same kernel, same inputs)
+    ok = bool(torch.equal(ys[0], ys[1]) and torch.equal(ys[0], w.y))
+    return {"value": w.units / (per_ms / 1e3), "unit": UNIT, "ms_per_step": per_ms, "launches": launches,
+            "hbm": {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak},
+            "how": f"{reps} x {nb} distinct 32 MB batches per CUDA graph, {rounds} replays, CUDA events",
+            "outputs_match_single_launch": ok}
+
+
 def e2e_measure(w, steps, world):
     """The metric through the host-buffer C ABI: pinned host input in, host output back, both copies
     inside the timed region, every step."""
@@ -589,6 +633,8 @@ def measure_config(name, args, rank, world, local, clk):
     if w.exchange:
         res["exchange"] = w.exchange
     res.update(secondary_rooflines(name, CONFIGS[name], w.units, mean_ms, clocks))
+    if name == "c1":
+        res["steady_state"] = c1_steady_state(w, args.steps, peak)
     if not args.no_e2e and name in ("c1", "c2", "c3", "c4", "c5"):
         res["e2e"] = e2e_measure(w, 3 if name in ("c2", "c3", "c5") else max(3, min(args.steps, 10)), world)
     if rank == 0 and world == 1 and not args.no_check and name in ("c1", "c2", "c3", "c4", "c5"):

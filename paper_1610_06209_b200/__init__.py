@@ -1022,3 +1022,4 @@ from .collision import (CollisionCurve, FamilyComparison, HashedPair, collision_
                         compare_families)
 from .newton import (LogisticProblem, NewtonTrace, SketchConfig, generate_ar1_problem, gradient,  # noqa: E402
                      hessian_sqrt, loss, sketched_step, solve)
+from . import wire  # noqa: E402,F401  (result-table wire format of the reference CLI)

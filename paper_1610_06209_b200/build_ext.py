@@ -69,7 +69,7 @@ def build(force: bool = False, verbose: bool = True, variant: str = "", defines:
     extra = tuple("-D" + d for d in defines)
     with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda f: _compile(f, objdir, extra, force), srcs))
-    cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs
+    cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcublas"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -13,6 +13,7 @@
 // natural), 1/N.  Twiddles come from an fp64-computed table (transforms.cpp:24-25 uses
 // the recurrence w *= wlen; the table is the exact e^{-2 pi i t / N} rounded once).
 // Dense baseline: a tiled fp32 GEMM Y = scale * X G^T per block, then the epilogue.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -171,55 +172,6 @@ __global__ void __launch_bounds__(kFT) family_kernel(const FamParams p) {
 }
 
 // ------------------------------------------------------------------ dense baseline
-// Y[v][b*m + i] = scale * sum_j G_b[i][j] x_v[j]   (64 x 64 output tiles, fp32 FMA)
-constexpr int kDT = 64, kDK = 16;
-
-__global__ void __launch_bounds__(256) dense_gemm_kernel(const float* __restrict__ X, int64_t ld_x, int64_t n_in,
-                                                         int64_t batch, const float* __restrict__ G, int64_t n,
-                                                         int64_t m, int64_t k, float scale, float* __restrict__ Y,
-                                                         int64_t ld_y) {
-  __shared__ float Xs[kDK][kDT + 1];
-  __shared__ float Gs[kDK][kDT + 1];
-  const int64_t v0 = (int64_t)blockIdx.x * kDT;
-  const int64_t c0 = (int64_t)blockIdx.y * kDT;  // output column (b*m + i) tile
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float acc[4][4] = {};
-  for (int64_t j0 = 0; j0 < n; j0 += kDK) {
-    for (int e = threadIdx.x; e < kDK * kDT; e += 256) {
-      const int r = e / kDK, jj = e - r * kDK;
-      const int64_t v = v0 + r, col = c0 + r, j = j0 + jj;
-      Xs[jj][r] = (v < batch && j < n && j < n_in) ? X[v * ld_x + j] : 0.0f;
-      float g = 0.0f;
-      if (col < k && j < n) {
-        const int64_t b = col / m, i = col - b * m;
-        g = G[(b * m + i) * n + j];
-      }
-      Gs[jj][r] = g;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int jj = 0; jj < kDK; ++jj) {
-      float xa[4], ga[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) xa[a] = Xs[jj][ty * 4 + a];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ga[q] = Gs[jj][tx * 4 + q];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[a][q] = fmaf(xa[a], ga[q], acc[a][q]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t v = v0 + ty * 4 + a, col = c0 + tx * 4 + q;
-      if (v < batch && col < k) Y[v * ld_y + col] = scale * acc[a][q];
-    }
-}
-
 // epilogues on Y rows: relu copy / signed argmax / gaussian or angular features
 __global__ void __launch_bounds__(256) dense_epilogue_kernel(const float* __restrict__ Y, int64_t ld_y, int64_t batch,
                                                              int64_t k, int op, int relu, float inv_sigma, float norm,
@@ -430,6 +382,42 @@ spn_status family_build(FamilyPlan** out, int variant, int64_t n, int64_t m, int
 
 void family_destroy(FamilyPlan* f) { delete f; }
 
+// One cuBLAS handle per (thread, device): handles are not safe to share across threads that set
+// different streams; created on first use and kept for the thread's lifetime.
+cublasHandle_t dense_handle(int device) {
+  struct Handles {
+    cublasHandle_t h[64] = {};
+    ~Handles() {
+      for (auto q : h)
+        if (q) cublasDestroy(q);
+    }
+  };
+  static thread_local Handles hs;
+  if (device < 0 || device >= 64) return nullptr;
+  if (!hs.h[device] && cublasCreate(&hs.h[device]) != CUBLAS_STATUS_SUCCESS) hs.h[device] = nullptr;
+  return hs.h[device];
+}
+
+spn_status dense_gemm(const FamilyPlan* f, const float* x, int64_t ld_x, int64_t n_in, int64_t batch,
+                      const float* G, float* Y, int64_t ld_y, cudaStream_t s) {
+  cublasHandle_t h = dense_handle(f->device);
+  if (!h) return set_error(SPN_ECUDA, "dense baseline: cublasCreate failed");
+  if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return set_error(SPN_ECUDA, "dense baseline: cublasSetStream");
+  const float alpha = static_cast<float>(f->scale), beta = 0.0f;
+  auto gemm = [&](cublasComputeType_t ct) {
+    return cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(f->k), static_cast<int>(batch),
+                        static_cast<int>(n_in), &alpha, G, CUDA_R_32F, static_cast<int>(f->n), x, CUDA_R_32F,
+                        static_cast<int>(ld_x), &beta, Y, CUDA_R_32F, static_cast<int>(ld_y), ct, CUBLAS_GEMM_DEFAULT);
+  };
+  // shapes / strides the emulated path does not take (e.g. unaligned leading dimensions) run as a
+  // plain fp32 cuBLAS GEMM — same result accuracy
+  cublasStatus_t st = gemm(CUBLAS_COMPUTE_32F_EMULATED_16BFX9);
+  if (st == CUBLAS_STATUS_NOT_SUPPORTED) st = gemm(CUBLAS_COMPUTE_32F);
+  if (st != CUBLAS_STATUS_SUCCESS)
+    return set_error(SPN_ECUDA, std::string("dense baseline: cublasGemmEx status ") + std::to_string(static_cast<int>(st)));
+  return SPN_OK;
+}
+
 spn_status family_run(const FamilyPlan* f, int op, const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
                       void* out, int64_t ld_out, int relu, double sigma, cudaStream_t s) {
   if (batch == 0) return SPN_OK;
@@ -446,9 +434,12 @@ spn_status family_run(const FamilyPlan* f, int op, const float* x, int64_t batch
     for (int t = 0; t < passes; ++t) {
       float* dst = direct ? static_cast<float*>(out) : Y;
       const int64_t ld = direct ? ld_out : f->k;
-      const dim3 grid(static_cast<unsigned>((batch + kDT - 1) / kDT), static_cast<unsigned>((f->k + kDT - 1) / kDT));
-      dense_gemm_kernel<<<grid, 256, 0, s>>>(x, ld_x, n_in, batch, f->dense + t * f->blocks * f->m * f->n, f->n, f->m,
-                                              f->k, static_cast<float>(f->scale), dst, ld);
+      // Y = scale * X G^T on the tensor cores: cuBLAS's fp32 GEMM emulated with BF16x9 products
+      // (CUBLAS_COMPUTE_32F_EMULATED_16BFX9, sm_100: fp32-accurate on tcgen05).  Column-major view:
+      // Y^T (k x batch, ld) = G (n x k, lda = n)^T * X^T (n_in x batch, ld_x); G's columns >= n_in
+      // meet the zero padding of x and are skipped.
+      if (spn_status st = dense_gemm(f, x, ld_x, n_in, batch, f->dense + t * f->blocks * f->m * f->n, dst, ld, s))
+        return st;
       if (!direct) {
         const int64_t g = std::min<int64_t>(batch, int64_t(f->sms) * 8);
         dense_epilogue_kernel<<<static_cast<unsigned>(g), 256, 0, s>>>(Y, f->k, batch, f->k, op, relu, inv_sigma,

@@ -73,6 +73,8 @@ struct ColParams {
   float cscale;
   int64_t rows_valid;    // EPI_Y: flat elements < rows_valid are stored
   int relu;
+  int discard_src;       // EPI_GATHER over a dead workspace: drop each source row's L2 line after the
+                         // tile is read (discard.global.L2: no write-back of the workspace to HBM)
   int pdl;               // launch with programmatic dependent launch (vector path: c5 1.366 -> 1.323 ms;
                          // the sketch path measured slightly slower with it, so it stays off there)
   // filled by set_tiling(): fast division by nstripes, log2 of nlo / nhi (powers of two)
@@ -1151,6 +1153,7 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     pb.dd[0] = nullptr;
     pb.dd[1] = nullptr;
     pb.rowmap = bp->rowmap;
+    pb.discard_src = 1;  // W is dead after this pass
     pb.dst = out + c0;
     e = lcol(lsb, CP_LAST, pb);
     if (e != cudaSuccess) return BigPlan::err(e, "sketch P4");

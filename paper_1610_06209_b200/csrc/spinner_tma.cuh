@@ -190,6 +190,14 @@ __global__ void __launch_bounds__(SColCfg<LS>::THREADS, TmaCfg<LS>::MIN_CTAS)
 #pragma unroll
       for (int j = 0; j < C::R; ++j) r[j] = buf[scol_s<C>(LB, w, j) * 32 + lane];
     }
+    if constexpr (EPI == EPI_GATHER) {
+      if (p.discard_src) {  // this row of the workspace is dead now: no write-back to HBM
+        const int64_t e = cti.e0 + ((int64_t)threadIdx.x << p.s0);
+        const int64_t off = e * p.src_ld + (int64_t)cti.cs * 32;
+        if (off + 32 <= p.src_valid)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(p.src + (int64_t)cti.v * p.src_vstride + off) : "memory");
+      }
+    }
     bulk_wait_read();  // my bulk stores out of the buffer about to be refilled have read it
     __syncthreads();   // buf free for the transposes; the previous tile's buffer free for a load
     const uint32_t nxt = tile + (NB - 1) * gridDim.x;

@@ -53,6 +53,7 @@ struct VecParams {
   int32_t* const* peers;
   int npeers;
   int64_t peer_row0;
+  int vec_major;       // OP_HASH: all tables of a vector in one CTA, back to back (see the kernel)
 };
 
 #ifndef SPN_EMBED_WARPS
@@ -748,11 +749,22 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
     cp_async_commit();
   }
 
-  for (int64_t base = (int64_t)blockIdx.x * C::GPC; base < total; base += stride) {
-    const int64_t item = base + g;
-    const bool active = item < total;
-    const int64_t v = active ? item / per_vec : 0;
-    const int64_t tab = active ? item - v * per_vec : 0;
+  // Work order.  Item-major (default): item = (vector, table) pairs dealt round robin over the
+  // grid.  Vector-major (multi-table hash with at least one vector per CTA slot, p.vec_major): a
+  // CTA takes a vector and runs all its tables back to back, so the vector is read from HBM once
+  // and from L2 for the other tables (item-major lets CTAs drift apart over a 2^20-vector batch
+  // and re-read x from HBM: 2.4x the algorithmic bytes at config 3).
+  const bool vmaj = OP == OP_HASH && p.vec_major;
+  const int64_t units = vmaj ? (p.batch + C::GPC - 1) / C::GPC : (total + C::GPC - 1) / C::GPC;
+  int64_t sub = 0;
+  for (int64_t u = blockIdx.x; u < units;
+       vmaj ? (++sub == per_vec ? (sub = 0, u += gridDim.x) : u) : (u += gridDim.x)) {
+    const int64_t base = u * C::GPC;
+    const int64_t vg = base + g;  // vector-major: this group's vector
+    const int64_t item = vmaj ? vg * per_vec + sub : base + g;
+    const bool active = vmaj ? vg < p.batch : item < total;
+    const int64_t v = active ? (vmaj ? vg : item / per_vec) : 0;
+    const int64_t tab = active ? (vmaj ? sub : item - v * per_vec) : 0;
     const float* xrow = p.x + v * p.ld_x;
 
     float r[C::R];

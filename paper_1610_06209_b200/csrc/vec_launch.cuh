@@ -42,9 +42,15 @@ cudaError_t launch_vec(const VecParams& p, cudaStream_t s, int sms, int64_t item
     if (occ < 1) occ = 1;
     occ_cache.store(occ);
   }
-  const int64_t ctas = (items + C::GPC - 1) / C::GPC;
+  int64_t ctas = (items + C::GPC - 1) / C::GPC;
+  VecParams q = p;
+  // multi-table hash over a batch that fills the persistent grid by vectors alone: vector-major
+  // order (every table of a vector in one CTA, back to back; the vector stays in L2)
+  const int64_t vslots = (p.batch + C::GPC - 1) / C::GPC;
+  q.vec_major = OP == OP_HASH && p.tables > 1 && vslots >= int64_t(sms) * occ;
+  if (q.vec_major) ctas = vslots;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ctas, int64_t(sms) * occ));
-  kern<<<static_cast<unsigned>(grid), C::THREADS, C::smem_bytes(OP), s>>>(p);
+  kern<<<static_cast<unsigned>(grid), C::THREADS, C::smem_bytes(OP), s>>>(q);
   return cudaGetLastError();
 }
 
