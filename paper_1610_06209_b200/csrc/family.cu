@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstring>
 #include <vector>
 
 #include "../../include/spinners_b200.h"
@@ -271,13 +272,31 @@ struct FamilyPlan {
   int64_t n = 0, m = 0, k = 0, tables = 0, blocks = 0;
   int N = 0, logN = 0;
   double scale = 1.0;
-  float *d1 = nullptr, *d2 = nullptr, *dense = nullptr;
+  float *d1 = nullptr, *d2 = nullptr, *dense = nullptr, *dense_lo = nullptr;  // dense: G = hi + lo (TF32 split)
   double2 *spec = nullptr, *tw = nullptr, *skw = nullptr;
   ~FamilyPlan() {
-    for (void* q : {(void*)d1, (void*)d2, (void*)dense, (void*)spec, (void*)tw, (void*)skw})
+    for (void* q : {(void*)d1, (void*)d2, (void*)dense, (void*)dense_lo, (void*)spec, (void*)tw, (void*)skw})
       if (q) cudaFree(q);
   }
 };
+
+// round an fp32 value to the nearest TF32 value (10 explicit mantissa bits), as an fp32
+__host__ __device__ inline float tf32_round(float v) {
+#ifdef __CUDA_ARCH__
+  uint32_t u = __float_as_uint(v);
+#else
+  uint32_t u;
+  std::memcpy(&u, &v, 4);
+#endif
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x0fffu + ((u >> 13) & 1u)) & 0xffffe000u;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(u);
+#else
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+#endif
+}
 
 bool family_variant(int v) { return v >= SPN_GCIRC_D2_HD1 && v <= SPN_GAUSSIAN_DENSE; }
 
@@ -322,8 +341,15 @@ spn_status family_build(FamilyPlan** out, int variant, int64_t n, int64_t m, int
   cudaError_t e = cudaSuccess;
   const int64_t tb = tables * blocks;
   if (variant == SPN_GAUSSIAN_DENSE) {
-    std::vector<float> g(dense.begin(), dense.end());
-    e = upload(g, &f->dense);
+    // G (fp32) = hi + lo with hi exactly representable in TF32 (3xTF32 GEMM, dense_gemm)
+    std::vector<float> hi(dense.size()), lo(dense.size());
+    for (size_t i = 0; i < dense.size(); ++i) {
+      const float g = static_cast<float>(dense[i]);
+      hi[i] = tf32_round(g);
+      lo[i] = g - hi[i];
+    }
+    e = upload(hi, &f->dense);
+    if (e == cudaSuccess) e = upload(lo, &f->dense_lo);
   } else {
     int lg = 0;
     while ((int64_t(1) << lg) < n) ++lg;
@@ -398,24 +424,52 @@ cublasHandle_t dense_handle(int device) {
   return hs.h[device];
 }
 
-spn_status dense_gemm(const FamilyPlan* f, const float* x, int64_t ld_x, int64_t n_in, int64_t batch,
-                      const float* G, float* Y, int64_t ld_y, cudaStream_t s) {
+// x = hi + lo per element, hi exactly representable in TF32 (round to nearest on the 13 dropped bits)
+__global__ void tf32_split_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_in, int64_t batch,
+                                  float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t total = n_in * batch;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / n_in, j = i - b * n_in;
+    const float v = x[b * ld_x + j];
+    const float h = tf32_round(v);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+
+// Y = scale * X G^T as a 3xTF32 product on the tensor cores: X G^T ~ Xhi Ghi^T + Xlo Ghi^T + Xhi Glo^T
+// (the dropped Xlo Glo^T term is ~2^-22 relative), each a cuBLAS TF32 GEMM accumulating in fp32 —
+// fp32-class accuracy (the 1e-5 bar) at tensor-core rate.  Column-major view: Y^T (k x batch, ld) =
+// G (n x k, lda = n)^T * X^T (n_in x batch); G's columns >= n_in meet x's zero padding.
+spn_status dense_gemm(const FamilyPlan* f, const float* x, int64_t ld_x, int64_t n_in, int64_t batch, int64_t goff,
+                      float* Y, int64_t ld_y, cudaStream_t s) {
   cublasHandle_t h = dense_handle(f->device);
   if (!h) return set_error(SPN_ECUDA, "dense baseline: cublasCreate failed");
   if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return set_error(SPN_ECUDA, "dense baseline: cublasSetStream");
-  const float alpha = static_cast<float>(f->scale), beta = 0.0f;
-  auto gemm = [&](cublasComputeType_t ct) {
+  float* xs = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&xs), sizeof(float) * static_cast<size_t>(2 * n_in * batch), s);
+  if (e != cudaSuccess) return cuda_error(e, "dense scratch");
+  float* xhi = xs;
+  float* xlo = xs + n_in * batch;
+  const int64_t blocks = std::min<int64_t>((n_in * batch + 255) / 256, int64_t(f->sms) * 8);
+  tf32_split_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(x, ld_x, n_in, batch, xhi, xlo);
+  const float alpha = static_cast<float>(f->scale), zero = 0.0f, one = 1.0f;
+  const float* ghi = f->dense + goff;
+  const float* glo = f->dense_lo + goff;
+  auto gemm = [&](const float* g, const float* xx, const float* beta) {
     return cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(f->k), static_cast<int>(batch),
-                        static_cast<int>(n_in), &alpha, G, CUDA_R_32F, static_cast<int>(f->n), x, CUDA_R_32F,
-                        static_cast<int>(ld_x), &beta, Y, CUDA_R_32F, static_cast<int>(ld_y), ct, CUBLAS_GEMM_DEFAULT);
+                        static_cast<int>(n_in), &alpha, g, CUDA_R_32F, static_cast<int>(f->n), xx, CUDA_R_32F,
+                        static_cast<int>(n_in), beta, Y, CUDA_R_32F, static_cast<int>(ld_y),
+                        CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT);
   };
-  // shapes / strides the emulated path does not take (e.g. unaligned leading dimensions) run as a
-  // plain fp32 cuBLAS GEMM — same result accuracy
-  cublasStatus_t st = gemm(CUBLAS_COMPUTE_32F_EMULATED_16BFX9);
-  if (st == CUBLAS_STATUS_NOT_SUPPORTED) st = gemm(CUBLAS_COMPUTE_32F);
+  cublasStatus_t st = gemm(ghi, xlo, &zero);  // small terms first
+  if (st == CUBLAS_STATUS_SUCCESS) st = gemm(glo, xhi, &one);
+  if (st == CUBLAS_STATUS_SUCCESS) st = gemm(ghi, xhi, &one);
+  cudaFreeAsync(xs, s);
   if (st != CUBLAS_STATUS_SUCCESS)
     return set_error(SPN_ECUDA, std::string("dense baseline: cublasGemmEx status ") + std::to_string(static_cast<int>(st)));
-  return SPN_OK;
+  e = cudaGetLastError();
+  return e == cudaSuccess ? SPN_OK : cuda_error(e, "dense baseline split");
 }
 
 spn_status family_run(const FamilyPlan* f, int op, const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
@@ -434,12 +488,8 @@ spn_status family_run(const FamilyPlan* f, int op, const float* x, int64_t batch
     for (int t = 0; t < passes; ++t) {
       float* dst = direct ? static_cast<float*>(out) : Y;
       const int64_t ld = direct ? ld_out : f->k;
-      // Y = scale * X G^T on the tensor cores: cuBLAS's fp32 GEMM emulated with BF16x9 products
-      // (CUBLAS_COMPUTE_32F_EMULATED_16BFX9, sm_100: fp32-accurate on tcgen05).  Column-major view:
-      // Y^T (k x batch, ld) = G (n x k, lda = n)^T * X^T (n_in x batch, ld_x); G's columns >= n_in
-      // meet the zero padding of x and are skipped.
-      if (spn_status st = dense_gemm(f, x, ld_x, n_in, batch, f->dense + t * f->blocks * f->m * f->n, dst, ld, s))
-        return st;
+      // Y = scale * X G^T: 3xTF32 GEMMs on the tensor cores (dense_gemm)
+      if (spn_status st = dense_gemm(f, x, ld_x, n_in, batch, t * f->blocks * f->m * f->n, dst, ld, s)) return st;
       if (!direct) {
         const int64_t g = std::min<int64_t>(batch, int64_t(f->sms) * 8);
         dense_epilogue_kernel<<<static_cast<unsigned>(g), 256, 0, s>>>(Y, f->k, batch, f->k, op, relu, inv_sigma,

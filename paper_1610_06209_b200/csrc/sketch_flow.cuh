@@ -1,0 +1,388 @@
+// Dataflow sketch: the four strided column passes of a SketchOperator (newton_sketch.cpp:74-101),
+// S a = sqrt(N/m) P H D3 H D2 H D1 a for every column a of a row-major A[n_in][d], run as ONE
+// persistent kernel instead of 4 launches per column group.
+//
+// The transform splits the N = 2^(lsa+lsb) index bits into a low half (lsa bits, contiguous rows)
+// and a high half (lsb bits), and regroups H D3 H D2 H D1 into four passes (spinner_big.cuh):
+//   P0 low  : D1, H(low)            A -> W       (A read from HBM once)
+//   P1 high : H(high), D2, H(high)  W -> W
+//   P2 low  : H(low), D3, H(low)    W -> W
+//   P3 high : H(high), gather P     W -> out     (W's lines discarded from L2: no write-back)
+// Work unit = one 64 KB task: a tile of 2^LSM rows x 32 columns (one 32-column "stripe"), or two
+// half-height tiles when a pass covers LSM-1 bits.  Tasks are numbered in waves of G stripes —
+// P0 of the wave's stripes, then P1, P2, P3 — and fetched by the CTAs in that order from a global
+// counter; a task of pass p waits (in the producer warp, before its loads) until every tile of pass
+// p-1 of its stripe has been stored, counted by per-(stripe, pass) completion counters.  So there
+// are no launch boundaries: the passes of different stripes overlap, nothing fills or drains per
+// pass, and every SM keeps NB-1 tile loads in flight (TMA, completing on mbarriers) while its
+// consumer warps transform the current tile and store it back with TMA.
+//
+// Progress: tasks are fetched in dependency order and every CTA consumes its tasks in fetch order,
+// so the earliest unfinished task never waits on a later one (no co-residency requirement).
+#pragma once
+
+#include <cstdlib>
+#include <cstring>
+
+#include "spinner_tma.cuh"
+
+namespace spn {
+
+struct FlowParams {
+  int nstripes, G;
+  uint32_t ntasks;
+  const float* d1;   // [N]
+  const float* d2t;  // [N], D2 transposed for the high pass: d2t[lo * 2^lsb + s] = D2[(s << lsa) + lo]
+  const float* d3;   // [N]
+  const int32_t* rowmap;  // [N]: output row of element e, or -1
+  float* w;               // workspace: [stripe][N][32]
+  int64_t wstride;        // N * 32
+  float* out;
+  int64_t ld_out;
+  float cscale;
+  uint32_t* ctr;  // [0]: next task; [1 + 4*s + p]: stored sub-tiles of (stripe s, pass p)
+};
+
+struct FlowMaps {
+  CUtensorMap a;    // A   : (col, 1, row, 1)            box {32, 1, 256, 1}
+  CUtensorMap wlo;  // W   : (col, 1, row, stripe)       low passes
+  CUtensorMap whi;  // W   : (col, lo, hs, stripe)       high passes (row = hs * 2^lsa + lo)
+};
+
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t cnt) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_n1() { asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); }
+// L2 eviction-priority policy for streamed-once data (A: read by P0 only), so it does not push the
+// stripes' live workspace out of L2
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tensor_load4_hint(float* sdst, const CUtensorMap* m, int c0, int c1, int c2, int c3,
+                                                  uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(sdst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+template <int LSA, int LSB>
+struct FlowCfg {
+  static constexpr int LSM = LSA > LSB ? LSA : LSB;
+  static constexpr int CTHREADS = 1 << LSM;      // consumers: one row of the task per thread
+  static constexpr int THREADS = CTHREADS + 64;  // + the loader warp + the storer warp
+  static constexpr size_t TILEB = sizeof(float) * (size_t(1) << LSM) * 32;
+  static constexpr size_t DSB = sizeof(float) * (size_t(1) << LSM);
+  static constexpr int NB = LSM >= 9 ? 3 : 4;  // buffers: NB-1 loads in flight
+  static constexpr size_t SMEM = NB * (TILEB + DSB) + NB * 24 + NB * 4 + 64;
+  static constexpr int NSUB_LO = 1 << (LSM - LSA), NSUB_HI = 1 << (LSM - LSB);
+  static constexpr int T_LO = (1 << LSB) / NSUB_LO;  // tasks per stripe, low pass
+  static constexpr int T_HI = (1 << LSA) / NSUB_HI;  // tasks per stripe, high pass
+};
+
+struct FlowTask {
+  int stripe, pass, idx;  // idx: task within (stripe, pass)
+};
+
+template <class F>
+__device__ __forceinline__ FlowTask flow_decode(uint32_t t, const FlowParams& p) {
+  const uint32_t per_stripe = 2 * F::T_LO + 2 * F::T_HI;
+  const uint32_t wave_tasks = (uint32_t)p.G * per_stripe;
+  const uint32_t wv = t / wave_tasks;
+  uint32_t r = t - wv * wave_tasks;
+  const int g = min(p.G, p.nstripes - (int)wv * p.G);
+  FlowTask k;
+  k.pass = 0;
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t n = (uint32_t)g * ((q & 1) ? F::T_HI : F::T_LO);
+    if (r < n) {
+      k.pass = q;
+      break;
+    }
+    r -= n;
+  }
+  const uint32_t tp = (k.pass & 1) ? F::T_HI : F::T_LO;
+  k.stripe = (int)wv * p.G + (int)(r / tp);
+  k.idx = (int)(r % tp);
+  return k;
+}
+
+// One sub-tile (2^LS rows x 32 columns, row-major in buf) through NPARTS H's over its LS bits,
+// D (2^LS floats in smem, one per row) before part 1 when DMASK bit 1 / part 0 when bit 0,
+// start layout B if START_B; the result goes back to buf (row-major) scaled by `scale`.
+template <int LS, int NPARTS, int DMASK, bool START_B>
+__device__ __forceinline__ void flow_tile(float* buf, const float* dsm, int w, int lane, int bar, float scale) {
+  using C = SColCfg<LS>;
+  float r[C::R];
+  constexpr bool LB = START_B && C::W > 1;
+#pragma unroll
+  for (int j = 0; j < C::R; ++j) r[j] = buf[scol_s<C>(LB, w, j) * 32 + lane];
+  named_bar(bar, C::THREADS);  // the tile is in registers: buf is free for the transposes
+#pragma unroll
+  for (int part = 0; part < NPARTS; ++part) {
+    const bool lay_b = C::W > 1 && (START_B ^ ((part & 1) != 0));
+    if ((DMASK >> part) & 1) {  // every D of the sketch passes is applied in layout A (s = w*R + j)
+      const float4* dv4 = reinterpret_cast<const float4*>(dsm + w * C::R);
+#pragma unroll
+      for (int q = 0; q < C::R / 4; ++q) {
+        const float4 dv = dv4[q];
+        r[4 * q] *= dv.x;
+        r[4 * q + 1] *= dv.y;
+        r[4 * q + 2] *= dv.z;
+        r[4 * q + 3] *= dv.w;
+      }
+    }
+    reg_fwht<C::R, 0, C::LR>(r);
+    if constexpr (C::W > 1) {
+#pragma unroll
+      for (int j = 0; j < C::R; ++j) buf[scol_s<C>(lay_b, w, j) * 32 + lane] = r[j];
+      named_bar(bar, C::THREADS);
+#pragma unroll
+      for (int j = 0; j < C::R; ++j) r[j] = buf[scol_s<C>(!lay_b, w, j) * 32 + lane];
+      named_bar(bar, C::THREADS);
+      if (!lay_b)
+        reg_fwht<C::R, C::LR - C::LW, C::LR>(r);
+      else
+        reg_fwht<C::R, 0, C::LW>(r);
+    }
+  }
+  constexpr bool END_B = C::W > 1 && (START_B ^ ((NPARTS & 1) != 0));
+#pragma unroll
+  for (int j = 0; j < C::R; ++j) buf[scol_s<C>(END_B, w, j) * 32 + lane] = r[j] * scale;
+  fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA store
+  named_bar(bar, C::THREADS);
+}
+
+// Roles: consumer warps (one row per thread) transform the tile in slot k; the loader warp
+// fetches tasks, waits on their dependencies and issues the TMA loads; the storer warp issues each
+// finished tile's TMA stores, frees the slot once the store has read it, and counts the tile for
+// its (stripe, pass) once the store is complete.  Loader and storer are separate warps so a loader
+// waiting on a dependency never holds up the stores that dependency is waiting for.
+template <int LSA, int LSB>
+__global__ void __launch_bounds__(FlowCfg<LSA, LSB>::THREADS, 1)
+    sketch_flow_kernel(const FlowParams p, const __grid_constant__ FlowMaps mp) {
+  using F = FlowCfg<LSA, LSB>;
+  constexpr int NB = F::NB;
+  extern __shared__ __align__(128) float smem[];
+  float* bufs = smem;                                                                   // NB x TILEB
+  float* dsl = smem + NB * (F::TILEB / 4);                                              // NB x DSB
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NB * ((F::TILEB + F::DSB) / 4));  // NB: loaded
+  uint64_t* ready = full + NB;                                                          // NB: computed
+  uint64_t* empty = ready + NB;                                                         // NB: stored (read)
+  int* tslot = reinterpret_cast<int*>(empty + NB);                                      // NB task ids
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&ready[b], 1);
+      mbar_init(&empty[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (tid == F::CTHREADS) {  // ---------------------------------------------- loader
+    const uint64_t pol_a = policy_evict_first();
+    for (uint32_t k = 0;; ++k) {
+      const int slot = (int)(k % NB);
+      if (k >= (uint32_t)NB) mbar_wait(&empty[slot], ((k / NB) - 1) & 1u);
+      const uint32_t t = atomicAdd(p.ctr, 1u);
+      if (t >= p.ntasks) {
+        tslot[slot] = -1;
+        mbar_arrive(&full[slot]);
+        return;
+      }
+      const FlowTask tk = flow_decode<F>(t, p);
+      if (tk.pass > 0) {  // every tile of the previous pass of this stripe is stored
+        const uint32_t need = (tk.pass & 1) ? (1u << LSB) : (1u << LSA);  // sub-tiles of pass - 1
+        const uint32_t* c = p.ctr + 1 + 4 * tk.stripe + (tk.pass - 1);
+        while (ld_acquire(c) < need) __nanosleep(100);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      tslot[slot] = (int)t;
+      float* buf = bufs + slot * (F::TILEB / 4);
+      float* ds = dsl + slot * (F::DSB / 4);
+      const bool low = (tk.pass & 1) == 0;
+      const int LS = low ? LSA : LSB;
+      const int nsub = low ? F::NSUB_LO : F::NSUB_HI;
+      const int box = LS > 8 ? 256 : (1 << LS), nbox = (1 << LS) / box;
+      const float* dsrc = tk.pass == 0 ? p.d1 : (tk.pass == 1 ? p.d2t : (tk.pass == 2 ? p.d3 : nullptr));
+      const uint32_t bytes = (uint32_t)F::TILEB + (dsrc ? (uint32_t)nsub * (4u << LS) : 0u);
+      mbar_arrive_tx(&full[slot], bytes);
+      for (int sb = 0; sb < nsub; ++sb) {
+        const int ti = tk.idx * nsub + sb;  // low: hi index, high: lo index
+        float* sbuf = buf + sb * ((1 << LS) * 32);
+        for (int b = 0; b < nbox; ++b) {
+          if (tk.pass == 0)
+            tensor_load4_hint(sbuf + b * box * 32, &mp.a, tk.stripe * 32, 0, (ti << LSA) + b * box, 0, &full[slot],
+                              pol_a);
+          else if (low)
+            tensor_load4(sbuf + b * box * 32, &mp.wlo, 0, 0, (ti << LSA) + b * box, tk.stripe, &full[slot]);
+          else
+            tensor_load4(sbuf + b * box * 32, &mp.whi, 0, ti, b * box, tk.stripe, &full[slot]);
+        }
+        if (dsrc) bulk_load(ds + sb * (1 << LS), dsrc + ((int64_t)ti << LS), 4u << LS, &full[slot]);
+      }
+    }
+  }
+  if (tid == F::CTHREADS + 32) {  // ------------------------------------------- storer
+    for (uint32_t k = 0;; ++k) {
+      const int slot = (int)(k % NB);
+      mbar_wait(&ready[slot], (k / NB) & 1u);
+      const int t = tslot[slot];
+      if (t < 0) break;
+      const FlowTask tk = flow_decode<F>((uint32_t)t, p);
+      if (tk.pass == 3) {  // gather: the consumers stored their rows and waited for the reads
+        mbar_arrive(&empty[slot]);
+        continue;
+      }
+      const bool low = (tk.pass & 1) == 0;
+      const int LS = low ? LSA : LSB;
+      const int nsub = low ? F::NSUB_LO : F::NSUB_HI;
+      const int box = LS > 8 ? 256 : (1 << LS), nbox = (1 << LS) / box;
+      float* buf = bufs + slot * (F::TILEB / 4);
+      for (int sb = 0; sb < nsub; ++sb) {
+        const int ti = tk.idx * nsub + sb;
+        float* sbuf = buf + sb * ((1 << LS) * 32);
+        for (int b = 0; b < nbox; ++b) {
+          if (low)
+            tensor_store4(&mp.wlo, 0, 0, (ti << LSA) + b * box, tk.stripe, sbuf + b * box * 32);
+          else
+            tensor_store4(&mp.whi, 0, ti, b * box, tk.stripe, sbuf + b * box * 32);
+        }
+      }
+      bulk_commit();
+      bulk_wait_read();  // the store has read the tile: the slot may be refilled
+      mbar_arrive(&empty[slot]);
+      bulk_wait_all();   // ... and is complete: count its sub-tiles for the dependent pass
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      red_release_add(p.ctr + 1 + 4 * tk.stripe + tk.pass, (uint32_t)nsub);
+    }
+    return;
+  }
+  if (tid >= F::CTHREADS) return;
+
+  // ---------------------------------------------------------------------- consumers
+  for (uint32_t k = 0;; ++k) {
+    const int slot = (int)(k % NB);
+    mbar_wait(&full[slot], (k / NB) & 1u);
+    const int t = tslot[slot];
+    if (t < 0) {
+      if (tid == 0) mbar_arrive(&ready[slot]);  // lets the storer see the end
+      break;
+    }
+    const FlowTask tk = flow_decode<F>((uint32_t)t, p);
+    float* buf = bufs + slot * (F::TILEB / 4);
+    const float* ds = dsl + slot * (F::DSB / 4);
+    const bool low = (tk.pass & 1) == 0;
+    const int LS = low ? LSA : LSB;
+    const int sub = tid >> LS, ltid = tid & ((1 << LS) - 1);
+    const int w = ltid >> 5, lane = ltid & 31;
+    const int ti = tk.idx * (low ? F::NSUB_LO : F::NSUB_HI) + sub;
+    float* sbuf = buf + sub * ((1 << LS) * 32);
+    const float* sds = ds + sub * (1 << LS);
+    const int bar = 1 + sub;
+    switch (tk.pass) {  // P0: D1 H | P1: H D2 H (start B) | P2: H D3 H (start B) | P3: H + gather
+      case 0: flow_tile<LSA, 1, 1, false>(sbuf, sds, w, lane, bar, 1.0f); break;
+      case 1: flow_tile<LSB, 2, 2, true>(sbuf, sds, w, lane, bar, 1.0f); break;
+      case 2: flow_tile<LSA, 2, 2, true>(sbuf, sds, w, lane, bar, 1.0f); break;
+      default: flow_tile<LSB, 1, 0, false>(sbuf, sds, w, lane, bar, p.cscale); break;
+    }
+    if (tk.pass == 3) {  // gather this tile's sampled rows: out[rowmap[e]][stripe*32 + c]
+      const int64_t e = (int64_t)ti + ((int64_t)ltid << LSA);
+      const int32_t orow = __ldg(p.rowmap + e);
+      if (orow >= 0) bulk_store(p.out + (int64_t)orow * p.ld_out + tk.stripe * 32, sbuf + ltid * 32, 128);
+      bulk_commit();
+      // W's row is dead after this pass: drop it from L2 without a write-back
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(p.w + tk.stripe * p.wstride + e * 32) : "memory");
+      bulk_wait_read();
+    }
+    named_bar(3, F::CTHREADS);  // the whole task is computed (and its gather stores have read smem)
+    if (tid == 0) mbar_arrive(&ready[slot]);
+  }
+  bulk_wait_all();
+}
+
+// ------------------------------------------------------------------------- host side
+inline int flow_mode();
+inline bool flow_enabled() { return flow_mode() != 0; }
+// stripes per wave (L2 working set = G x 16 MB at N = 2^17); config 4: G = 2 0.191 ms, 3 0.174 ms
+// (DRAM 157 MB = 1.15x algorithmic), 4 0.170 ms (290 MB: the workspace starts spilling from L2)
+inline int flow_waves_g() {
+  static const int g = [] {
+    const char* e = std::getenv("SPN_FLOW_G");
+    const int v = e ? std::atoi(e) : 3;
+    return v < 1 ? 1 : v;
+  }();
+  return g;
+}
+
+template <int LSA, int LSB>
+inline cudaError_t launch_flow_t(FlowParams fp, const float* a, int64_t n_in, int64_t dcols, int64_t ld_a, int sms,
+                                 cudaStream_t s, bool* done) {
+  using F = FlowCfg<LSA, LSB>;
+  *done = false;
+  const int64_t nn = int64_t(1) << (LSA + LSB);
+  FlowMaps mp;
+  std::memset(&mp, 0, sizeof(mp));
+  const int box_lo = LSA > 8 ? 256 : (1 << LSA), box_hi = LSB > 8 ? 256 : (1 << LSB);
+  if (!encode_view(&mp.a, a, dcols, ld_a, 0, n_in, 1, 0, box_lo)) return cudaSuccess;
+  if (!encode_view(&mp.wlo, fp.w, 32, 32, 0, nn, fp.nstripes, fp.wstride, box_lo)) return cudaSuccess;
+  if (!encode_view(&mp.whi, fp.w, 32, 32, LSA, int64_t(1) << LSB, fp.nstripes, fp.wstride, box_hi))
+    return cudaSuccess;
+  auto kern = sketch_flow_kernel<LSA, LSB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int occ = 1;
+  if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, F::THREADS, F::SMEM)) return e;
+  occ = occ < 1 ? 1 : occ;
+  fp.ntasks = (uint32_t)fp.nstripes * (2 * F::T_LO + 2 * F::T_HI);
+  const int64_t grid = std::min<int64_t>(int64_t(sms) * occ, fp.ntasks);
+  kern<<<(unsigned)grid, F::THREADS, F::SMEM, s>>>(fp, mp);
+  *done = true;
+  return cudaGetLastError();
+}
+
+// 1: the dataflow kernel (default), 0: grouped pass launches.  (A register-direct variant — tiles
+// moved global <-> registers with LDG/STG, smem only for transposes, the next tile prefetched into a
+// second register set — measured 0.286 vs 0.172 ms at config 4 and was dropped: at 128 registers
+// and one 512-thread CTA per SM the direct loads cannot keep enough bytes in flight.)
+inline int flow_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("SPN_FLOW");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+
+// lsa = ceil(L/2), lsb = floor(L/2) for N = 2^L, L in [10, 18] (both halves in [5, 9]).
+inline cudaError_t launch_flow(int lsa, int lsb, const FlowParams& fp, const float* a, int64_t n_in, int64_t dcols,
+                               int64_t ld_a, int sms, cudaStream_t s, bool* done) {
+  *done = false;
+#define SPN_FLOW_CASE(A, B) \
+  if (lsa == A && lsb == B) return launch_flow_t<A, B>(fp, a, n_in, dcols, ld_a, sms, s, done);
+  SPN_FLOW_CASE(5, 5) SPN_FLOW_CASE(6, 5) SPN_FLOW_CASE(6, 6) SPN_FLOW_CASE(7, 6) SPN_FLOW_CASE(7, 7)
+  SPN_FLOW_CASE(8, 7) SPN_FLOW_CASE(8, 8) SPN_FLOW_CASE(9, 8) SPN_FLOW_CASE(9, 9)
+#undef SPN_FLOW_CASE
+  return cudaSuccess;
+}
+
+}  // namespace spn

@@ -348,6 +348,7 @@ inline cudaError_t launch_row(const RowParams& p, int sms, cudaStream_t s) {
 }  // namespace spn
 #include "spinner_pass.cuh"
 #include "spinner_tma.cuh"
+#include "sketch_flow.cuh"
 namespace spn {
 
 // L2-resident working set per pass group: 24 MB for the vector passes (c5: 1.275 vs
@@ -1096,6 +1097,37 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     cudaError_t e = lcol(lsa, CP_SINGLE, cp);
     if (e == cudaSuccess) e = bp->note_use(s0);
     return e == cudaSuccess ? SPN_OK : BigPlan::err(e, "sketch single pass");
+  }
+  // One persistent dataflow launch (sketch_flow.cuh) when the operands are tensor views: every
+  // 32-column stripe through the four passes with per-(stripe, pass) dependencies instead of
+  // 4 launches per column group.
+  if (tma && flow_enabled() && dcols % 32 == 0 && lsa >= 5 && lsa <= 9 && lsb >= 5 && lsb <= 9) {
+    FlowParams fp{};
+    fp.nstripes = static_cast<int>(dcols / 32);
+    fp.G = flow_waves_g();
+    fp.d1 = d1;
+    fp.d2t = bp->sk_d[1];
+    fp.d3 = bp->sk_d[2];
+    fp.rowmap = bp->rowmap;
+    fp.wstride = nn * 32;
+    fp.out = out;
+    fp.ld_out = ld_out;
+    fp.cscale = static_cast<float>(cscale);
+    Scratch wsp, ctrs;
+    if (cudaError_t e = wsp.alloc(static_cast<size_t>(nn) * static_cast<size_t>(dcols) * 4, s0))
+      return BigPlan::err(e, "sketch workspace");
+    const size_t nctr = 1 + 4 * static_cast<size_t>(fp.nstripes);
+    if (cudaError_t e = ctrs.alloc(nctr * 4, s0)) return BigPlan::err(e, "sketch counters");
+    if (cudaError_t e = cudaMemsetAsync(ctrs.p, 0, nctr * 4, s0)) return BigPlan::err(e, "sketch counters");
+    fp.w = static_cast<float*>(wsp.p);
+    fp.ctr = static_cast<uint32_t*>(ctrs.p);
+    bool done = false;
+    cudaError_t e = launch_flow(lsa, lsb, fp, a, n_in, dcols, ld_a, sms, s0, &done);
+    if (e != cudaSuccess) return BigPlan::err(e, "sketch dataflow kernel");
+    if (done) {
+      if (cudaError_t e2 = bp->note_use(s0)) return BigPlan::err(e2, "sketch use event");
+      return SPN_OK;
+    }
   }
   // column groups of ~32 MB of workspace
   int64_t dc = std::max<int64_t>(32, (group_bytes(true) / (nn * 4)) / 32 * 32);
