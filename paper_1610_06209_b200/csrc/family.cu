@@ -273,9 +273,11 @@ struct FamilyPlan {
   int N = 0, logN = 0;
   double scale = 1.0;
   float *d1 = nullptr, *d2 = nullptr, *dense = nullptr, *dense_lo = nullptr;  // dense: G = hi + lo (TF32 split)
+  float* dense32 = nullptr;                                                      // dense: G in fp32
   double2 *spec = nullptr, *tw = nullptr, *skw = nullptr;
   ~FamilyPlan() {
-    for (void* q : {(void*)d1, (void*)d2, (void*)dense, (void*)dense_lo, (void*)spec, (void*)tw, (void*)skw})
+    for (void* q : {(void*)d1, (void*)d2, (void*)dense, (void*)dense_lo, (void*)dense32, (void*)spec, (void*)tw,
+                    (void*)skw})
       if (q) cudaFree(q);
   }
 };
@@ -346,10 +348,14 @@ spn_status family_build(FamilyPlan** out, int variant, int64_t n, int64_t m, int
     for (size_t i = 0; i < dense.size(); ++i) {
       const float g = static_cast<float>(dense[i]);
       hi[i] = tf32_round(g);
-      lo[i] = g - hi[i];
+      lo[i] = tf32_round(g - hi[i]);
     }
     e = upload(hi, &f->dense);
     if (e == cudaSuccess) e = upload(lo, &f->dense_lo);
+    if (e == cudaSuccess) {
+      for (size_t i = 0; i < dense.size(); ++i) hi[i] = static_cast<float>(dense[i]);
+      e = upload(hi, &f->dense32);
+    }
   } else {
     int lg = 0;
     while ((int64_t(1) << lg) < n) ++lg;
@@ -433,7 +439,7 @@ __global__ void tf32_split_kernel(const float* __restrict__ x, int64_t ld_x, int
     const float v = x[b * ld_x + j];
     const float h = tf32_round(v);
     hi[i] = h;
-    lo[i] = v - h;
+    lo[i] = tf32_round(v - h);
   }
 }
 
@@ -441,11 +447,25 @@ __global__ void tf32_split_kernel(const float* __restrict__ x, int64_t ld_x, int
 // (the dropped Xlo Glo^T term is ~2^-22 relative), each a cuBLAS TF32 GEMM accumulating in fp32 —
 // fp32-class accuracy (the 1e-5 bar) at tensor-core rate.  Column-major view: Y^T (k x batch, ld) =
 // G (n x k, lda = n)^T * X^T (n_in x batch); G's columns >= n_in meet x's zero padding.
+//
+// The Gaussian random-feature epilogue multiplies the projection's error by |z| / sigma (the angle), so
+// for that op the GEMM runs as a plain fp32 cuBLAS SGEMM instead (fuzz case n = 636, d' = 1272: 3xTF32
+// features 2.1e-5 relative L2 vs the 1e-5 bar; the split's ~2^-22 relative residual is 4x fp32's).
 spn_status dense_gemm(const FamilyPlan* f, const float* x, int64_t ld_x, int64_t n_in, int64_t batch, int64_t goff,
-                      float* Y, int64_t ld_y, cudaStream_t s) {
+                      float* Y, int64_t ld_y, cudaStream_t s, bool fp32_exact) {
   cublasHandle_t h = dense_handle(f->device);
   if (!h) return set_error(SPN_ECUDA, "dense baseline: cublasCreate failed");
   if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return set_error(SPN_ECUDA, "dense baseline: cublasSetStream");
+  if (fp32_exact) {
+    const float alpha = static_cast<float>(f->scale), beta = 0.0f;
+    const cublasStatus_t st = cublasGemmEx(
+        h, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(f->k), static_cast<int>(batch), static_cast<int>(n_in), &alpha,
+        f->dense32 + goff, CUDA_R_32F, static_cast<int>(f->n), x, CUDA_R_32F, static_cast<int>(ld_x), &beta, Y,
+        CUDA_R_32F, static_cast<int>(ld_y), CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    if (st != CUBLAS_STATUS_SUCCESS)
+      return set_error(SPN_ECUDA, std::string("dense baseline: cublasGemmEx status ") + std::to_string(static_cast<int>(st)));
+    return SPN_OK;
+  }
   float* xs = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&xs), sizeof(float) * static_cast<size_t>(2 * n_in * batch), s);
   if (e != cudaSuccess) return cuda_error(e, "dense scratch");
@@ -489,7 +509,8 @@ spn_status family_run(const FamilyPlan* f, int op, const float* x, int64_t batch
       float* dst = direct ? static_cast<float*>(out) : Y;
       const int64_t ld = direct ? ld_out : f->k;
       // Y = scale * X G^T: 3xTF32 GEMMs on the tensor cores (dense_gemm)
-      if (spn_status st = dense_gemm(f, x, ld_x, n_in, batch, t * f->blocks * f->m * f->n, dst, ld, s)) return st;
+      if (spn_status st = dense_gemm(f, x, ld_x, n_in, batch, t * f->blocks * f->m * f->n, dst, ld, s, op == 2))
+        return st;
       if (!direct) {
         const int64_t g = std::min<int64_t>(batch, int64_t(f->sms) * 8);
         dense_epilogue_kernel<<<static_cast<unsigned>(g), 256, 0, s>>>(Y, f->k, batch, f->k, op, relu, inv_sigma,
