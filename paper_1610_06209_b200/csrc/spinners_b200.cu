@@ -106,6 +106,8 @@ struct spn_plan {
   cudaStream_t hs[kHostStreams] = {};
   void* hbuf[kHostStreams][3] = {};  // [stream][x | out0 | out1]
   size_t hbuf_bytes[kHostStreams][3] = {};
+  void* hstage[kHostStreams][2] = {};  // pinned staging of pageable outputs [stream][out0 | out1]
+  size_t hstage_bytes[kHostStreams][2] = {};
 
   ~spn_plan();
 };
@@ -132,6 +134,9 @@ spn_plan::~spn_plan() {
     for (auto& a : hbuf)
       for (auto* p : a)
         if (p) cudaFree(p);
+    for (auto& a : hstage)
+      for (auto* p : a)
+        if (p) cudaFreeHost(p);
     for (auto s : hs)
       if (s) cudaStreamDestroy(s);
   }
@@ -983,8 +988,52 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
         if (q) cudaStreamSynchronize(q);
     }
   } drain{p};
-  auto d2h = [&](const HostOut& o, int64_t r0, int64_t rows, const void* dsrc, cudaStream_t st) -> cudaError_t {
+  // A D2H copy into PAGEABLE memory does not return until it has completed, so the next chunk's H2D would
+  // wait for this chunk's kernel: the copy engine idles (config 3 with numpy ids: 43 vs 55 GB/s).  Pageable
+  // outputs therefore land in a pinned staging buffer per stream and are copied out on the host one round
+  // later, after that stream has been synchronised (the other streams' copies keep the engine busy).
+  const HostOut* outs[2] = {&o0, &o1};
+  bool staged[2] = {false, false};
+  for (int b = 0; b < 2; ++b) {
+    if (!outs[b]->ptr) continue;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, outs[b]->ptr) != cudaSuccess) cudaGetLastError();
+    staged[b] = at.type != cudaMemoryTypeHost && at.type != cudaMemoryTypeManaged;
+    if (!staged[b]) continue;
+    const size_t need = static_cast<size_t>(chunk * outs[b]->row_bytes);
+    for (int s = 0; s < nst; ++s)
+      if (p->hstage_bytes[s][b] < need) {
+        if (p->hstage[s][b]) cudaFreeHost(p->hstage[s][b]);
+        p->hstage[s][b] = nullptr;
+        p->hstage_bytes[s][b] = 0;
+        SPN_CUDA(cudaMallocHost(&p->hstage[s][b], need));
+        p->hstage_bytes[s][b] = need;
+      }
+  }
+  int64_t pend_r0[spn_plan::kHostStreams], pend_rows[spn_plan::kHostStreams];
+  for (int s = 0; s < spn_plan::kHostStreams; ++s) pend_rows[s] = 0;
+  auto flush = [&](int s) -> cudaError_t {  // stream s's staged outputs -> the caller's buffers
+    if (pend_rows[s] == 0) return cudaSuccess;
+    if (cudaError_t e = cudaStreamSynchronize(p->hs[s])) return e;
+    for (int b = 0; b < 2; ++b) {
+      if (!staged[b]) continue;
+      const HostOut& o = *outs[b];
+      const char* src = static_cast<const char*>(p->hstage[s][b]);
+      char* dst = static_cast<char*>(o.ptr) + pend_r0[s] * o.ld_bytes;
+      if (o.ld_bytes == o.row_bytes)
+        std::memcpy(dst, src, static_cast<size_t>(o.row_bytes * pend_rows[s]));
+      else
+        for (int64_t r = 0; r < pend_rows[s]; ++r)
+          std::memcpy(dst + r * o.ld_bytes, src + r * o.row_bytes, static_cast<size_t>(o.row_bytes));
+    }
+    pend_rows[s] = 0;
+    return cudaSuccess;
+  };
+  auto d2h = [&](int b, int64_t r0, int64_t rows, const void* dsrc, int s) -> cudaError_t {
+    const HostOut& o = *outs[b];
     if (!o.ptr) return cudaSuccess;
+    cudaStream_t st = p->hs[s];
+    if (staged[b]) return cudaMemcpyAsync(p->hstage[s][b], dsrc, o.row_bytes * rows, cudaMemcpyDeviceToHost, st);
     char* dst = static_cast<char*>(o.ptr) + r0 * o.ld_bytes;
     if (o.ld_bytes == o.row_bytes) return cudaMemcpyAsync(dst, dsrc, o.row_bytes * rows, cudaMemcpyDeviceToHost, st);
     return cudaMemcpy2DAsync(dst, o.ld_bytes, dsrc, o.row_bytes, o.row_bytes, rows, cudaMemcpyDeviceToHost, st);
@@ -993,6 +1042,7 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
   for (int64_t r0 = 0; r0 < batch; r0 += chunk, ++c) {
     const int s = c % nst;
     const int64_t rows = std::min(chunk, batch - r0);
+    SPN_CUDA(flush(s));  // stream s's previous chunk (nst chunks ago)
     float* dx = static_cast<float*>(p->hbuf[s][0]);
     char* dout0 = static_cast<char*>(p->hbuf[s][1]);
     char* dout1 = static_cast<char*>(p->hbuf[s][2]);
@@ -1002,10 +1052,17 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
       SPN_CUDA(cudaMemcpy2DAsync(dx, in_row, x + r0 * ld_x, ld_x * 4, in_row, rows, cudaMemcpyHostToDevice,
                                  p->hs[s]));
     if (spn_status st = launch(dx, rows, n_in, dout0, dout1, p->hs[s])) return st;
-    SPN_CUDA(d2h(o0, r0, rows, dout0, p->hs[s]));
-    SPN_CUDA(d2h(o1, r0, rows, dout1, p->hs[s]));
+    SPN_CUDA(d2h(0, r0, rows, dout0, s));
+    SPN_CUDA(d2h(1, r0, rows, dout1, s));
+    if (staged[0] || staged[1]) {
+      pend_r0[s] = r0;
+      pend_rows[s] = rows;
+    }
   }
-  for (int s = 0; s < nst; ++s) SPN_CUDA(cudaStreamSynchronize(p->hs[s]));
+  for (int s = 0; s < nst; ++s) {
+    SPN_CUDA(cudaStreamSynchronize(p->hs[s]));
+    SPN_CUDA(flush(s));
+  }
   return SPN_OK;
 }
 
