@@ -774,7 +774,7 @@ def run_reference(args, rank, world):
     head = lines.pop(names[0])
     res = {"impl": "reference", **head, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (seeded, BASELINE config shapes)"}
+           "data": "synthetic (seeded, BASELINE config shapes and distributions)"}
     if lines:
         res["configs"] = lines
     return res
