@@ -13,6 +13,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -506,7 +507,10 @@ spn_status plan_create_impl(spn_plan** out, const spn_plan_desc* d, bool raw_spe
     return fail(SPN_EUNSUPPORTED, "circulant family: n > 2^13 (Toeplitz 2^12) not supported (fp64 FFT in smem)");
   if (!d->table_seeds && d->tables != 1) return fail(SPN_EINVAL, "tables > 1 needs table_seeds");
   if (d->scale != 0.0 && !std::isfinite(d->scale)) return fail(SPN_EDOMAIN, "non-finite scale");
-  auto* p = new spn_plan();
+  // owned until the end: a host allocation that throws (std::bad_alloc -> SPN_ENOMEM at the ABI
+  // barrier) must not leak the half-built plan
+  std::unique_ptr<spn_plan> owner(new spn_plan());
+  auto* p = owner.get();
   p->variant = d->variant;
   p->n = d->n;
   p->m = d->m;
@@ -522,20 +526,14 @@ spn_status plan_create_impl(spn_plan** out, const spn_plan_desc* d, bool raw_spe
     p->lazy_d = true;
     p->spec_seed = raw_spec_seed ? d->seed : spn::mix_seed(d->table_seeds ? d->table_seeds[0] : d->seed, 0);
     for (int di = 0; di < 3; ++di) p->dsign[di] = 1;
-    if (spn_status s = finish_plan(p)) {
-      delete p;
-      return s;
-    }
+    if (spn_status s = finish_plan(p)) return s;
     p->big.dev_rad = true;
     p->big.dev_seed = p->spec_seed;
     {
       DeviceGuard g(p->device);
-      if (spn_status s = p->big.prefetch_sketch(p->n)) {
-        delete p;
-        return s;
-      }
+      if (spn_status s = p->big.prefetch_sketch(p->n)) return s;
     }
-    *out = p;
+    *out = owner.release();
     return SPN_OK;
   }
   for (auto& v : p->d) v.resize(static_cast<size_t>(p->tables * per));
@@ -560,11 +558,8 @@ spn_status plan_create_impl(spn_plan** out, const spn_plan_desc* d, bool raw_spe
     spn::parallel_for(nblk, realize);
   else
     for (int64_t i = 0; i < nblk; ++i) realize(i);
-  if (spn_status s = finish_plan(p)) {
-    delete p;
-    return s;
-  }
-  *out = p;
+  if (spn_status s = finish_plan(p)) return s;
+  *out = owner.release();
   return SPN_OK;
 }
 }  // namespace

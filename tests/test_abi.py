@@ -143,3 +143,30 @@ def test_spec_json_round_trip(spn):
         assert (t.variant, t.n, t.m, t.seed, t.effective_scale()) == (s.variant, 64, 32, 7, s.effective_scale())
     with pytest.raises(spn.DomainError):
         spn.SpinnerSpec.from_json({"variant": "Nope", "n": 4, "m": 4, "seed": 0})
+
+
+def test_host_allocation_failure_is_a_status_not_an_abort(spn):
+    """Every C-ABI entry point is an exception barrier: a host allocation that cannot succeed (2^25 tables
+    of 2^20-point HDg blocks = 2^45 doubles per diagonal) comes back as SPN_ENOMEM instead of terminating
+    the process (std::bad_alloc never crosses the extern "C" boundary)."""
+    import ctypes
+    d = spn._Desc()
+    d.variant, d.n, d.m, d.k, d.tables = int(spn.SpinnerVariant.hdg_hd2_hd1), 1 << 20, 1 << 20, 1 << 20, 1 << 25
+    seeds = (spn._u64 * 4)(1, 2, 3, 4)  # never read: the allocation fails first
+    d.table_seeds = ctypes.cast(seeds, ctypes.POINTER(spn._u64))
+    h = spn._vp()
+    assert spn._plan_create(ctypes.byref(h), ctypes.byref(d)) == spn.SPN_ENOMEM
+    assert not h.value
+    assert "allocation" in spn._last_error().decode()
+
+
+def test_new_entry_points_reject_bad_arguments(spn):
+    import ctypes
+    h = spn._vp()
+    r = np.zeros(4)
+    assert spn._plan_resample(None, None, 0, 1) == spn.SPN_EINVAL
+    assert spn._plan_resample(ctypes.byref(h), None, 0, 1) == spn.SPN_EINVAL
+    assert spn._plan_with_tail(ctypes.byref(h), None, r.ctypes.data) == spn.SPN_EINVAL
+    assert spn._sketch_host(None, None, 1, 1, 1, None, 1, 1.0, None, 1) == spn.SPN_EINVAL
+    assert spn._hash_project_host(None, None, 1, 1, 1, None, None, 1) == spn.SPN_EINVAL
+    assert spn._hash_peers(None, None, 1, 1, 1, None, 1, 0, 1, None) == spn.SPN_EINVAL

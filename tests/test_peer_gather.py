@@ -66,3 +66,25 @@ def test_fused_peer_gather_two_ranks(tmp_path, oracle, total):
         want, gaps = oracle.hash(*d, n, n, n, 1, float(np.sqrt(n)), x)
         bad = (single[:, t] != want[:, 0]) & ~(gaps[:, 0] < 1e-5)
         assert not bad.any(), (t, int(bad.sum()))
+
+
+def test_peer_hash_rejects_rows_outside_the_gathered_table():
+    """spn_hash_f32_peers gets the gathered table's row count: a shard that would write past it is
+    refused by the C ABI (and by PeerCodes.hash before it), never written into a peer's memory."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import paper_1610_06209_b200 as spn
+    from paper_1610_06209_b200.shard import PeerCodes
+    n, tables, total = 256, 2, 100
+    h = spn.MultiTableHasher(spn.SpinnerVariant.hd3_hd2_hd1, n, n, tables, seed=5)
+    pc = PeerCodes(total, tables, 1, 0)
+    x = torch.randn(50, n, device="cuda")
+    with pytest.raises(ValueError):
+        pc.hash(h, x, 80)
+    st = spn._hash_peers(h.plan._h, x.data_ptr(), 50, n, n, pc.ptrs.data_ptr(), 1, 80, total, None)
+    assert st == spn.SPN_EINVAL
+    table = pc.hash(h, x, 50)  # rows 50..99: fits
+    want = h.hash_ids(x)
+    assert torch.equal(table[50:], want) and bool((table[:50] == -1).all())
