@@ -813,7 +813,11 @@ def main():
             res["configs"] = lines
         print(json.dumps(res), flush=True)
     if world > 1:
+        import gc
         import torch.distributed as dist
+        gc.collect()
+        torch.cuda.ipc_collect()  # release the peer tables mapped from the other ranks (PeerCodes)
+        barrier(world)  # ... on every rank before any producer exits
         dist.destroy_process_group()
     del torch
 
