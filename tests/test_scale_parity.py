@@ -242,3 +242,17 @@ def test_output_buffers_are_validated(spn, torch):
     hb = np.full((10, 80), 7.0, dtype=np.float32)
     sp.apply(xh, out=hb[:, :64])
     assert np.array_equal(hb[:, :64], big[:, :64].cpu().numpy()) and (hb[:, 64:] == 7.0).all()
+
+
+@pytest.mark.parametrize("input_dim,d,rows", [(100000, 64, 2048), (1 << 16, 32, 1000), (1000, 96, 300),
+                                              (40000, 160, 4096), (1 << 18, 32, 512)])
+def test_dataflow_sketch_shapes_match_reference(spn, ref, torch, input_dim, d, rows):
+    """The dataflow sketch kernel (d a multiple of 32) over zero-padded inputs (input_dim < N) and every
+    low/high bit split it instantiates (N = 2^10 .. 2^18), first-m and random P, against the reference."""
+    rng = np.random.default_rng(input_dim + d)
+    a = rng.standard_normal((input_dim, d)).astype(np.float32)
+    for mode in ("first", "random"):
+        sk = spn.SketchOperator(spn.SpinnerVariant.hd3_hd2_hd1, input_dim, rows, 17, mode=mode, p_seed=5)
+        want = ref.sketch(HD3, a, rows, 17, row_list=sk.row_list, threads=THREADS)
+        got = sk.apply(torch.from_numpy(a).cuda()).cpu().numpy()
+        assert row_rel(got.T, want.T).max() <= RTOL, mode
