@@ -203,6 +203,7 @@ class Workload:
         self.spn, self.torch, self.name, self.cfg = spn, torch, name, CONFIGS[name]
         self.rank, self.world, self.device = rank, world, device
         cfg = self.cfg
+        dev = torch.cuda.current_device()  # every plan on this rank's GPU (torch.cuda.set_device(LOCAL_RANK))
         strong = scaling == "strong"
         g = torch.Generator(device="cuda")
         g.manual_seed(1234 + (0 if strong else rank))
@@ -222,19 +223,19 @@ class Workload:
 
         if name == "c1":
             self.r0, self.units = rows_of(cfg["batch"])
-            self.sp = spn.StackedSpinner(V.hd3_hd2_hd1, 1024, 1024, 1024, 42, scale=1.0)
+            self.sp = spn.StackedSpinner(V.hd3_hd2_hd1, 1024, 1024, 1024, 42, scale=1.0, device=dev)
             x = gen((cfg["batch"], 1024), "n")
             self.x = (x / x.norm(dim=1, keepdim=True))[self.r0:self.r0 + self.units].contiguous()
             self.y = torch.empty_like(self.x)
         elif name == "c2":
             self.r0, self.units = rows_of(cfg["batch"])
-            self.sp = spn.StackedSpinner(V.hd3_hd2_hd1, 1024, 1024, cfg["k"], 5)
+            self.sp = spn.StackedSpinner(V.hd3_hd2_hd1, 1024, 1024, cfg["k"], 5, device=dev)
             self.fm = spn.FeatureMap(self.sp, spn.KernelKind.gaussian(cfg["sigma"]))
             self.x = gen((cfg["batch"], cfg["n_in"]), "u")[self.r0:self.r0 + self.units].contiguous()
             self.out = torch.empty((self.units, 2 * cfg["k"]), device="cuda")
         elif name == "c3":
             self.r0, self.units = rows_of(cfg["batch"])
-            self.h = spn.MultiTableHasher(V.hd3_hd2_hd1, cfg["n"], cfg["n"], cfg["tables"], seed=3)
+            self.h = spn.MultiTableHasher(V.hd3_hd2_hd1, cfg["n"], cfg["n"], cfg["tables"], seed=3, device=dev)
             self.x = torch.empty((self.units, cfg["n"]), device="cuda")
             # N(0,1) then L2-normalised, generated on device in 2^16-row blocks keyed by the global row
             blk_rows = 1 << 16
@@ -260,7 +261,7 @@ class Workload:
                     self.gather_total = total
         elif name == "c4":
             self.c0, self.units = rows_of(cfg["d"])  # columns
-            self.sk = spn.SketchOperator(V.hd3_hd2_hd1, cfg["N"], cfg["m"], 11, mode="random", p_seed=77)
+            self.sk = spn.SketchOperator(V.hd3_hd2_hd1, cfg["N"], cfg["m"], 11, mode="random", p_seed=77, device=dev)
             a = gen((cfg["N"], cfg["d"]), "n")
             self.x = a[:, self.c0:self.c0 + self.units].contiguous()
             del a
@@ -269,7 +270,7 @@ class Workload:
             self.launches_per_step = 4 * groups
         elif name == "c5":
             self.r0, self.units = rows_of(cfg["batch"])
-            self.sp = spn.StackedSpinner(V.gauss3, cfg["n"], cfg["n"], cfg["n"], 13, scale=1.0)
+            self.sp = spn.StackedSpinner(V.gauss3, cfg["n"], cfg["n"], cfg["n"], 13, scale=1.0, device=dev)
             self.x = torch.empty((self.units, cfg["n"]), device="cuda")
             for r in range(self.units):  # row r of the global batch from its own seed
                 gr = torch.Generator(device="cuda")
@@ -283,14 +284,14 @@ class Workload:
             self.newton = newton
             f = torch.randn((cfg["N"], cfg["d"]), device="cuda", generator=g)
             y = torch.where(torch.rand(cfg["N"], device="cuda", generator=g) < 0.5, -1.0, 1.0)
-            self.prob = spn.LogisticProblem(f, y)
+            self.prob = spn.LogisticProblem(f, y, device=dev)
             self.prob.workspace(cfg["m"])
             self.xk = torch.full((cfg["d"],), 0.01, dtype=torch.float64, device="cuda")
             self.units = cfg["d"]  # columns sketched per iteration
             self.t = 0
             import concurrent.futures
             self.pool = concurrent.futures.ThreadPoolExecutor(1)  # next sketch realised during this step
-            self.mk = lambda it: spn.SketchOperator(V.hd3_hd2_hd1, cfg["N"], cfg["m"], spn.mix_seed(3, it))  # noqa
+            self.mk = lambda it: spn.SketchOperator(V.hd3_hd2_hd1, cfg["N"], cfg["m"], spn.mix_seed(3, it), device=dev)  # noqa
             self.pending = self.pool.submit(self.mk, 0)
             self.launches_per_step = 16  # pass over A + 4 sketch passes + line search (a lower bound)
         elif name == "c7":
@@ -307,7 +308,7 @@ class Workload:
             self.cx = torch.from_numpy(x.astype(np.float32)).cuda()
             self.cy = torch.from_numpy(y.astype(np.float32)).cuda()
             self.cd = 2.0 * np.sin(ang / 2.0)
-            self.fac = spn.make_hasher_factory(V.hd3_hd2_hd1, n, cfg["m"])
+            self.fac = spn.make_hasher_factory(V.hd3_hd2_hd1, n, cfg["m"], device=dev)
             self.units = 2 * P * cfg["trials"]
             self.t = 0
         torch.cuda.synchronize()
