@@ -699,6 +699,10 @@ __device__ __forceinline__ void stage_x(float* xb, const float* __restrict__ xro
 template <int LOG_R, int LOG_T, int OP, bool SIGNS>
 __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T>::min_ctas(OP))
     spinner_vec_kernel(const VecParams p) {
+  // programmatic dependent launch (vec_launch.cuh): let the next kernel on the stream launch, then
+  // wait for the previous one (a no-op without the launch attribute)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   using C = VCfg<LOG_R, LOG_T>;
   extern __shared__ __align__(16) float smem[];
   constexpr bool END_B = OP != OP_HASH;  // epilogue needs coalesced layout B

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <cstdlib>
 #include <utility>
 
 #include "spinner_vec.cuh"
@@ -50,8 +51,24 @@ cudaError_t launch_vec(const VecParams& p, cudaStream_t s, int sms, int64_t item
   q.vec_major = OP == OP_HASH && p.tables > 1 && vslots >= int64_t(sms) * occ;
   if (q.vec_major) ctas = vslots;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ctas, int64_t(sms) * occ));
-  kern<<<static_cast<unsigned>(grid), C::THREADS, C::smem_bytes(OP), s>>>(q);
-  return cudaGetLastError();
+  // programmatic dependent launch: the kernel lets its successor on the stream launch at once (the
+  // successor's CTAs take SM slots as ours retire and wait in griddepcontrol.wait for our completion),
+  // hiding the launch gap between back-to-back calls (c1 in a CUDA graph)
+  static const bool pdl = [] {
+    const char* e = std::getenv("SPN_VEC_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::smem_bytes(OP);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, q);
 }
 
 template <int OP, bool SIGNS, int... L>
