@@ -266,8 +266,11 @@ class Workload:
             self.x = a[:, self.c0:self.c0 + self.units].contiguous()
             del a
             self.out = torch.empty((cfg["m"], self.units), device="cuda")
-            groups = math.ceil(self.units / max(32, ((32 << 20) // (cfg["N"] * 4)) // 32 * 32))
-            self.launches_per_step = 4 * groups
+            if self.units % 32 == 0 and os.environ.get("SPN_FLOW", "1") != "0":
+                self.launches_per_step = 1  # the dataflow sketch kernel (sketch_flow.cuh): the whole step
+            else:  # grouped pass launches: 4 per column group
+                groups = math.ceil(self.units / max(32, ((32 << 20) // (cfg["N"] * 4)) // 32 * 32))
+                self.launches_per_step = 4 * groups
         elif name == "c5":
             self.r0, self.units = rows_of(cfg["batch"])
             self.sp = spn.StackedSpinner(V.gauss3, cfg["n"], cfg["n"], cfg["n"], 13, scale=1.0, device=dev)
