@@ -18,6 +18,7 @@ Bars (north_star): fp32 outputs <= 1e-5 relative L2 per vector; ids bit-exact ex
 (reference top-two |y| within 1e-5 relative), which are counted and reported.
 """
 import os
+import warnings
 
 import numpy as np
 import pytest
@@ -53,12 +54,21 @@ def ids_and_gaps(y, k):
     return ids, gap
 
 
+class ParityReport(UserWarning):
+    """Parity figures surfaced in pytest's warnings summary (visible under -q, unlike print)."""
+
+
+def report(msg):
+    print(msg)
+    warnings.warn(msg, ParityReport)
+
+
 def check_ids(got, want, gaps, what):
     got, want, gaps = np.asarray(got), np.asarray(want), np.asarray(gaps)
     near = gaps < NEAR_TIE
     bad = (got != want) & ~near
-    print(f"[{what}] ids: {got.size} checked, {int((got != want).sum())} differ, {int(near.sum())} near-ties "
-          f"(top-two |y| within {NEAR_TIE:g} relative), {int(bad.sum())} mismatches outside near-ties")
+    report(f"[{what}] ids: {got.size} checked, {int((got != want).sum())} differ, {int(near.sum())} near-ties "
+           f"(top-two |y| within {NEAR_TIE:g} relative), {int(bad.sum())} mismatches outside near-ties")
     assert not bad.any(), f"{what}: {bad.sum()} id mismatches outside near-ties (of {got.size})"
 
 
@@ -103,7 +113,7 @@ def test_c2_full_batch_sampled_rows(spn, ref, torch):
     rows_t = torch.from_numpy(rows).cuda()
     f_ref = ref.embed(HD3, n, k, seed, 0, sigma, x[rows_t].cpu().numpy(), n_in=n_in, threads=THREADS)
     rel = row_rel(out[rows_t].cpu().numpy(), f_ref)
-    print(f"[c2] 2000 of 60000 rows: max rel L2 {rel.max():.3e}")
+    report(f"[c2] 2000 of 60000 rows: max rel L2 {rel.max():.3e}")
     assert rel.max() <= RTOL
 
 
@@ -142,7 +152,7 @@ def test_c4_all_256_columns(spn, ref, torch):
         torch.cuda.synchronize()
         want = ref.sketch(HD3, ah, m, seed, row_list=sk.row_list, threads=THREADS)
         rel = row_rel(out.cpu().numpy().T, want.T)  # per column (= per sketched vector)
-        print(f"[c4 {mode}] 256 columns: max rel L2 {rel.max():.3e}")
+        report(f"[c4 {mode}] 256 columns: max rel L2 {rel.max():.3e}")
         assert rel.max() <= RTOL
         # value semantics through spn_sketch_f32_host: the same numbers
         out_h = sk.apply(ah)
@@ -161,7 +171,7 @@ def test_c5_full_batch(spn, ref, torch):
     d = [a[0].astype(np.float32).astype(np.float64) for a in sp.diagonals()]
     y_ref = ref.chain(d[0], d[1], d[2], 1.0, x.cpu().numpy(), relu=True, threads=THREADS)
     rel = row_rel(y.cpu().numpy(), y_ref)
-    print(f"[c5] 256 x 2^20: max rel L2 {rel.max():.3e}")
+    report(f"[c5] 256 x 2^20: max rel L2 {rel.max():.3e}")
     assert rel.max() <= RTOL
 
 
