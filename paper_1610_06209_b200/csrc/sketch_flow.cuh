@@ -210,7 +210,15 @@ __global__ void __launch_bounds__(FlowCfg<LSA, LSB>::THREADS, 1)
       if (tk.pass > 0) {  // every tile of the previous pass of this stripe is stored
         const uint32_t need = (tk.pass & 1) ? (1u << LSB) : (1u << LSA);  // sub-tiles of pass - 1
         const uint32_t* c = p.ctr + 1 + 4 * tk.stripe + (tk.pass - 1);
-        while (ld_acquire(c) < need) __nanosleep(100);
+        // a dependency that never completes is a bug: abort the grid (a CUDA error) rather than hang the GPU
+        uint64_t t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (ld_acquire(c) < need) {
+          __nanosleep(100);
+          uint64_t t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if (t1 - t0 > 5000000000ull) __trap();
+        }
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       tslot[slot] = (int)t;
