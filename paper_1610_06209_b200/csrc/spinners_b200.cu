@@ -57,6 +57,16 @@ struct DeviceGuard {
   }
 };
 
+// What kind of memory a caller's pointer is (pageable host memory reports cudaMemoryTypeUnregistered).
+cudaMemoryType host_ptr_kind(const void* ptr) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return cudaMemoryTypeUnregistered;
+  }
+  return at.type;
+}
+
 using spn::kMaxLogNVec;
 constexpr int kMaxLogN = 20;     // multi-pass path up to 2^20
 
@@ -880,6 +890,8 @@ spn_status spn_sketch_f32_host(const spn_plan* cp, const float* a, int64_t n_in,
                                int64_t ld_out) { SPN_TRY
   if (spn_status st = sketch_check(cp, a, n_in, d, ld_a, rows, m_out, out, ld_out)) return st;
   if (d == 0 || m_out == 0) return SPN_OK;
+  if (host_ptr_kind(a) == cudaMemoryTypeDevice || host_ptr_kind(out) == cudaMemoryTypeDevice)
+    return fail(SPN_EINVAL, "host entry point given a device pointer");
   auto* p = const_cast<spn_plan*>(cp);
   std::lock_guard<std::mutex> lock(p->mu);
   DeviceGuard g(p->device);
@@ -993,11 +1005,12 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
   // later, after that stream has been synchronised (the other streams' copies keep the engine busy).
   const HostOut* outs[2] = {&o0, &o1};
   bool staged[2] = {false, false};
+  if (host_ptr_kind(x) == cudaMemoryTypeDevice) return fail(SPN_EINVAL, "host entry point given a device input");
   for (int b = 0; b < 2; ++b) {
     if (!outs[b]->ptr) continue;
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, outs[b]->ptr) != cudaSuccess) cudaGetLastError();
-    staged[b] = at.type != cudaMemoryTypeHost && at.type != cudaMemoryTypeManaged;
+    const cudaMemoryType kind = host_ptr_kind(outs[b]->ptr);
+    if (kind == cudaMemoryTypeDevice) return fail(SPN_EINVAL, "host entry point given a device output");
+    staged[b] = kind != cudaMemoryTypeHost && kind != cudaMemoryTypeManaged;
     if (!staged[b]) continue;
     const size_t need = static_cast<size_t>(chunk * outs[b]->row_bytes);
     for (int s = 0; s < nst; ++s)
