@@ -500,6 +500,34 @@ def secondary_rooflines(name, cfg, units, step_ms, clocks):
     return out
 
 
+# FP32 butterfly adds per unit (3 H's of n log2 n adds each per spinner block; c2 four blocks per sample,
+# c3 eight tables per vector): the ALU roof of SURVEY §8(d), at 128 FP32 adds / clk / SM
+FP32_ADDS_PER_UNIT = {"c1": 3 * 10 * 1024, "c2": 4 * 3 * 10 * 1024, "c3": 8 * 3 * 14 * 16384,
+                      "c4": 3 * 17 * (1 << 17), "c5": 3 * 20 * (1 << 20)}
+
+
+def fp32_roofline(name, units, step_ms, clocks):
+    if name not in FP32_ADDS_PER_UNIT:
+        return {}
+    mhz = clocks.get("sm_mhz") or 1965.0
+    adds = FP32_ADDS_PER_UNIT[name] * units
+    floor = adds / (148 * 128 * mhz * 1e6) * 1e3
+    out = {"roofline_fp32": {"bound": "fp32 add pipe", "adds_per_step": adds, "floor_ms": floor,
+                             "measured_ms": step_ms, "frac": floor / step_ms, "sm_mhz": mhz,
+                             "model": "FP32 butterfly adds (3 n log2 n per spinner block) at 128 adds/clk/SM"}}
+    try:  # the pipe utilisation ncu measured for this config's kernel (committed capture)
+        with open(os.path.join(ROOT, "profiles", f"r02_{name}_ncu_full.json")) as f:
+            m = json.load(f)["launches"][0]["metrics"]
+        out["roofline_fp32"]["ncu_fma_pipe_active_pct"] = float(
+            m["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"][0])
+        out["roofline_fp32"]["ncu_issue_active_pct"] = float(
+            m["smsp__issue_active.avg.pct_of_peak_sustained_active"][0])
+        out["roofline_fp32"]["ncu_source"] = f"profiles/r02_{name}_ncu_full.json"
+    except Exception:
+        pass
+    return out
+
+
 def traffic_from_profiles(config):
     """DRAM bytes (read + write) per step from the committed ncu captures (profiles/traffic.json)."""
     try:
@@ -637,6 +665,7 @@ def measure_config(name, args, rank, world, local, clk):
     if w.exchange:
         res["exchange"] = w.exchange
     res.update(secondary_rooflines(name, CONFIGS[name], w.units, mean_ms, clocks))
+    res.update(fp32_roofline(name, w.units, mean_ms, clocks))
     if name == "c1":
         res["steady_state"] = c1_steady_state(w, args.steps, peak)
     if not args.no_e2e and name in ("c1", "c2", "c3", "c4", "c5"):
