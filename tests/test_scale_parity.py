@@ -266,3 +266,19 @@ def test_dataflow_sketch_shapes_match_reference(spn, ref, torch, input_dim, d, r
         want = ref.sketch(HD3, a, rows, 17, row_list=sk.row_list, threads=THREADS)
         got = sk.apply(torch.from_numpy(a).cuda()).cpu().numpy()
         assert row_rel(got.T, want.T).max() <= RTOL, mode
+
+
+def test_host_entry_points_reject_device_pointers(spn, torch):
+    """The _host entry points copy through pinned staging / cudaMemcpy: a device pointer is refused
+    (SPN_EINVAL) instead of being memcpy'd on the host."""
+    sp = spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, 64, 64, 64, 1)
+    xd = torch.randn((4, 64), device="cuda")
+    yh = np.empty((4, 64), dtype=np.float32)
+    yd = torch.empty((4, 64), device="cuda")
+    assert spn._apply_host(sp.plan._h, xd.data_ptr(), 4, 64, 64, yh.ctypes.data, 64, 0) == spn.SPN_EINVAL
+    xh = xd.cpu().numpy()
+    assert spn._apply_host(sp.plan._h, xh.ctypes.data, 4, 64, 64, yd.data_ptr(), 64, 0) == spn.SPN_EINVAL
+    sk = spn.SketchOperator(spn.SpinnerVariant.hd3_hd2_hd1, 64, 16, 3)
+    out = np.empty((16, 4), dtype=np.float32)
+    a = torch.randn((64, 4), device="cuda")
+    assert spn._sketch_host(sk.plan._h, a.data_ptr(), 64, 4, 4, None, 16, 0.25, out.ctypes.data, 4) == spn.SPN_EINVAL
