@@ -217,6 +217,57 @@ struct Swz {
   }
 };
 
+// Layout-B side of a transpose as 8x8 b16 matrix moves (ldmatrix / stmatrix .x4): one
+// instruction moves four registers of every lane (512 B per warp) where LDS.32 / STS.32
+// move one (128 B), cutting the transpose's shared-memory instructions from R + R/4 to
+// R/4 + R/4.  For fp32 data an 8x8 b16 matrix is 8 rows of four floats and lane l gets
+// word l&3 of row l>>2: with matrix q's rows the eight 16-B chunks of elements
+// (j0+q)*T + 32w + [0, 32) (rows supplied by lanes 8q..8q+7), lane l receives element
+// (j0+q)*T + 32w + l — exactly register j0+q of layout B.  The swizzle XORs whole 16-B
+// chunks inside that 128-B line, so each matrix is still one conflict-free wavefront.
+// Needs whole warps per group (T >= 32) and 16-B chunks (R >= 4).
+template <class C>
+struct MatB {
+  static constexpr bool ON = C::T >= 32 && C::R >= 4;
+  static constexpr int S = C::LOG_R - C::LOG_T;            // (e >> LOG_R) == (j >> S) on the B side
+  static constexpr int P = ((C::XMASK + 1) << S) / 4 > 0 ? ((C::XMASK + 1) << S) / 4 : 1;  // swizzle period in j0/4
+  uint32_t off[P];                                          // byte offsets of this lane's row, per j0/4 mod P
+  __device__ __forceinline__ MatB(const float* sm, int t) {
+    const int l = t & 31, w = t >> 5, q = l >> 3, rho = l & 7;
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const int c = ((4 * k + q) >> S) & C::XMASK;
+      off[k] = base + 4u * static_cast<uint32_t>((4 * k + q) * C::T + 32 * w + 4 * (rho ^ c));
+    }
+  }
+  __device__ __forceinline__ uint32_t addr(int k) const {  // k = j0 / 4 (compile-time after unrolling)
+    return off[k % P] + 16u * static_cast<uint32_t>((k - k % P) * C::T);
+  }
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t a, float& r0, float& r1, float& r2, float& r3) {
+  uint32_t u0, u1, u2, u3;
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(u0), "=r"(u1), "=r"(u2), "=r"(u3)
+               : "r"(a)
+               : "memory");
+  r0 = __uint_as_float(u0);
+  r1 = __uint_as_float(u1);
+  r2 = __uint_as_float(u2);
+  r3 = __uint_as_float(u3);
+}
+__device__ __forceinline__ void stsm_x4(uint32_t a, float r0, float r1, float r2, float r3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};\n" ::"r"(a),
+               "r"(__float_as_uint(r0)), "r"(__float_as_uint(r1)), "r"(__float_as_uint(r2)),
+               "r"(__float_as_uint(r3))
+               : "memory");
+}
+
+#ifndef SPN_XPOSE_MATRIX
+#define SPN_XPOSE_MATRIX 1
+#endif
+
 template <class C>
 __device__ __forceinline__ void xpose_A_to_B(float (&r)[C::R], float* sm, int t) {
   const Swz<C> z(t);
@@ -230,16 +281,28 @@ __device__ __forceinline__ void xpose_A_to_B(float (&r)[C::R], float* sm, int t)
     for (int j = 0; j < C::R; ++j) sm[sw<C>(t * C::R + j)] = r[j];
   }
   group_sync<C>();
+  if constexpr (MatB<C>::ON && SPN_XPOSE_MATRIX) {
+    const MatB<C> mb(sm, t);
 #pragma unroll
-  for (int j = 0; j < C::R; ++j) r[j] = sm[z.B(t, j)];
+    for (int k = 0; k < C::R / 4; ++k) ldsm_x4(mb.addr(k), r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < C::R; ++j) r[j] = sm[z.B(t, j)];
+  }
   group_sync<C>();
 }
 
 template <class C>
 __device__ __forceinline__ void xpose_B_to_A(float (&r)[C::R], float* sm, int t) {
   const Swz<C> z(t);
+  if constexpr (MatB<C>::ON && SPN_XPOSE_MATRIX) {
+    const MatB<C> mb(sm, t);
 #pragma unroll
-  for (int j = 0; j < C::R; ++j) sm[z.B(t, j)] = r[j];
+    for (int k = 0; k < C::R / 4; ++k) stsm_x4(mb.addr(k), r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < C::R; ++j) sm[z.B(t, j)] = r[j];
+  }
   group_sync<C>();
   if constexpr (C::R >= 4) {
 #pragma unroll
