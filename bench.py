@@ -418,7 +418,7 @@ class Workload:
         if n in ("c1", "c3"):
             cfg = self.cfg
             nn = cfg["n"]
-            rows = np.sort(rng.choice(self.units, min(self.units, 64 if n == "c3" else 512), replace=False))
+            rows = np.sort(rng.choice(self.units, min(self.units, 1024 if n == "c3" else 512), replace=False))
             xs = self.x[torch.from_numpy(rows).cuda()].cpu().numpy()
             if n == "c1":
                 got = self.ids_last.cpu().numpy()[rows] if hasattr(self, "ids_last") else None
@@ -440,7 +440,7 @@ class Workload:
                 res.update(rows=int(rows.size), ids=int(want.size), id_mismatches=int(diff.sum()),
                            near_ties=int(near.sum()), mismatches_outside_near_ties=int((diff & ~near).sum()))
         elif n == "c2":
-            rows = np.sort(rng.choice(self.units, 256, replace=False))
+            rows = np.sort(rng.choice(self.units, min(self.units, 2048), replace=False))
             rt = torch.from_numpy(rows).cuda()
             want = ref.embed(HD3, 1024, self.cfg["k"], 5, 0, self.cfg["sigma"], self.x[rt].cpu().numpy(),
                              n_in=self.cfg["n_in"], threads=thr)
@@ -450,10 +450,11 @@ class Workload:
             want = ref.sketch(HD3, a, self.cfg["m"], 11, row_list=self.sk.row_list, threads=thr)
             res.update(columns=int(self.units), max_rel_l2=rel(self.out.cpu().numpy().T, want.T))
         elif n == "c5":
-            rows = np.arange(min(self.units, 8))
+            rows = np.sort(rng.choice(self.units, min(self.units, 32), replace=False))
             d = [v[0].astype(np.float32).astype(np.float64) for v in self.sp.diagonals()]
-            want = ref.chain(d[0], d[1], d[2], 1.0, self.x[:rows.size].cpu().numpy(), relu=True, threads=thr)
-            res.update(rows=int(rows.size), max_rel_l2=rel(self.y[:rows.size].cpu().numpy(), want))
+            rt = torch.from_numpy(rows).cuda()
+            want = ref.chain(d[0], d[1], d[2], 1.0, self.x[rt].cpu().numpy(), relu=True, threads=thr)
+            res.update(rows=int(rows.size), max_rel_l2=rel(self.y[rt].cpu().numpy(), want))
         res["pass"] = bool(res.get("max_rel_l2", res.get("y_max_rel_l2", 0.0)) <= 1e-5 and
                            res.get("mismatches_outside_near_ties", 0) == 0)
         return res
@@ -462,11 +463,12 @@ class Workload:
 # Issue floors from the ncu instruction mix (tools/sass_mix.py on the committed ncu reports):
 # warp-issue cycles per unit with FADD2 counted twice, at the clock the floor was computed for.
 ISSUE_FLOOR = {
-    "c2": {"ms": 0.356, "mhz": 1785.0, "model": "6.26 K issue cycles per sample (1536 FADD2 x2, 768 FADD, 432 sign "
-           "flips, 555 LDS/STS, 416 FMUL, 256 MUFU, ~450 address/loop) over 60000 samples on 592 SMSPs"},
-    "c3": {"ms": 205.6, "mhz": 1965.0, "model": "28.5 K warp-issue cycles per (vector, table) (9216 FADD2 x2, 3072 "
-           "FADD, 1931 LOP3 + 192 R2P sign flips, 1925 LDS/STS transposes, 576 LDG, 754 IMAD, argmax) over "
-           "2^20 x 8 items on 592 SMSPs"},
+    "c2": {"ms": 0.307, "mhz": 1965.0, "model": "5.95 K issue cycles per sample (1536 FADD2 x2, 768 FADD, 513 LOP3 + "
+           "48 R2P sign flips, 96 STS + 75 LDS + 64 LDSM + 32 STSM, 416 FMUL, 256 MUFU, ~550 address/loop) over 60000 "
+           "samples on 592 SMSPs (profiles/r02_c2_sass_mix.txt)"},
+    "c3": {"ms": 197.8, "mhz": 1965.0, "model": "27.4 K warp-issue cycles per (vector, table) (9216 FADD2 x2, 3072 "
+           "FADD, 1919 LOP3 + 192 R2P sign flips, 389 STS + 384 LDSM transposes, 576 LDG, 658 IMAD, argmax) over "
+           "2^20 x 8 items on 592 SMSPs (profiles/r02_c3_sass_mix.txt)"},
 }
 
 # L2-resident read-modify-write bandwidth measured on this pool's B200 (tools/microbench/mb.cu, in-place
