@@ -482,14 +482,17 @@ def secondary_rooflines(name, cfg, units, step_ms, clocks):
     through L2), the issue-bound ones (c2, c3) against their instruction-count floor."""
     out = {}
     if name in ("c4", "c5"):
-        if name == "c5":
-            l2_bytes = 4 * 2 * units * cfg["n"] * 4
+        if name == "c5":  # + D1, D2, D3 (fp32, n each) read by their pass for every vector (ncu: the three
+            # passes with a diagonal move 2x the group's bytes from L2, profiles/r02_c5_ncu_full.json)
+            l2_bytes = (4 * 2 + 3) * units * cfg["n"] * 4
+            model = "4 passes x (read + write) of the working set + 3 diagonal reads per vector through L2"
         else:  # passes 1-3 read + write A's columns, pass 4 reads them and writes the m gathered rows
             l2_bytes = 7 * cfg["N"] * units * 4 + cfg["m"] * units * 4
+            model = "4 passes x (read + write) of the working set through L2"
         ach = l2_bytes / (step_ms * 1e-3) / 1e9
         out["roofline_l2"] = {"bound": "l2", "achieved": ach, "peak": L2_RMW_GBS, "unit": "GB/s",
                               "frac": ach / L2_RMW_GBS,
-                              "traffic_model": "4 passes x (read + write) of the working set through L2",
+                              "traffic_model": model,
                               "l2_bytes_per_step": l2_bytes,
                               "peak_source": "tools/microbench/mb.cu L2 rmw, 32 MB, this pool's B200"}
     if name in ISSUE_FLOOR:
