@@ -139,10 +139,11 @@ __device__ __forceinline__ void bfly_inpair(float& a, float& b) {
 #endif
 constexpr int kInpairFfma2MinR = SPN_INPAIR_FFMA2_MIN_R;
 
-template <int R, int BLO, int BHI>
+template <int R, int BLO, int BHI, bool REV = false>
 __device__ __forceinline__ void reg_fwht(float (&r)[R]) {
 #pragma unroll
-  for (int b = BLO; b < BHI; ++b) {
+  for (int bb = BLO; bb < BHI; ++bb) {
+    const int b = REV ? BLO + BHI - 1 - bb : bb;  // the stages commute: any order
     const int h = 1 << b;
     if (b == 0) {
       // FFMA2 halves the issue slots but occupies the FP32 pipe longer than two FADDs:
@@ -263,6 +264,10 @@ __device__ __forceinline__ void stsm_x4(uint32_t a, float r0, float r1, float r2
                "r"(__float_as_uint(r3))
                : "memory");
 }
+
+#ifndef SPN_F1_REV
+#define SPN_F1_REV 1
+#endif
 
 #ifndef SPN_XPOSE_MATRIX
 #define SPN_XPOSE_MATRIX 1
@@ -430,7 +435,7 @@ __device__ __forceinline__ void spinner_chain(float (&r)[C::R], float* sm, const
     for (int h = 0; h < 3; ++h) {
       xor_signs<C>(r, w);
       if (h < 2) load_words<C>(w, h == 0 ? w1p : w2p, tb, t);  // in flight during the butterflies
-      reg_fwht<C::R, 0, C::LOG_R>(r);
+      reg_fwht<C::R, 0, C::LOG_R, SPN_F1_REV>(r);
 #ifndef SPN_DBG_NOXPOSE  // (bound experiments only: wrong results)
       xpose_A_to_B<C>(r, sm, t);
 #endif
