@@ -969,8 +969,13 @@ spn_status host_pipeline(spn_plan* p, const float* x, int64_t batch, int64_t ld_
     const int64_t v = e ? std::atoll(e) : 128;  // config 3 (64 GiB in): 44.2 GB/s H2D vs 42.8 at 48 MB
     return v > 0 ? v : int64_t(128);
   }();
+  static const int64_t min_kb = [] {
+    const char* e = std::getenv("SPN_HOST_MIN_CHUNK_KB");
+    const int64_t v = e ? std::atoll(e) : 4096;
+    return v > 0 ? v : int64_t(4096);
+  }();
   const int64_t target = std::min<int64_t>(cap_mb << 20,
-                                           std::max<int64_t>(int64_t(4) << 20, batch * row_bytes / SPN_HOST_CHUNK_DIV));
+                                           std::max<int64_t>(min_kb << 10, batch * row_bytes / SPN_HOST_CHUNK_DIV));
   int64_t chunk = std::max<int64_t>(1, target / row_bytes);
   chunk = std::min(chunk, batch);
   static const int nst = [] {
