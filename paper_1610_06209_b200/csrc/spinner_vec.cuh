@@ -696,7 +696,10 @@ __device__ __forceinline__ int group_signed_argmax(const float (&r)[C::R], int f
   if (__any_sync(0xffffffffu, cand)) {
     int jb;
     float vb;
-    thread_first_hit<C>(r, M, first_i, stride_i, rows, full, jb, vb);
+    if (full)
+      thread_first_hit<C>(r, M, first_i, stride_i, rows, true, jb, vb);
+    else
+      thread_first_hit<C>(r, M, first_i, stride_i, rows, false, jb, vb);
     if (cand) key = argmax_key(first_i + jb * stride_i, vb, c);
   }
 #pragma unroll
@@ -728,7 +731,10 @@ __device__ __forceinline__ void cta_signed_argmax_post(const float (&r)[C::R], i
   if (__any_sync(0xffffffffu, cand)) {
     int jb;
     float vb;
-    thread_first_hit<C>(r, M, first_i, stride_i, rows, full, jb, vb);
+    if (full)
+      thread_first_hit<C>(r, M, first_i, stride_i, rows, true, jb, vb);
+    else
+      thread_first_hit<C>(r, M, first_i, stride_i, rows, false, jb, vb);
     if (cand) atomicMin(reinterpret_cast<int*>(red) + W + par, argmax_key(first_i + jb * stride_i, vb, c));
   }
 }
@@ -975,13 +981,19 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
             if (jb >= 0) argbest_merge(best, am, (int)row0 + jb * C::T + t, vb);
           }
           if (p.y && active) {
-            const bool all_rows = rows >= C::N;
+            // the full-block, no-ReLU case without per-element predicates (config 1)
+            if (rows >= C::N && !p.relu) {
 #pragma unroll
-            for (int j = 0; j < C::R; ++j) {
-              const int i = j * C::T + t;
-              float out = r[j] * p.c;
-              if (p.relu) out = fmaxf(out, 0.0f);
-              if (all_rows || i < rows) __stcs(yrow + i, out);
+              for (int j = 0; j < C::R; ++j) __stcs(yrow + j * C::T + t, r[j] * p.c);
+            } else {
+              const int nrows = (int)rows;
+#pragma unroll
+              for (int j = 0; j < C::R; ++j) {
+                const int i = j * C::T + t;
+                float out = r[j] * p.c;
+                if (p.relu) out = fmaxf(out, 0.0f);
+                if (i < nrows) __stcs(yrow + i, out);
+              }
             }
           }
           continue;
