@@ -466,9 +466,12 @@ ISSUE_FLOOR = {
     "c2": {"ms": 0.307, "mhz": 1965.0, "model": "5.95 K issue cycles per sample (1536 FADD2 x2, 768 FADD, 513 LOP3 + "
            "48 R2P sign flips, 96 STS + 75 LDS + 64 LDSM + 32 STSM, 416 FMUL, 256 MUFU, ~550 address/loop) over 60000 "
            "samples on 592 SMSPs (profiles/r02_c2_sass_mix.txt)"},
-    "c3": {"ms": 197.8, "mhz": 1965.0, "model": "27.4 K warp-issue cycles per (vector, table) (9216 FADD2 x2, 3072 "
-           "FADD, 1919 LOP3 + 192 R2P sign flips, 389 STS + 384 LDSM transposes, 576 LDG, 658 IMAD, argmax) over "
+    "c3": {"ms": 192.8, "mhz": 1965.0, "model": "26.7 K warp-issue cycles per (vector, table) (9216 FADD2 x2, 3072 "
+           "FADD, 1919 LOP3 + 192 R2P sign flips, 389 STS + 384 LDSM transposes, 576 LDG, 202 IMAD, argmax) over "
            "2^20 x 8 items on 592 SMSPs (profiles/r02_c3_sass_mix.txt)"},
+    "c1": {"ms": 0.0056, "mhz": 1965.0, "model": "1.58 K issue cycles per vector (384 FADD2 x2, 192 FADD, 124 LOP3 + 12 "
+           "R2P sign flips, 64 STS/LDS/LDSM/STSM, 35 LDG + 33 STG, argmax) over 4096 vectors on 592 SMSPs: one wave, "
+           "bound by each warp's own chain latency (profiles/r02_c1_sass_mix.txt)"},
 }
 
 # L2-resident read-modify-write bandwidth measured on this pool's B200 (tools/microbench/mb.cu, in-place
