@@ -24,7 +24,7 @@
 
 namespace spn {
 
-enum Op : int { OP_HASH = 0, OP_APPLY = 1, OP_EMBED_GAUSS = 2, OP_EMBED_ANG = 3, OP_EMBED_GAUSS_P = 4 };
+enum Op : int { OP_HASH = 0, OP_APPLY = 1, OP_EMBED_GAUSS = 2, OP_EMBED_ANG = 3, OP_EMBED_GAUSS_P = 4, OP_APPLY_P = 5 };
 enum Layout : int { LAY_B = 0, LAY_A = 1 };
 
 // One diagonal position (D1/D2/D3) in one layout, for every (table, block).
@@ -54,6 +54,7 @@ struct VecParams {
   int npeers;
   int64_t peer_row0;
   int vec_major;       // OP_HASH: all tables of a vector in one CTA, back to back (see the kernel)
+  int perm;            // host: run the apply + ids as OP_APPLY_P (permuted coordinates, 16-B x / y moves)
 };
 
 #ifndef SPN_EMBED_WARPS
@@ -76,7 +77,7 @@ struct VCfg {
   // apply; the embed kernels keep 24 (80 registers; at 72 they spill: 0.475 vs 0.443 ms)
   static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 28 : (R == 64 ? 12 : 12));
   __host__ __device__ static constexpr int min_ctas(int op) {
-    return (R == 32 && op >= 2) ? (SPN_EMBED_WARPS / (THREADS / 32) > 0 ? SPN_EMBED_WARPS / (THREADS / 32) : 1)
+    return (R == 32 && op >= 2 && op <= 4) ? (SPN_EMBED_WARPS / (THREADS / 32) > 0 ? SPN_EMBED_WARPS / (THREADS / 32) : 1)
                                 : MIN_CTAS_BASE;
   }
   // looped chain (one copy of the D -> H body, R == T only): keeps the n = 16384 kernel
@@ -478,6 +479,23 @@ __device__ __forceinline__ void load_x_B(float (&r)[C::R], const float* __restri
   }
 }
 
+// Load row v in layout B of PERMUTED coordinates (OP_APPLY_P, R == T, no padding, 16-B aligned rows):
+// the kernel's element e' = j*T + t is the real coordinate e = (j & 3) | (t << 2) | ((j >> 2) << (LOG_T + 2))
+// (H_n commutes with the bit permutation; the host permutes the diagonals to match, as for
+// OP_EMBED_GAUSS_P), so register quad q of lane t is the four consecutive floats at 4t + q * 4T: one
+// coalesced 16-B load each (a warp covers 512 contiguous bytes per instruction).
+template <class C>
+__device__ __forceinline__ void load_x_perm(float (&r)[C::R], const float* __restrict__ xrow, int t) {
+#pragma unroll
+  for (int q = 0; q < C::R / 4; ++q) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(xrow + q * 4 * C::T + 4 * t));
+    r[4 * q] = v.x;
+    r[4 * q + 1] = v.y;
+    r[4 * q + 2] = v.z;
+    r[4 * q + 3] = v.w;
+  }
+}
+
 // Per-thread signed argmax over this thread's registers, whose element indices
 // increase with j (both layouts).  Branch-free: pass 1 takes max |y| (FMNMX on the
 // ALU pipe), pass 2 walks j downward so the FIRST register reaching the max wins
@@ -682,10 +700,12 @@ __device__ __forceinline__ int key_to_id(int key, int64_t k) {
 }
 // Single-warp groups (T <= 32): group max by shuffles, the lanes holding it search their
 // registers, then a shuffle min over keys.  Returns the key in every thread of the group.
-template <class C>
+// QUAD > 0 (permuted coordinates, OP_APPLY_P): register j holds element (j & 3) + first_i + (j >> 2) * QUAD
+// (increasing in j); the caller guarantees every element is a valid row.
+template <class C, int QUAD = 0>
 __device__ __forceinline__ int group_signed_argmax(const float (&r)[C::R], int first_i, int stride_i, int rows,
                                                    float c) {
-  const bool full = first_i + (C::R - 1) * stride_i < rows;
+  const bool full = QUAD > 0 || first_i + (C::R - 1) * stride_i < rows;
   const float m = thread_absmax<C>(r, first_i, stride_i, rows, full);
   constexpr int LIM = C::T < 32 ? C::T : 32;
   float M = m;
@@ -700,7 +720,7 @@ __device__ __forceinline__ int group_signed_argmax(const float (&r)[C::R], int f
       thread_first_hit<C>(r, M, first_i, stride_i, rows, true, jb, vb);
     else
       thread_first_hit<C>(r, M, first_i, stride_i, rows, false, jb, vb);
-    if (cand) key = argmax_key(first_i + jb * stride_i, vb, c);
+    if (cand) key = argmax_key(QUAD > 0 ? (jb & 3) + first_i + (jb >> 2) * QUAD : first_i + jb * stride_i, vb, c);
   }
 #pragma unroll
   for (int off = LIM / 2; off > 0; off >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, off));
@@ -794,7 +814,10 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
   const int64_t per_vec = (OP == OP_HASH) ? p.tables : 1;
   const int64_t total = p.batch * per_vec;
   const int64_t stride = (int64_t)gridDim.x * C::GPC;
-  const bool want_ids = (OP == OP_HASH) || (OP == OP_APPLY && p.ids != nullptr);
+  constexpr bool APPLY = OP == OP_APPLY || OP == OP_APPLY_P;
+  constexpr bool PERM = OP == OP_APPLY_P;  // permuted coordinates: 16-B x loads and y stores
+  static_assert(!PERM || (LOG_R == LOG_T && LOG_R >= 2), "permuted apply needs R == T");
+  const bool want_ids = (OP == OP_HASH) || (APPLY && p.ids != nullptr);
   const bool staged = STAGE_X && p.x_vec_ok;
   // single-block tables take the two-phase argmax (group_signed_argmax / cta_signed_argmax_*);
   // multi-warp groups post each table's winner into smem and write its id one table later
@@ -927,7 +950,10 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
           for (int j = 0; j < C::R; ++j) r[j] = __int_as_float(0x3f800000 + j * 977 + t * 131 + (int)base);
         }
 #else
-        load_x_B<C>(r, xrow, p.n_in, t);
+        if constexpr (PERM)
+          load_x_perm<C>(r, xrow, t);
+        else
+          load_x_B<C>(r, xrow, p.n_in, t);
 #endif
         if constexpr (END_B) {
           if constexpr (C::T > 1) xpose_B_to_A<C>(r, sm, t);
@@ -966,6 +992,16 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
       } else {
         // layout B: element i = j*T + t -> coalesced stores
         float* yrow = p.y + v * p.ld_y + row0;
+        if constexpr (PERM) {  // full single-block rows (host-checked): 16-B stores, permuted argmax index
+          if (want_ids) fast_key = group_signed_argmax<C, 4 * C::T>(r, 4 * t, 0, (int)rows, p.c);
+          if (p.y && active) {
+#pragma unroll
+            for (int q = 0; q < C::R / 4; ++q)
+              __stcs(reinterpret_cast<float4*>(yrow + q * 4 * C::T + 4 * t),
+                     make_float4(r[4 * q] * p.c, r[4 * q + 1] * p.c, r[4 * q + 2] * p.c, r[4 * q + 3] * p.c));
+          }
+          continue;
+        }
         if constexpr (OP == OP_APPLY) {
           if (fast_ids) {
             if constexpr (DEFER) {

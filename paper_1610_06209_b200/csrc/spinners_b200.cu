@@ -304,7 +304,9 @@ spn_status run_vec(const spn_plan* p, int op, spn::VecParams& v, cudaStream_t s)
   if (items == 0) return SPN_OK;
   DeviceGuard g(p->device);
   const int signs = p->dsign[0] && p->dsign[1] && p->dsign[2];
-  cudaError_t e = vec_launcher(p->log_n, op, signs)(v, s, p->sms, items);
+  const spn::LaunchFn fn = (op == spn::OP_APPLY && v.perm) ? spn::vec_launcher_apply_perm()
+                                                           : vec_launcher(p->log_n, op, signs);
+  cudaError_t e = fn(v, s, p->sms, items);
   if (e != cudaSuccess) return cuda_fail(e, "spinner_vec_kernel launch");
   return SPN_OK;
 }
@@ -765,6 +767,19 @@ spn_status spn_hash_f32(const spn_plan* p, const float* x, int64_t batch, int64_
   v.ids = ids;
   v.y = y;
   v.ld_y = ld_y;
+  // hash + y at n = 1024 in permuted coordinates (16-B x loads and y stores): full single-block rows,
+  // sign diagonals, 16-B aligned rows (SPN_APPLY_PERM=0 turns it off)
+  static const bool perm_on = [] {
+    const char* e = std::getenv("SPN_APPLY_PERM");
+    return !(e && e[0] == '0');
+  }();
+  auto al16 = [](const void* q, int64_t ld) { return reinterpret_cast<uintptr_t>(q) % 16 == 0 && ld % 4 == 0; };
+  if (perm_on && y && ids && p->n == 1024 && p->vsgnP[0][0] && p->blocks == 1 && p->tables == 1 && p->m == 1024 &&
+      p->k == 1024 && n_in == 1024 && al16(x, ld_x) && al16(y, ld_y)) {
+    v.perm = 1;
+    for (int di = 0; di < 3; ++di)
+      for (int lay = 0; lay < 2; ++lay) v.d[di][lay].sgn = p->vsgnP[di][lay];
+  }
   return run_vec(p, y ? spn::OP_APPLY : spn::OP_HASH, v, static_cast<cudaStream_t>(stream));
   SPN_CATCH
 }

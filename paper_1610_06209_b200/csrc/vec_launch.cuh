@@ -26,6 +26,8 @@ LaunchFn vec_launcher_gauss(int log_n, int signs);
 LaunchFn vec_launcher_ang(int log_n, int signs);
 // n = 1024 Gaussian embed in permuted coordinates (16-B output stores), sign diagonals
 LaunchFn vec_launcher_gauss_perm();
+// n = 1024 apply + ids in permuted coordinates (16-B x loads and y stores), sign diagonals
+LaunchFn vec_launcher_apply_perm();
 
 // Persistent grid: min(work, SMs x resident CTAs per SM).
 template <int LOG_N, int OP, bool SIGNS>

@@ -60,6 +60,32 @@ def test_config1_hash_and_projection(spn, oracle, golden, torch):
     assert_ids(h.projector.plan.hash(x).cpu().numpy()[:, 0], golden["c1_ids"], gaps[:, 0])
 
 
+def test_config1_permuted_and_general_kernels_agree_with_reference(spn, oracle, golden, torch):
+    """16-B aligned rows take the permuted-coordinate n = 1024 hash + y kernel (OP_APPLY_P: 16-B x loads and
+    y stores, host-permuted sign masks); rows at a 4-B offset take the general kernel.  Both match the
+    reference: ids bit-exact except near-ties, y within RTOL, and the two agree to RTOL."""
+    c = cases.C1
+    sp = spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, c["n"], c["n"], c["n"], c["table_seed"], scale=1.0)
+    xs = golden["c1_x"]
+    d = oracle.realize(HD3, c["n"], c["n"], c["n"], c["table_seed"])
+    _, gaps = oracle.hash(*d, c["n"], c["n"], c["n"], 1, 1.0, xs)
+    b = xs.shape[0]
+    xa = dev(torch, xs)                                                   # aligned: permuted kernel
+    buf = torch.zeros(b * c["n"] + 1, device="cuda")
+    buf[1:] = xa.reshape(-1)
+    xu = buf[1:].view(b, c["n"])                                          # 4-B offset: general kernel
+    ya = torch.empty((b, c["n"]), device="cuda")
+    ybuf = torch.empty(b * c["n"] + 1, device="cuda")
+    yu = ybuf[1:].view(b, c["n"])
+    ida = sp.plan.hash(xa, y_out=ya).cpu().numpy()[:, 0]
+    idu = sp.plan.hash(xu, y_out=yu).cpu().numpy()[:, 0]
+    torch.cuda.synchronize()
+    for ids, y in ((ida, ya), (idu, yu)):
+        assert_ids(ids, golden["c1_ids"], gaps[:, 0])
+        assert row_rel(y.cpu().numpy(), golden["c1_y"]).max() <= RTOL
+    assert row_rel(ya.cpu().numpy(), yu.cpu().numpy()).max() <= RTOL
+
+
 def test_config2_random_features(spn, golden, torch):
     c = cases.C2
     sp = spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, c["n"], min(c["n"], c["k"]), c["k"], c["seed"])
