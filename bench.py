@@ -469,9 +469,9 @@ ISSUE_FLOOR = {
     "c3": {"ms": 192.8, "mhz": 1965.0, "model": "26.7 K warp-issue cycles per (vector, table) (9216 FADD2 x2, 3072 "
            "FADD, 1919 LOP3 + 192 R2P sign flips, 389 STS + 384 LDSM transposes, 576 LDG, 202 IMAD, argmax) over "
            "2^20 x 8 items on 592 SMSPs (profiles/r02_c3_sass_mix.txt)"},
-    "c1": {"ms": 0.0056, "mhz": 1965.0, "model": "1.58 K issue cycles per vector (384 FADD2 x2, 192 FADD, 124 LOP3 + 12 "
-           "R2P sign flips, 64 STS/LDS/LDSM/STSM, 35 LDG + 33 STG, argmax) over 4096 vectors on 592 SMSPs: one wave, "
-           "bound by each warp's own chain latency (profiles/r02_c1_sass_mix.txt)"},
+    "c1": {"ms": 0.00527, "mhz": 1965.0, "model": "1.50 K issue cycles per vector (384 FADD2 x2, 192 FADD, 125 LOP3 + 12 "
+           "R2P sign flips, 64 STS/LDS/LDSM/STSM, 8 LDG.128 + 8 STG.128 in permuted coordinates, argmax) over 4096 "
+           "vectors on 592 SMSPs: one wave, bound by each warp's own chain latency (profiles/r02_c1_sass_mix.txt)"},
 }
 
 # L2-resident read-modify-write bandwidth measured on this pool's B200 (tools/microbench/mb.cu, in-place
