@@ -92,6 +92,8 @@ def config_dict(name, world, scaling):
         "each rank a full batch)" if scaling == "weak" else
         ("columns sharded across ranks)" if name == "c4" else "batch sharded across ranks)")) + (
         " + all-gather of the codes" if name == "c3" and world > 1 else "")
+    d["l2"] = ("L2 flushed (256 MB write + read-back) between timed steps" if FLUSH.get(name)
+               else "inputs + outputs larger than the 126 MB L2")
     return d
 
 
