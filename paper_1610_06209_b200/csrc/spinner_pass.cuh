@@ -271,6 +271,9 @@ struct RowParams2 {
   int relu;
 };
 
+#ifndef SPN_ROW_STAGE_D
+#define SPN_ROW_STAGE_D 1
+#endif
 #ifndef SPN_ROW_DIRECT
 #define SPN_ROW_DIRECT 1  // c5: 1.321 -> 1.316 ms (3 A/B pairs)
 #endif
@@ -288,6 +291,10 @@ __global__ void __launch_bounds__(1 << LT) rowpass_staged_kernel(const RowParams
   extern __shared__ __align__(16) float smem[];
   float* xb = smem;                          // staging buffer (swizzled 16-B chunks)
   float* sm = DIRECT ? smem : smem + C::N;   // transpose buffer
+  // RP_MID: this segment's diagonal slice, copied by each thread (its own float4s, cp.async) at the
+  // start of the item so the L2 round trip overlaps the first H half instead of stalling after it
+  constexpr bool STAGE_D = SPN_ROW_STAGE_D && DIRECT && PROG == RP_MID;
+  float* db = sm + C::N;
   const int t = threadIdx.x;
   const int64_t items = p.nvec * p.nseg;
   const int lgseg = __ffsll(p.nseg) - 1;
@@ -304,6 +311,12 @@ __global__ void __launch_bounds__(1 << LT) rowpass_staged_kernel(const RowParams
   cp_async_commit();
   for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const int64_t v = item >> lgseg, seg = item & (p.nseg - 1);
+    if constexpr (STAGE_D) {
+      const float* dsrc = p.d + seg * C::N;
+#pragma unroll
+      for (int q = 0; q < C::R / 4; ++q) cp_async16(db + (q * C::T + t) * 4, dsrc + (q * C::T + t) * 4, 16);
+      cp_async_commit();
+    }
     float r[C::R];
     if constexpr (DIRECT) {
       const float* src = p.src + v * p.src_vstride + seg * C::N + t;
@@ -335,9 +348,10 @@ __global__ void __launch_bounds__(1 << LT) rowpass_staged_kernel(const RowParams
     if constexpr (PROG != RP_FIRST) fwht_B_to_A<C>(r, sm, t);
     if constexpr (PROG != RP_LAST) {
       const float4* f = reinterpret_cast<const float4*>(p.d + seg * C::N);
+      if constexpr (STAGE_D) cp_async_wait_all();  // this thread's own copies: no barrier needed
 #pragma unroll
       for (int q = 0; q < C::R / 4; ++q) {
-        const float4 dv = __ldg(f + q * C::T + t);
+        const float4 dv = STAGE_D ? reinterpret_cast<const float4*>(db)[q * C::T + t] : __ldg(f + q * C::T + t);
         r[4 * q] *= dv.x;
         r[4 * q + 1] *= dv.y;
         r[4 * q + 2] *= dv.z;
@@ -417,7 +431,7 @@ template <int LR, int LT, int PROG>
 inline cudaError_t launch_srow(const RowParams2& p, int sms, cudaStream_t s) {
   using C = VCfg<LR, LT>;
   auto kern = rowpass_staged_kernel<LR, LT, PROG>;
-  constexpr size_t smem = sizeof(float) * (RowCfg<PROG>::DIRECT ? 1 : 2) * C::N;
+  constexpr size_t smem = sizeof(float) * C::N * (RowCfg<PROG>::DIRECT ? (SPN_ROW_STAGE_D && PROG == RP_MID ? 2 : 1) : 2);
   static int occ = 0;
   if (occ == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
