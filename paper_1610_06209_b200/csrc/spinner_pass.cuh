@@ -351,7 +351,11 @@ __global__ void __launch_bounds__(1 << LT) rowpass_staged_kernel(const RowParams
       if constexpr (STAGE_D) cp_async_wait_all();  // this thread's own copies: no barrier needed
 #pragma unroll
       for (int q = 0; q < C::R / 4; ++q) {
+#ifdef SPN_DBG_NODIAG_ROW  // (bound experiments only: wrong results)
+        const float4 dv = make_float4(1.f, -1.f, 1.f, -1.f);
+#else
         const float4 dv = STAGE_D ? reinterpret_cast<const float4*>(db)[q * C::T + t] : __ldg(f + q * C::T + t);
+#endif
         r[4 * q] *= dv.x;
         r[4 * q + 1] *= dv.y;
         r[4 * q + 2] *= dv.z;

@@ -214,7 +214,11 @@ __global__ void __launch_bounds__(SColCfg<LS>::THREADS, TmaCfg<LS>::MIN_CTAS)
                                                              w * (C::R * 32)) + lane;
 #pragma unroll
           for (int q = 0; q < C::R / 4; ++q) {
+#ifdef SPN_DBG_NODIAG_COL  // (bound experiments only: wrong results)
+            const float4 dv = make_float4(1.f, -1.f, 1.f, -1.f);
+#else
             const float4 dv = __ldg(Dp + q * 32);
+#endif
             r[4 * q] *= dv.x;
             r[4 * q + 1] *= dv.y;
             r[4 * q + 2] *= dv.z;
