@@ -223,6 +223,11 @@ SPN_API spn_status spn_check_rows_f32(const float* x, int64_t batch, int64_t ld_
 SPN_API spn_status spn_hash_f32_peers(const spn_plan* plan, const float* x, int64_t batch, int64_t ld_x,
                                       int64_t n_in, int32_t* const* peers, int32_t npeers, int64_t row0,
                                       int64_t total, void* stream);
+/* Let kernels launched on `device` load/store memory that lives on `peer_device` (the peer
+ * tables of spn_hash_f32_peers on a multi-GPU node: cudaDeviceEnablePeerAccess from device's
+ * context; already enabled, or device == peer_device, is SPN_OK).  SPN_EUNSUPPORTED when the
+ * pair has no peer path (the caller then gathers with a collective instead). */
+SPN_API spn_status spn_enable_peer_access(int32_t device, int32_t peer_device);
 
 /* collision_curve / compare_families (lsh.cpp:38-96; lsh.hpp:38-75), the counting core.
  * plan: `trials` tables of make_hasher_factory(v, n, m) with table seeds mix_seed(seed, t)

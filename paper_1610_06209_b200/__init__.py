@@ -74,6 +74,7 @@ _plan_diagonals = _sig("spn_plan_diagonals", C.c_int, [_vp, _vp, _vp, _vp])
 _apply = _sig("spn_apply_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i32, _vp])
 _hash = _sig("spn_hash_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp])
 _hash_peers = _sig("spn_hash_f32_peers", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _i64, _i64, _vp])
+_enable_peer = _sig("spn_enable_peer_access", C.c_int, [_i32, _i32])
 _embed = _sig("spn_embed_f32", C.c_int, [_vp, _i32, _dbl, _vp, _i64, _i64, _i64, _vp, _i64, _vp])
 _sketch = _sig("spn_sketch_f32", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _dbl, _vp, _i64, _vp])
 _apply_host = _sig("spn_apply_f32_host", C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i32])
@@ -108,7 +109,7 @@ ABI_SYMBOLS = ("spn_status_string", "spn_last_error", "spn_version", "spn_plan_c
                "spn_gram_error_host", "spn_hash_f32_peers", "spn_fwht_f32", "spn_fwht_f32_host", "spn_diag_f32",
                "spn_diag_f32_host", "spn_circulant_create", "spn_circulant_destroy", "spn_circulant_apply_f32",
                "spn_circulant_apply_f32_host", "spn_hash_project_f32_host", "spn_sketch_f32_host", "spn_plan_resample",
-               "spn_plan_with_tail")
+               "spn_plan_with_tail", "spn_enable_peer_access")
 
 
 # ----------------------------------------------------------------------- errors

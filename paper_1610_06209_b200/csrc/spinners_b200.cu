@@ -823,6 +823,28 @@ spn_status spn_collision_hits_f32(const spn_plan* p, const float* xy, int64_t pa
   SPN_CATCH
 }
 
+spn_status spn_enable_peer_access(int32_t device, int32_t peer_device) { SPN_TRY
+  int count = 0;
+  SPN_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count || peer_device < 0 || peer_device >= count)
+    return fail(SPN_EINVAL, "peer access: device index out of range");
+  if (device == peer_device) return SPN_OK;
+  int can = 0;
+  SPN_CUDA(cudaDeviceCanAccessPeer(&can, device, peer_device));
+  if (!can)
+    return fail(SPN_EUNSUPPORTED, "no peer access from cuda:" + std::to_string(device) + " to cuda:" +
+                                      std::to_string(peer_device));
+  DeviceGuard g(device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    (void)cudaGetLastError();  // clear the (non-sticky) error state
+    return SPN_OK;
+  }
+  SPN_CUDA(e);
+  return SPN_OK;
+  SPN_CATCH
+}
+
 spn_status spn_hash_f32_peers(const spn_plan* p, const float* x, int64_t batch, int64_t ld_x, int64_t n_in,
                               int32_t* const* peers, int32_t npeers, int64_t row0, int64_t total,
                               void* stream) { SPN_TRY

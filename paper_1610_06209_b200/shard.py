@@ -67,11 +67,15 @@ class PeerCodes:
             # (NVLink / NVSwitch peer access); otherwise the caller falls back to NCCL all-gather
             devs = [None] * world
             dist.all_gather_object(devs, device)
+            from . import _check, _enable_peer
             for r, dev in enumerate(devs):
                 if r == rank or dev == device:
                     continue
                 if not torch.cuda.can_device_access_peer(device, dev):
                     raise RuntimeError(f"no peer access from cuda:{device} to rank {r}'s cuda:{dev}")
+                # the IPC mapping below lands in cuda:{dev}'s context; the hash kernel runs on
+                # cuda:{device}, which must be allowed to address that device's memory
+                _check(_enable_peer(device, dev))
             dist.all_gather_object(handles, reduce_tensor(self.table))
         peers = []
         for r in range(world):

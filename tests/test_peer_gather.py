@@ -88,3 +88,22 @@ def test_peer_hash_rejects_rows_outside_the_gathered_table():
     table = pc.hash(h, x, 50)  # rows 50..99: fits
     want = h.hash_ids(x)
     assert torch.equal(table[50:], want) and bool((table[:50] == -1).all())
+
+
+def test_enable_peer_access():
+    """spn_enable_peer_access: the hash kernel on cuda:d may store into a peer table on cuda:e only once
+    d's context has peer access to e (the IPC mapping itself lands in e's context).  Same device and
+    already-enabled pairs are no-ops; bad indices are refused; every peer-capable pair enables."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import paper_1610_06209_b200 as spn
+    assert spn._enable_peer(0, 0) == spn.SPN_OK
+    assert spn._enable_peer(0, torch.cuda.device_count()) == spn.SPN_EINVAL
+    assert spn._enable_peer(-1, 0) == spn.SPN_EINVAL
+    for d in range(torch.cuda.device_count()):
+        for e in range(torch.cuda.device_count()):
+            want = spn.SPN_OK if d == e or torch.cuda.can_device_access_peer(d, e) else spn.SPN_EUNSUPPORTED
+            assert spn._enable_peer(d, e) == want
+            assert spn._enable_peer(d, e) == want  # second call: already enabled
