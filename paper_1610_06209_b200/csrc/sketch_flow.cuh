@@ -30,6 +30,7 @@ namespace spn {
 
 struct FlowParams {
   int nstripes, G;
+  int nodep;  // bound experiments only (SPN_DBG_FLOW_NODEP): skip the dependency waits (wrong results)
   uint32_t ntasks;
   const float* d1;   // [N]
   const float* d2t;  // [N], D2 transposed for the high pass: d2t[lo * 2^lsb + s] = D2[(s << lsa) + lo]
@@ -52,6 +53,20 @@ struct FlowMaps {
 __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t cnt) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+#ifndef SPN_FLOW2_DEFER
+#define SPN_FLOW2_DEFER 1
+#endif
 __device__ __forceinline__ void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -82,6 +97,7 @@ __device__ __forceinline__ void tensor_load4_hint(float* sdst, const CUtensorMap
 
 template <int LSA, int LSB>
 struct FlowCfg {
+  static constexpr int LSA_ = LSA, LSB_ = LSB;
   static constexpr int LSM = LSA > LSB ? LSA : LSB;
   static constexpr int CTHREADS = 1 << LSM;      // consumers: one row of the task per thread
   static constexpr int THREADS = CTHREADS + 64;  // + the loader warp + the storer warp
@@ -93,6 +109,9 @@ struct FlowCfg {
   static constexpr int T_LO = (1 << LSB) / NSUB_LO;  // tasks per stripe, low pass
   static constexpr int T_HI = (1 << LSA) / NSUB_HI;  // tasks per stripe, high pass
 };
+
+template <class F>
+__host__ __device__ constexpr int LSA_of() { return F::LSA_; }
 
 struct FlowTask {
   int stripe, pass, idx;  // idx: task within (stripe, pass)
@@ -124,9 +143,8 @@ __device__ __forceinline__ FlowTask flow_decode(uint32_t t, const FlowParams& p)
 // One sub-tile (2^LS rows x 32 columns, row-major in buf) through NPARTS H's over its LS bits,
 // D (2^LS floats in smem, one per row) before part 1 when DMASK bit 1 / part 0 when bit 0,
 // start layout B if START_B; the result goes back to buf (row-major) scaled by `scale`.
-template <int LS, int NPARTS, int DMASK, bool START_B>
-__device__ __forceinline__ void flow_tile(float* buf, const float* dsm, int w, int lane, int bar, float scale) {
-  using C = SColCfg<LS>;
+template <class C, int NPARTS, int DMASK, bool START_B>
+__device__ __forceinline__ void flow_tile_c(float* buf, const float* dsm, int w, int lane, int bar, float scale) {
   float r[C::R];
   constexpr bool LB = START_B && C::W > 1;
 #pragma unroll
@@ -167,6 +185,11 @@ __device__ __forceinline__ void flow_tile(float* buf, const float* dsm, int w, i
   named_bar(bar, C::THREADS);
 }
 
+template <int LS, int NPARTS, int DMASK, bool START_B>
+__device__ __forceinline__ void flow_tile(float* buf, const float* dsm, int w, int lane, int bar, float scale) {
+  flow_tile_c<SColCfg<LS>, NPARTS, DMASK, START_B>(buf, dsm, w, lane, bar, scale);
+}
+
 // Roles: consumer warps (one row per thread) transform the tile in slot k; the loader warp
 // fetches tasks, waits on their dependencies and issues the TMA loads; the storer warp issues each
 // finished tile's TMA stores, frees the slot once the store has read it, and counts the tile for
@@ -199,15 +222,17 @@ __global__ void __launch_bounds__(FlowCfg<LSA, LSB>::THREADS, 1)
     const uint64_t pol_a = policy_evict_first();
     for (uint32_t k = 0;; ++k) {
       const int slot = (int)(k % NB);
-      if (k >= (uint32_t)NB) mbar_wait(&empty[slot], ((k / NB) - 1) & 1u);
+      // the task fetch and its dependency wait (two L2 round trips) come before the wait for the
+      // slot, so only the TMA load itself follows the slot's release
       const uint32_t t = atomicAdd(p.ctr, 1u);
       if (t >= p.ntasks) {
+        if (k >= (uint32_t)NB) mbar_wait(&empty[slot], ((k / NB) - 1) & 1u);
         tslot[slot] = -1;
         mbar_arrive(&full[slot]);
         return;
       }
       const FlowTask tk = flow_decode<F>(t, p);
-      if (tk.pass > 0) {  // every tile of the previous pass of this stripe is stored
+      if (tk.pass > 0 && !p.nodep) {  // every tile of the previous pass of this stripe is stored
         const uint32_t need = (tk.pass & 1) ? (1u << LSB) : (1u << LSA);  // sub-tiles of pass - 1
         const uint32_t* c = p.ctr + 1 + 4 * tk.stripe + (tk.pass - 1);
         // a dependency that never completes is a bug: abort the grid (a CUDA error) rather than hang the GPU
@@ -221,6 +246,7 @@ __global__ void __launch_bounds__(FlowCfg<LSA, LSB>::THREADS, 1)
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
+      if (k >= (uint32_t)NB) mbar_wait(&empty[slot], ((k / NB) - 1) & 1u);
       tslot[slot] = (int)t;
       float* buf = bufs + slot * (F::TILEB / 4);
       float* ds = dsl + slot * (F::DSB / 4);
@@ -325,18 +351,252 @@ __global__ void __launch_bounds__(FlowCfg<LSA, LSB>::THREADS, 1)
   bulk_wait_all();
 }
 
+// ------------------------------------------------------------------ two consumer groups
+// The one-group kernel above runs its 16 consumer warps in lock step over one task: shared-memory
+// phases (tile -> registers, the transposes, registers -> tile: ~384 KB per 64 KB task) and butterfly
+// phases alternate, so the SM's shared-memory pipe idles during the butterflies and its FP32 pipe
+// during the moves (~6.1 K cycles per task against ~3 K of shared-memory time and ~1.7 K of adds).
+// Here the consumers are two independent groups of 8 warps, each transforming a whole 64 KB task with
+// 64 rows per thread (SCol2Cfg: 6 register bits, so a 2^9-row tile still needs one transpose per H);
+// task k of the CTA's fetch order goes to group k & 1, and the groups drift out of phase so one
+// group's moves overlap the other's butterflies.  Same task order, counters, loader and storer.
+template <int LS_>
+struct SCol2Cfg {
+  static constexpr int LS = LS_;
+  static constexpr int LR = LS < 6 ? LS : 6;
+  static constexpr int LW = LS - LR;
+  static constexpr int R = 1 << LR, W = 1 << LW, S = 1 << LS;
+  static constexpr int THREADS = 32 * W;
+};
+
+template <int LSA, int LSB>
+struct Flow2Cfg {
+  using F = FlowCfg<LSA, LSB>;
+  static constexpr int NGROUPS = 2;
+  static constexpr int GTHREADS = 1 << (F::LSM - 1);  // 64 rows per thread
+  static constexpr int CTHREADS = NGROUPS * GTHREADS;
+  static constexpr int THREADS = CTHREADS + 64;
+  static constexpr bool OK = F::LSM == 9;  // 256-thread groups, three 64 KB slots
+};
+
+template <int LS, int NPARTS, int DMASK, bool START_B, bool GATHER, class F>
+__device__ __forceinline__ void flow2_task(const FlowParams& p, const FlowTask& tk, float* buf, const float* ds,
+                                           int g, int gtid, float scale) {
+  using C = SCol2Cfg<LS>;
+  constexpr int NSUB = 1 << (F::LSM - LS);
+  const int sub = gtid / C::THREADS, ltid = gtid % C::THREADS;
+  const int w = ltid >> 5, lane = ltid & 31;
+  float* sbuf = buf + sub * (C::S * 32);
+  flow_tile_c<C, NPARTS, DMASK, START_B>(sbuf, ds + sub * C::S, w, lane, NSUB > 1 ? 3 + 2 * g + sub : 1 + g, scale);
+  if constexpr (GATHER) {  // this sub-tile's sampled rows: out[rowmap[e]][stripe*32 + c], two rows per thread
+    const int ti = tk.idx * NSUB + sub;
+#pragma unroll
+    for (int h = 0; h < C::S / C::THREADS; ++h) {
+      const int row = ltid + h * C::THREADS;
+      const int64_t e = (int64_t)ti + ((int64_t)row << LSA_of<F>());
+      const int32_t orow = __ldg(p.rowmap + e);
+      if (orow >= 0) bulk_store(p.out + (int64_t)orow * p.ld_out + tk.stripe * 32, sbuf + row * 32, 128);
+      // W's row is dead after this pass: drop it from L2 without a write-back
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(p.w + tk.stripe * p.wstride + e * 32) : "memory");
+    }
+    bulk_commit();
+    bulk_wait_read();
+  }
+}
+
+template <int LSA, int LSB>
+__global__ void __launch_bounds__(Flow2Cfg<LSA, LSB>::THREADS, 1)
+    sketch_flow2_kernel(const FlowParams p, const __grid_constant__ FlowMaps mp) {
+  using F = FlowCfg<LSA, LSB>;
+  using F2 = Flow2Cfg<LSA, LSB>;
+  constexpr int NB = F::NB;
+  extern __shared__ __align__(128) float smem[];
+  float* bufs = smem;
+  float* dsl = smem + NB * (F::TILEB / 4);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NB * ((F::TILEB + F::DSB) / 4));
+  uint64_t* ready = full + NB;
+  uint64_t* empty = ready + NB;
+  int* tslot = reinterpret_cast<int*>(empty + NB);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&ready[b], 1);
+      mbar_init(&empty[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (tid == F2::CTHREADS) {  // ---------------------------------------------- loader
+    const uint64_t pol_a = policy_evict_first();
+    int ends = 0;
+    for (uint32_t k = 0;; ++k) {
+      const int slot = (int)(k % NB);
+      // the task fetch and its dependency wait (two L2 round trips) come before the wait for the
+      // slot, so only the TMA load itself follows the slot's release
+      const uint32_t t = ends ? p.ntasks : atomicAdd(p.ctr, 1u);
+      if (t >= p.ntasks) {  // one end marker per consumer group (consecutive k: one for each parity)
+        if (k >= (uint32_t)NB) mbar_wait(&empty[slot], ((k / NB) - 1) & 1u);
+        tslot[slot] = -1;
+        mbar_arrive(&full[slot]);
+        if (++ends == F2::NGROUPS) return;
+        continue;
+      }
+      const FlowTask tk = flow_decode<F>(t, p);
+      if (tk.pass > 0 && !p.nodep) {
+        const uint32_t need = (tk.pass & 1) ? (1u << LSB) : (1u << LSA);
+        const uint32_t* c = p.ctr + 1 + 4 * tk.stripe + (tk.pass - 1);
+        uint64_t t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (ld_acquire(c) < need) {
+          __nanosleep(100);
+          uint64_t t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if (t1 - t0 > 5000000000ull) __trap();
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      if (k >= (uint32_t)NB) mbar_wait(&empty[slot], ((k / NB) - 1) & 1u);
+      tslot[slot] = (int)t;
+      float* buf = bufs + slot * (F::TILEB / 4);
+      float* ds = dsl + slot * (F::DSB / 4);
+      const bool low = (tk.pass & 1) == 0;
+      const int LS = low ? LSA : LSB;
+      const int nsub = low ? F::NSUB_LO : F::NSUB_HI;
+      const int box = LS > 8 ? 256 : (1 << LS), nbox = (1 << LS) / box;
+      const float* dsrc = tk.pass == 0 ? p.d1 : (tk.pass == 1 ? p.d2t : (tk.pass == 2 ? p.d3 : nullptr));
+      const uint32_t bytes = (uint32_t)F::TILEB + (dsrc ? (uint32_t)nsub * (4u << LS) : 0u);
+      mbar_arrive_tx(&full[slot], bytes);
+      for (int sb = 0; sb < nsub; ++sb) {
+        const int ti = tk.idx * nsub + sb;
+        float* sbuf = buf + sb * ((1 << LS) * 32);
+        for (int b = 0; b < nbox; ++b) {
+          if (tk.pass == 0)
+            tensor_load4_hint(sbuf + b * box * 32, &mp.a, tk.stripe * 32, 0, (ti << LSA) + b * box, 0, &full[slot],
+                              pol_a);
+          else if (low)
+            tensor_load4(sbuf + b * box * 32, &mp.wlo, 0, 0, (ti << LSA) + b * box, tk.stripe, &full[slot]);
+          else
+            tensor_load4(sbuf + b * box * 32, &mp.whi, 0, ti, b * box, tk.stripe, &full[slot]);
+        }
+        if (dsrc) bulk_load(ds + sb * (1 << LS), dsrc + ((int64_t)ti << LS), 4u << LS, &full[slot]);
+      }
+    }
+  }
+  if (tid == F2::CTHREADS + 32) {  // ------------------------------------------- storer
+    uint32_t* pend_ctr = nullptr;
+    uint32_t pend_n = 0;
+    for (uint32_t k = 0;; ++k) {
+      const int slot = (int)(k % NB);
+      mbar_wait(&ready[slot], (k / NB) & 1u);
+      const int t = tslot[slot];
+      if (t < 0) break;
+      const FlowTask tk = flow_decode<F>((uint32_t)t, p);
+      if (tk.pass == 3) {
+        mbar_arrive(&empty[slot]);
+        if (pend_ctr) {  // nothing of this task to store: complete the deferred count now
+          bulk_wait_all();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          red_release_add(pend_ctr, pend_n);
+          pend_ctr = nullptr;
+        }
+        continue;
+      }
+      const bool low = (tk.pass & 1) == 0;
+      const int LS = low ? LSA : LSB;
+      const int nsub = low ? F::NSUB_LO : F::NSUB_HI;
+      const int box = LS > 8 ? 256 : (1 << LS), nbox = (1 << LS) / box;
+      float* buf = bufs + slot * (F::TILEB / 4);
+      for (int sb = 0; sb < nsub; ++sb) {
+        const int ti = tk.idx * nsub + sb;
+        float* sbuf = buf + sb * ((1 << LS) * 32);
+        for (int b = 0; b < nbox; ++b) {
+          if (low)
+            tensor_store4(&mp.wlo, 0, 0, (ti << LSA) + b * box, tk.stripe, sbuf + b * box * 32);
+          else
+            tensor_store4(&mp.whi, 0, ti, b * box, tk.stripe, sbuf + b * box * 32);
+        }
+      }
+      bulk_commit();
+      bulk_wait_read();
+      mbar_arrive(&empty[slot]);
+      if (pend_ctr) {  // the deferred task's store was committed before this one: at most 1 group pending
+        bulk_wait_n1();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        red_release_add(pend_ctr, pend_n);
+        pend_ctr = nullptr;
+      }
+      uint32_t* myctr = p.ctr + 1 + 4 * tk.stripe + tk.pass;
+      // If the next task is already computed, issue its store before waiting for this store to
+      // complete (the count is deferred by one task; never while the next task is still waiting on
+      // anything, so a dependent of this task cannot be what holds it up).
+      const int nslot = (int)((k + 1) % NB);
+      if (SPN_FLOW2_DEFER && mbar_test(&ready[nslot], ((k + 1) / NB) & 1u) && tslot[nslot] >= 0) {
+        pend_ctr = myctr;
+        pend_n = (uint32_t)nsub;
+        continue;
+      }
+      bulk_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      red_release_add(myctr, (uint32_t)nsub);
+    }
+    if (pend_ctr) {
+      bulk_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      red_release_add(pend_ctr, pend_n);
+    }
+    return;
+  }
+  if (tid >= F2::CTHREADS) return;
+
+  // ---------------------------------------------------------------------- consumers
+  const int g = tid / F2::GTHREADS, gtid = tid % F2::GTHREADS;
+  for (uint32_t k = (uint32_t)g;; k += F2::NGROUPS) {
+    const int slot = (int)(k % NB);
+    mbar_wait(&full[slot], (k / NB) & 1u);
+    const int t = tslot[slot];
+    if (t < 0) {
+      if (gtid == 0) mbar_arrive(&ready[slot]);  // lets the storer see the end
+      break;
+    }
+    const FlowTask tk = flow_decode<F>((uint32_t)t, p);
+    float* buf = bufs + slot * (F::TILEB / 4);
+    const float* ds = dsl + slot * (F::DSB / 4);
+    switch (tk.pass) {  // P0: D1 H | P1: H D2 H (start B) | P2: H D3 H (start B) | P3: H + gather
+      case 0: flow2_task<LSA, 1, 1, false, false, F>(p, tk, buf, ds, g, gtid, 1.0f); break;
+      case 1: flow2_task<LSB, 2, 2, true, false, F>(p, tk, buf, ds, g, gtid, 1.0f); break;
+      case 2: flow2_task<LSA, 2, 2, true, false, F>(p, tk, buf, ds, g, gtid, 1.0f); break;
+      default: flow2_task<LSB, 1, 0, false, true, F>(p, tk, buf, ds, g, gtid, p.cscale); break;
+    }
+    named_bar(1 + g, F2::GTHREADS);  // the whole task is computed (and its gather stores have read smem)
+    if (gtid == 0) mbar_arrive(&ready[slot]);
+  }
+  bulk_wait_all();
+}
+
 // ------------------------------------------------------------------------- host side
 inline int flow_mode();
 inline bool flow_enabled() { return flow_mode() != 0; }
-// stripes per wave (L2 working set = G x 16 MB at N = 2^17); config 4: G = 2 0.191 ms, 3 0.174 ms
-// (DRAM 157 MB = 1.15x algorithmic), 4 0.170 ms (290 MB: the workspace starts spilling from L2)
+// Stripes per wave.  The L2 working set is G stripes of N x 32 floats (16 MB at N = 2^17); a pass of a
+// stripe can start only when the stripe's previous pass is complete, so the G - 1 other stripes'
+// tasks between them must cover the tasks in flight on the grid (~450: 3 per SM).  Config 4, one
+// consumer group: G = 2 0.191 ms, 3 0.174 ms (DRAM 157 MB = 1.15x algorithmic), 4 0.170 ms (290 MB: the
+// workspace starts spilling from L2); two consumer groups: G = 2 0.184, 3 0.159, 4 0.148 ms (= the
+// time without any dependency wait, SPN_DBG_FLOW_NODEP), 8 0.174 ms.  SPN_FLOW_G overrides (0 = auto).
 inline int flow_waves_g() {
   static const int g = [] {
     const char* e = std::getenv("SPN_FLOW_G");
-    const int v = e ? std::atoi(e) : 3;
-    return v < 1 ? 1 : v;
+    const int v = e ? std::atoi(e) : 0;
+    return v < 0 ? 0 : v;
   }();
   return g;
+}
+inline int flow_auto_g(int64_t stripe_bytes, int tasks_per_stripe_pass, bool two_groups) {
+  const int64_t budget = (two_groups ? 64ll : 48ll) << 20;
+  const int by_l2 = (int)(budget / stripe_bytes);
+  const int by_dep = 1 + (512 + tasks_per_stripe_pass - 1) / tasks_per_stripe_pass;
+  return std::max(2, std::max(by_l2, by_dep));
 }
 
 template <int LSA, int LSB>
@@ -352,6 +612,24 @@ inline cudaError_t launch_flow_t(FlowParams fp, const float* a, int64_t n_in, in
   if (!encode_view(&mp.wlo, fp.w, 32, 32, 0, nn, fp.nstripes, fp.wstride, box_lo)) return cudaSuccess;
   if (!encode_view(&mp.whi, fp.w, 32, 32, LSA, int64_t(1) << LSB, fp.nstripes, fp.wstride, box_hi))
     return cudaSuccess;
+  fp.ntasks = (uint32_t)fp.nstripes * (2 * F::T_LO + 2 * F::T_HI);
+  const bool two = Flow2Cfg<LSA, LSB>::OK && flow_mode() == 2;
+  if (fp.G <= 0) fp.G = flow_auto_g(nn * 32 * 4, std::min(F::T_LO, F::T_HI), two);
+  if constexpr (Flow2Cfg<LSA, LSB>::OK) {
+    if (two) {  // two consumer groups (one CTA per SM)
+      auto kern2 = sketch_flow2_kernel<LSA, LSB>;
+      static bool attr2 = false;
+      if (!attr2) {
+        cudaError_t e = cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM);
+        if (e != cudaSuccess) return e;
+        attr2 = true;
+      }
+      const int64_t grid2 = std::min<int64_t>(int64_t(sms), fp.ntasks);
+      kern2<<<(unsigned)grid2, Flow2Cfg<LSA, LSB>::THREADS, F::SMEM, s>>>(fp, mp);
+      *done = true;
+      return cudaGetLastError();
+    }
+  }
   auto kern = sketch_flow_kernel<LSA, LSB>;
   static bool attr = false;
   if (!attr) {
@@ -362,21 +640,21 @@ inline cudaError_t launch_flow_t(FlowParams fp, const float* a, int64_t n_in, in
   int occ = 1;
   if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, F::THREADS, F::SMEM)) return e;
   occ = occ < 1 ? 1 : occ;
-  fp.ntasks = (uint32_t)fp.nstripes * (2 * F::T_LO + 2 * F::T_HI);
   const int64_t grid = std::min<int64_t>(int64_t(sms) * occ, fp.ntasks);
   kern<<<(unsigned)grid, F::THREADS, F::SMEM, s>>>(fp, mp);
   *done = true;
   return cudaGetLastError();
 }
 
-// 1: the dataflow kernel (default), 0: grouped pass launches.  (A register-direct variant — tiles
+// 2 (default): the dataflow kernel with two consumer groups where it exists (2^9-row tiles, N = 2^17
+// and 2^18), else the one-group kernel; 1: the one-group kernel; 0: grouped pass launches.  (A register-direct variant — tiles
 // moved global <-> registers with LDG/STG, smem only for transposes, the next tile prefetched into a
 // second register set — measured 0.286 vs 0.172 ms at config 4 and was dropped: at 128 registers
 // and one 512-thread CTA per SM the direct loads cannot keep enough bytes in flight.)
 inline int flow_mode() {
   static const int m = [] {
     const char* e = std::getenv("SPN_FLOW");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   return m;
 }
