@@ -360,6 +360,16 @@ __global__ void __launch_bounds__(FlowCfg<LSA, LSB>::THREADS, 1)
 // 64 rows per thread (SCol2Cfg: 6 register bits, so a 2^9-row tile still needs one transpose per H);
 // task k of the CTA's fetch order goes to group k & 1, and the groups drift out of phase so one
 // group's moves overlap the other's butterflies.  Same task order, counters, loader and storer.
+// (Tried on top of this and dropped: passes 0-2 storing their results straight from registers, one
+// 128-B stripe row per warp instruction, with the slot released right after the last transpose read
+// and a per-warp release count: correct, a third less shared-memory traffic per task and no storer
+// warp, but 0.174 vs 0.147 ms at config 4 — 0.166 even with the release fence removed: the 64 STG
+// per thread cost more than the staged TMA store.  And a ring of six 32 KB units instead of three
+// 64 KB slots for the 9 + 8 bit split — a high-pass task one 256-row sub-tile in one unit on a whole
+// group (8 warps x 32 rows per thread), a low-pass task two units, a published (task, unit) queue —
+// so that the high passes hold two units and keep four loading: correct, but 0.179 ms (0.174 without
+// dependency waits): at 32 rows per thread the phases between the group barriers are half as long
+// and the barriers cost more than the extra loads in flight save.)
 template <int LS_>
 struct SCol2Cfg {
   static constexpr int LS = LS_;
@@ -613,7 +623,7 @@ inline cudaError_t launch_flow_t(FlowParams fp, const float* a, int64_t n_in, in
   if (!encode_view(&mp.whi, fp.w, 32, 32, LSA, int64_t(1) << LSB, fp.nstripes, fp.wstride, box_hi))
     return cudaSuccess;
   fp.ntasks = (uint32_t)fp.nstripes * (2 * F::T_LO + 2 * F::T_HI);
-  const bool two = Flow2Cfg<LSA, LSB>::OK && flow_mode() == 2;
+  const bool two = Flow2Cfg<LSA, LSB>::OK && flow_mode() >= 2;
   if (fp.G <= 0) fp.G = flow_auto_g(nn * 32 * 4, std::min(F::T_LO, F::T_HI), two);
   if constexpr (Flow2Cfg<LSA, LSB>::OK) {
     if (two) {  // two consumer groups (one CTA per SM)
