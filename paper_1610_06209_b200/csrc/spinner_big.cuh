@@ -1107,6 +1107,8 @@ inline spn_status sketch_run(int64_t nn, const std::vector<double>* d, const int
     fp.G = flow_waves_g();
     static const int nodep = [] { const char* e = std::getenv("SPN_DBG_FLOW_NODEP"); return e ? std::atoi(e) : 0; }();
     fp.nodep = nodep;
+    static const int wlast = [] { const char* e = std::getenv("SPN_FLOW_WLAST"); return e ? std::atoi(e) : 1; }();
+    fp.wlast = wlast;
     fp.d1 = d1;
     fp.d2t = bp->sk_d[1];
     fp.d3 = bp->sk_d[2];

@@ -16,7 +16,7 @@ lines = [ln for ln in open(path).read().splitlines() if ln.startswith('"')]
 per = collections.OrderedDict()
 for r in csv.DictReader(io.StringIO("\n".join(lines))):
     per.setdefault(r["ID"], {"kernel": r["Kernel Name"]})[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
-hot = [v for v in per.values() if "spinner_vec" in v["kernel"] or "pass" in v["kernel"]]
+hot = [v for v in per.values() if "spinner_vec" in v["kernel"] or "pass" in v["kernel"] or "sketch_flow" in v["kernel"]]
 step = hot[-per_step:]
 rd = sum(v["dram__bytes_read.sum"] for v in step)
 wr = sum(v["dram__bytes_write.sum"] for v in step)
