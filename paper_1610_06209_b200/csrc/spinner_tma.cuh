@@ -125,6 +125,23 @@ __device__ __forceinline__ void tensor_store4(const CUtensorMap* m, int c0, int 
 #define SPN_TMA_NBUF 2
 #endif
 
+// Tile config of the TMA column pass: 32 rows per thread (5 register bits).  SPN_TCOL_LR8 = 6 runs the
+// 2^8-row tiles with 64 rows per thread on 4 warps instead (three CTAs of 128 threads per SM instead of
+// two of 256, longer phases between the CTA barriers, three tiles loading per SM instead of two):
+// measured equal (c5 1.290 vs 1.289 ms, grouped c4 passes 0.189 vs 0.187 ms), so the default stays 5.
+#ifndef SPN_TCOL_LR8
+#define SPN_TCOL_LR8 5
+#endif
+template <int LS_>
+struct TColCfg {
+  static constexpr int LS = LS_;
+  static constexpr int LR = LS == 8 ? SPN_TCOL_LR8 : (LS < 5 ? LS : 5);
+  static constexpr int LW = LS - LR;
+  static constexpr int R = 1 << LR, W = 1 << LW, S = 1 << LS;
+  static constexpr int THREADS = 32 * W;
+  static constexpr int RPT = S / THREADS;  // tile rows per thread in the per-row epilogues
+};
+
 template <int LS>
 struct TmaCfg {
   static constexpr size_t TILE = sizeof(float) * (size_t(1) << LS) * 32;
@@ -133,7 +150,7 @@ struct TmaCfg {
   static constexpr int BOX = LS > 8 ? 256 : (1 << LS);  // rows per tensor copy
   static constexpr int NBOX = (1 << LS) / BOX;
   static constexpr int BY_SMEM = (int)((227u * 1024u) / SMEM);
-  static constexpr int BY_REGS = 512 / SColCfg<LS>::THREADS;
+  static constexpr int BY_REGS = 512 / TColCfg<LS>::THREADS;
   static constexpr int M0 = BY_SMEM < BY_REGS ? BY_SMEM : BY_REGS;
   static constexpr int MIN_CTAS = M0 < 1 ? 1 : M0;
 };
@@ -150,13 +167,12 @@ __device__ __forceinline__ void tma_issue_tile(const CUtensorMap* m, const TileI
 }
 
 template <int LS, int NPARTS, int DMASK, bool START_B, int DMODE, int EPI>
-__global__ void __launch_bounds__(SColCfg<LS>::THREADS, TmaCfg<LS>::MIN_CTAS)
+__global__ void __launch_bounds__(TColCfg<LS>::THREADS, TmaCfg<LS>::MIN_CTAS)
     colpass_tma_kernel(const ColParams p, const __grid_constant__ TmaMaps tm) {
   pdl_enter();
-  using C = SColCfg<LS>;
+  using C = TColCfg<LS>;
   using T = TmaCfg<LS>;
   constexpr int NB = T::NBUF;  // tiles in flight: NB-1 loads ahead of the compute
-  static_assert(C::THREADS == C::S, "one row per thread");
   // tile buffers at the dynamic-smem base (tensor copies need 128-B aligned smem), barriers after them
   extern __shared__ __align__(128) float smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NB * (C::S * 32));
@@ -191,11 +207,14 @@ __global__ void __launch_bounds__(SColCfg<LS>::THREADS, TmaCfg<LS>::MIN_CTAS)
       for (int j = 0; j < C::R; ++j) r[j] = buf[scol_s<C>(LB, w, j) * 32 + lane];
     }
     if constexpr (EPI == EPI_GATHER) {
-      if (p.discard_src) {  // this row of the workspace is dead now: no write-back to HBM
-        const int64_t e = cti.e0 + ((int64_t)threadIdx.x << p.s0);
-        const int64_t off = e * p.src_ld + (int64_t)cti.cs * 32;
-        if (off + 32 <= p.src_valid)
-          asm volatile("discard.global.L2 [%0], 128;" ::"l"(p.src + (int64_t)cti.v * p.src_vstride + off) : "memory");
+      if (p.discard_src) {  // these rows of the workspace are dead now: no write-back to HBM
+#pragma unroll
+        for (int h = 0; h < C::RPT; ++h) {
+          const int64_t e = cti.e0 + ((int64_t)(threadIdx.x + h * C::THREADS) << p.s0);
+          const int64_t off = e * p.src_ld + (int64_t)cti.cs * 32;
+          if (off + 32 <= p.src_valid)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(p.src + (int64_t)cti.v * p.src_vstride + off) : "memory");
+        }
       }
     }
     bulk_wait_read();  // my bulk stores out of the buffer about to be refilled have read it
@@ -278,19 +297,22 @@ __global__ void __launch_bounds__(SColCfg<LS>::THREADS, TmaCfg<LS>::MIN_CTAS)
         bulk_commit();
       }
     } else {
-      const int s = threadIdx.x;
-      const int64_t e = cti.e0 + ((int64_t)s << p.s0);
-      if constexpr (EPI == EPI_GATHER) {
-        const int32_t orow = __ldg(p.rowmap + e);
-        if (orow >= 0) bulk_store(p.dst + (int64_t)orow * p.ld_out + (int64_t)cti.cs * 32, buf + s * 32, 128);
-      } else {
-        const int64_t f = e * p.dst_ld + (int64_t)cti.cs * 32;
-        float* drow = p.dst + (int64_t)cti.v * p.dst_vstride + f;
-        if (EPI == EPI_STORE || f + 32 <= p.rows_valid) {
-          bulk_store(drow, buf + s * 32, 128);
+#pragma unroll
+      for (int h = 0; h < C::RPT; ++h) {
+        const int s = threadIdx.x + h * C::THREADS;
+        const int64_t e = cti.e0 + ((int64_t)s << p.s0);
+        if constexpr (EPI == EPI_GATHER) {
+          const int32_t orow = __ldg(p.rowmap + e);
+          if (orow >= 0) bulk_store(p.dst + (int64_t)orow * p.ld_out + (int64_t)cti.cs * 32, buf + s * 32, 128);
         } else {
-          for (int q = 0; q < 32; ++q)
-            if (f + q < p.rows_valid) drow[q] = buf[s * 32 + q];
+          const int64_t f = e * p.dst_ld + (int64_t)cti.cs * 32;
+          float* drow = p.dst + (int64_t)cti.v * p.dst_vstride + f;
+          if (EPI == EPI_STORE || f + 32 <= p.rows_valid) {
+            bulk_store(drow, buf + s * 32, 128);
+          } else {
+            for (int q = 0; q < 32; ++q)
+              if (f + q < p.rows_valid) drow[q] = buf[s * 32 + q];
+          }
         }
       }
       bulk_commit();
@@ -303,7 +325,7 @@ __global__ void __launch_bounds__(SColCfg<LS>::THREADS, TmaCfg<LS>::MIN_CTAS)
 // described as tensor views (the caller then uses the cp.async pass).
 template <int LS, int NPARTS, int DMASK, bool START_B, int DMODE, int EPI>
 inline cudaError_t launch_tcol(const ColParams& p_in, int sms, cudaStream_t s, bool* done) {
-  using C = SColCfg<LS>;
+  using C = TColCfg<LS>;
   using T = TmaCfg<LS>;
   *done = false;
   ColParams p = p_in;
