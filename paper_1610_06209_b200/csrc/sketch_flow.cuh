@@ -562,6 +562,7 @@ __global__ void __launch_bounds__(Flow2Cfg<LSA, LSB>::THREADS, 1)
   const int g = tid / F2::GTHREADS, gtid = tid % F2::GTHREADS;
   for (uint32_t k = (uint32_t)g;; k += F2::NGROUPS) {
     const int slot = (int)(k % NB);
+    // (one warp polling and the others asleep in the group barrier measured the same: 0.148 ms)
     mbar_wait(&full[slot], (k / NB) & 1u);
     const int t = tslot[slot];
     if (t < 0) {

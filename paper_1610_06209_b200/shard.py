@@ -62,28 +62,53 @@ class PeerCodes:
         self.table = torch.full((total, tables), -1, dtype=torch.int32, device=f"cuda:{device}")
         torch.cuda.synchronize(device)  # the fill must land before any peer can write into the table
         handles = [None] * world
+
+        def agree(ok, what, exc=None):
+            # every rank must take the same branch (a rank that raises alone would leave the others
+            # waiting in the next collective): share the outcome and fail together
+            flags = [None] * world
+            dist.all_gather_object(flags, (bool(ok), "" if exc is None else f"{type(exc).__name__}: {exc}"))
+            bad = [(r, m) for r, (f, m) in enumerate(flags) if not f]
+            if bad:
+                raise RuntimeError(f"{what} failed on rank(s) " + ", ".join(f"{r} ({m})" for r, m in bad))
+
         if world > 1:
             # P2P capability first: every peer table must be directly addressable from this GPU
             # (NVLink / NVSwitch peer access); otherwise the caller falls back to NCCL all-gather
             devs = [None] * world
             dist.all_gather_object(devs, device)
             from . import _check, _enable_peer
-            for r, dev in enumerate(devs):
-                if r == rank or dev == device:
-                    continue
-                if not torch.cuda.can_device_access_peer(device, dev):
-                    raise RuntimeError(f"no peer access from cuda:{device} to rank {r}'s cuda:{dev}")
-                # the IPC mapping below lands in cuda:{dev}'s context; the hash kernel runs on
-                # cuda:{device}, which must be allowed to address that device's memory
-                _check(_enable_peer(device, dev))
+            exc = None
+            try:
+                for r, dev in enumerate(devs):
+                    if r == rank or dev == device:
+                        continue
+                    if not torch.cuda.can_device_access_peer(device, dev):
+                        raise RuntimeError(f"no peer access from cuda:{device} to rank {r}'s cuda:{dev}")
+                    # the IPC mapping below lands in cuda:{dev}'s context; the hash kernel runs on
+                    # cuda:{device}, which must be allowed to address that device's memory
+                    _check(_enable_peer(device, dev))
+            except Exception as e:  # noqa: BLE001 - reported through agree()
+                exc = e
+            agree(exc is None, "peer access", exc)
             dist.all_gather_object(handles, reduce_tensor(self.table))
         peers = []
-        for r in range(world):
-            if r == rank:
-                peers.append(self.table)
-            else:
-                fn, args = handles[r]
-                peers.append(fn(*args))  # maps rank r's table into this process (cudaIpcOpenMemHandle)
+        exc = None
+        try:
+            for r in range(world):
+                if r == rank:
+                    peers.append(self.table)
+                else:
+                    fn, args = handles[r]
+                    peers.append(fn(*args))  # maps rank r's table into this process (cudaIpcOpenMemHandle)
+        except Exception as e:  # noqa: BLE001
+            exc = e
+        if world > 1:
+            if exc is not None:
+                peers = []
+            agree(exc is None, "mapping the peer tables", exc)
+        elif exc is not None:
+            raise exc
         self._peers = peers  # keep the mappings alive
         self.ptrs = torch.tensor([t.data_ptr() for t in peers], dtype=torch.int64, device=f"cuda:{device}")
 
