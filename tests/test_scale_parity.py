@@ -268,6 +268,22 @@ def test_dataflow_sketch_shapes_match_reference(spn, ref, torch, input_dim, d, r
         assert row_rel(got.T, want.T).max() <= RTOL, mode
 
 
+@pytest.mark.parametrize("input_dim,d,rows", [(1 << 17, 96, 1024), (150000, 64, 700), (1 << 17, 288, 2048)])
+def test_two_group_dataflow_sketch_repeatable(spn, ref, torch, input_dim, d, rows):
+    """The two-consumer-group dataflow kernel (2^9-row tiles: N = 2^17 and 2^18; stripe counts below, equal
+    to and above the wave size) run 25 times back to back on one plan: every run bit-identical (the tasks'
+    order of execution differs from run to run, the arithmetic must not) and equal to the reference."""
+    rng = np.random.default_rng(input_dim + 7 * d)
+    a = rng.standard_normal((input_dim, d)).astype(np.float32)
+    sk = spn.SketchOperator(spn.SpinnerVariant.hd3_hd2_hd1, input_dim, rows, 23, mode="random", p_seed=9)
+    ad = torch.from_numpy(a).cuda()
+    first = sk.apply(ad).clone()
+    for _ in range(24):
+        assert torch.equal(sk.apply(ad), first)
+    want = ref.sketch(HD3, a, rows, 23, row_list=sk.row_list, threads=THREADS)
+    assert row_rel(first.cpu().numpy().T, want.T).max() <= RTOL
+
+
 def test_host_entry_points_reject_device_pointers(spn, torch):
     """The _host entry points copy through pinned staging / cudaMemcpy: a device pointer is refused
     (SPN_EINVAL) instead of being memcpy'd on the host."""
