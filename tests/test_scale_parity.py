@@ -268,9 +268,9 @@ def test_dataflow_sketch_shapes_match_reference(spn, ref, torch, input_dim, d, r
         assert row_rel(got.T, want.T).max() <= RTOL, mode
 
 
-@pytest.mark.parametrize("input_dim,d,rows", [(1 << 17, 96, 1024), (150000, 64, 700), (1 << 17, 288, 2048)])
+@pytest.mark.parametrize("input_dim,d,rows", [(1 << 17, 32, 256), (1 << 17, 96, 1024), (150000, 64, 700), (1 << 17, 288, 2048)])
 def test_two_group_dataflow_sketch_repeatable(spn, ref, torch, input_dim, d, rows):
-    """The two-consumer-group dataflow kernel (2^9-row tiles: N = 2^17 and 2^18; stripe counts below, equal
+    """The two-consumer-group dataflow kernel (2^9-row tiles: N = 2^17 and 2^18; stripe counts below (1 and 2), equal
     to and above the wave size) run 25 times back to back on one plan: every run bit-identical (the tasks'
     order of execution differs from run to run, the arithmetic must not) and equal to the reference."""
     rng = np.random.default_rng(input_dim + 7 * d)
