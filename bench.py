@@ -500,6 +500,21 @@ def secondary_rooflines(name, cfg, units, step_ms, clocks):
                               "traffic_model": model,
                               "l2_bytes_per_step": l2_bytes,
                               "peak_source": "tools/microbench/mb.cu L2 rmw, 32 MB, this pool's B200"}
+    if name == "c4":
+        # shared-memory roof of the dataflow sketch kernel (sketch_flow.cuh): every 64 KB task moves its
+        # tile through shared memory 6 times (TMA in, tile -> registers, one transpose = write + read,
+        # registers -> tile, TMA store out) plus one more transpose for the two passes that apply two H's;
+        # the last pass stores only the sampled rows (5 moves).  27 tile moves per element over the four
+        # passes, against 128 B / clk / SM (tools/microbench/mb.cu measures 124).
+        mhz = clocks.get("sm_mhz") or 1965.0
+        smem_bytes = 27 * cfg["N"] * units * 4
+        peak = 124.0 * 148 * mhz * 1e6 / 1e9
+        ach = smem_bytes / (step_ms * 1e-3) / 1e9
+        out["roofline_smem"] = {"bound": "shared memory", "achieved": ach, "peak": peak, "unit": "GB/s",
+                                "frac": ach / peak, "smem_bytes_per_step": smem_bytes, "sm_mhz": mhz,
+                                "model": "27 tile moves through shared memory per element over the 4 passes "
+                                         "(6 + 8 + 8 + 5) at the measured 124 B/clk/SM; ncu l1tex throughput of "
+                                         "the same kernel: profiles/r02_c4_ncu_full.json"}
     if name in ISSUE_FLOOR:
         f = ISSUE_FLOOR[name]
         mhz = clocks.get("sm_mhz") or f["mhz"]
