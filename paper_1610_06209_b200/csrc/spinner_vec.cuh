@@ -61,6 +61,12 @@ struct VecParams {
 #define SPN_EMBED_WARPS 24  // n = 1024 embed register budget (resident warps / SM); 20/22/26 measured slower
 #endif
 
+#ifndef SPN_TW64
+#define SPN_TW64 12  // resident warps / SM the R = 64 kernels are compiled for
+#endif
+#ifndef SPN_LOOP_MIN_R
+#define SPN_LOOP_MIN_R 64
+#endif
 template <int LOG_R_, int LOG_T_>
 struct VCfg {
   static constexpr int LOG_R = LOG_R_, LOG_T = LOG_T_, LOG_N = LOG_R + LOG_T;
@@ -75,15 +81,16 @@ struct VCfg {
   // register budget: resident warps/SM we ask ptxas to allow (R data registers + ~50)
   // R = 32: 28 warps (one wave for config 1's 4096 vectors: 18.6 vs 21.1 us) for hash /
   // apply; the embed kernels keep 24 (80 registers; at 72 they spill: 0.475 vs 0.443 ms)
-  static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 28 : (R == 64 ? 12 : 12));
+  static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 28 : (R == 64 ? SPN_TW64 : 12));
   __host__ __device__ static constexpr int min_ctas(int op) {
     return (R == 32 && op >= 2 && op <= 4) ? (SPN_EMBED_WARPS / (THREADS / 32) > 0 ? SPN_EMBED_WARPS / (THREADS / 32) : 1)
                                 : MIN_CTAS_BASE;
   }
   // looped chain (one copy of the D -> H body, R == T only): keeps the n = 16384 kernel
   // (R = 128, fully unrolled ~57 KB of SASS) inside the 32 KB L1.5 instruction cache.
-  // For n = 1024 the unrolled chain fits and measured faster (0.475 vs 0.498 ms).
-  static constexpr bool LOOPED = LOG_R == LOG_T && R >= 128;
+  // For n = 1024 the unrolled chain fits and measured faster (0.475 vs 0.498 ms); for n = 4096
+  // (R = 64) the loop wins: 8-table hash 62.9 -> 77.2 adds/clk/SM, apply 0.62 -> 0.69 of HBM.
+  static constexpr bool LOOPED = LOG_R == LOG_T && R >= SPN_LOOP_MIN_R;
   static constexpr int MIN_CTAS_BASE = TARGET_WARPS / (THREADS / 32) > 0 ? TARGET_WARPS / (THREADS / 32) : 1;
   // per group: transpose buffer (+ an x staging buffer for the embed ops, which reuse
   // x across blocks and prefetch the next row with cp.async)
