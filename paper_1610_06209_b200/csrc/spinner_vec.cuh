@@ -61,8 +61,17 @@ struct VecParams {
 #define SPN_EMBED_WARPS 24  // n = 1024 embed register budget (resident warps / SM); 20/22/26 measured slower
 #endif
 
+#ifndef SPN_APPLY_PREFETCH
+#define SPN_APPLY_PREFETCH 1
+#endif
+#ifndef SPN_TW13
+#define SPN_TW13 12  // resident warps / SM the n = 2^13 (R = 128, T = 64) kernels are compiled for
+#endif
 #ifndef SPN_TW64
 #define SPN_TW64 12  // resident warps / SM the R = 64 kernels are compiled for
+#endif
+#ifndef SPN_LOOP_ODD_MIN_R
+#define SPN_LOOP_ODD_MIN_R 128
 #endif
 #ifndef SPN_LOOP_MIN_R
 #define SPN_LOOP_MIN_R 64
@@ -81,7 +90,7 @@ struct VCfg {
   // register budget: resident warps/SM we ask ptxas to allow (R data registers + ~50)
   // R = 32: 28 warps (one wave for config 1's 4096 vectors: 18.6 vs 21.1 us) for hash /
   // apply; the embed kernels keep 24 (80 registers; at 72 they spill: 0.475 vs 0.443 ms)
-  static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 28 : (R == 64 ? SPN_TW64 : 12));
+  static constexpr int TARGET_WARPS = R <= 16 ? 32 : (R == 32 ? 28 : (R == 64 ? SPN_TW64 : (LOG_T == 6 ? SPN_TW13 : 12)));
   __host__ __device__ static constexpr int min_ctas(int op) {
     return (R == 32 && op >= 2 && op <= 4) ? (SPN_EMBED_WARPS / (THREADS / 32) > 0 ? SPN_EMBED_WARPS / (THREADS / 32) : 1)
                                 : MIN_CTAS_BASE;
@@ -91,6 +100,17 @@ struct VCfg {
   // For n = 1024 the unrolled chain fits and measured faster (0.475 vs 0.498 ms); for n = 4096
   // (R = 64) the loop wins: 8-table hash 62.9 -> 77.2 adds/clk/SM, apply 0.62 -> 0.69 of HBM.
   static constexpr bool LOOPED = LOG_R == LOG_T && R >= SPN_LOOP_MIN_R;
+  // R == 2T (n = 2^11, 2^13) as a one-body loop too.  The two layouts' register bits overlap in one
+  // element bit (LOG_T), so if layout B numbers its registers pb(j) = (j >> 1) | ((j & 1) << (LOG_R-1))
+  // (the shared bit on top) both directions run the same code: butterflies over all LOG_R register
+  // bits, a transpose (direction chosen at run time: only the transposes have two copies), butterflies
+  // over register bits [0, LOG_T).  Loads, stores and the layout-B transposes index registers through
+  // pb(); the host packs the all-sign plans' layout-B masks in the same order (build_vec_layouts).
+  static constexpr bool LOOPED_ODD = LOG_R == LOG_T + 1 && R >= SPN_LOOP_ODD_MIN_R;
+  template <bool PI>
+  __host__ __device__ static constexpr int pb(int j) {
+    return PI ? ((j >> 1) | ((j & 1) << (LOG_R - 1))) : j;
+  }
   static constexpr int MIN_CTAS_BASE = TARGET_WARPS / (THREADS / 32) > 0 ? TARGET_WARPS / (THREADS / 32) : 1;
   // per group: transpose buffer (+ an x staging buffer for the embed ops, which reuse
   // x across blocks and prefetch the next row with cp.async)
@@ -281,6 +301,32 @@ __device__ __forceinline__ void stsm_x4(uint32_t a, float r0, float r1, float r2
                : "memory");
 }
 
+// The same moves for the looped R == 2T chain, whose layout-B registers are numbered pb(j): matrix q of
+// quad k carries the standard register pinv(4k + q) = 2 (4k + q) for the first half of the quads and
+// 2 (4k + q - R/2) + 1 for the second, so every ldmatrix / stmatrix still fills an aligned register quad
+// in physical order (with pb() applied to the destination registers instead, ptxas shuffled every quad
+// into place with MOVs).  S = 1, so the swizzle chunk (j >> 1) & 7 is the same for 2m and 2m + 1 and the
+// odd half sits one register row (4T bytes) further.
+template <class C>
+struct MatBP {
+  static constexpr int H = C::R / 8;  // quads per half
+  uint32_t off[2];
+  __device__ __forceinline__ MatBP(const float* sm, int t) {
+    const int l = t & 31, w = t >> 5, q = l >> 3, rho = l & 7;
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const int j = 2 * (4 * kk + q);
+      const int c = (j >> 1) & C::XMASK;
+      off[kk] = base + 4u * static_cast<uint32_t>(j * C::T + 32 * w + 4 * (rho ^ c));
+    }
+  }
+  __device__ __forceinline__ uint32_t addr(int k) const {  // k: physical quad (compile-time after unrolling)
+    const int kh = k % H, odd = k / H;
+    return off[kh % 2] + 4u * static_cast<uint32_t>(C::T * (8 * (kh - kh % 2) + odd));
+  }
+};
+
 #ifndef SPN_F1_REV
 #define SPN_F1_REV 1
 #endif
@@ -289,7 +335,7 @@ __device__ __forceinline__ void stsm_x4(uint32_t a, float r0, float r1, float r2
 #define SPN_XPOSE_MATRIX 1
 #endif
 
-template <class C>
+template <class C, bool PI = false>
 __device__ __forceinline__ void xpose_A_to_B(float (&r)[C::R], float* sm, int t) {
   const Swz<C> z(t);
   if constexpr (C::R >= 4) {
@@ -302,27 +348,35 @@ __device__ __forceinline__ void xpose_A_to_B(float (&r)[C::R], float* sm, int t)
     for (int j = 0; j < C::R; ++j) sm[sw<C>(t * C::R + j)] = r[j];
   }
   group_sync<C>();
-  if constexpr (MatB<C>::ON && SPN_XPOSE_MATRIX) {
+  if constexpr (MatB<C>::ON && SPN_XPOSE_MATRIX && PI) {
+    const MatBP<C> mb(sm, t);
+#pragma unroll
+    for (int k = 0; k < C::R / 4; ++k) ldsm_x4(mb.addr(k), r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+  } else if constexpr (MatB<C>::ON && SPN_XPOSE_MATRIX) {
     const MatB<C> mb(sm, t);
 #pragma unroll
     for (int k = 0; k < C::R / 4; ++k) ldsm_x4(mb.addr(k), r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
   } else {
 #pragma unroll
-    for (int j = 0; j < C::R; ++j) r[j] = sm[z.B(t, j)];
+    for (int j = 0; j < C::R; ++j) r[C::template pb<PI>(j)] = sm[z.B(t, j)];
   }
   group_sync<C>();
 }
 
-template <class C>
+template <class C, bool PI = false>
 __device__ __forceinline__ void xpose_B_to_A(float (&r)[C::R], float* sm, int t) {
   const Swz<C> z(t);
-  if constexpr (MatB<C>::ON && SPN_XPOSE_MATRIX) {
+  if constexpr (MatB<C>::ON && SPN_XPOSE_MATRIX && PI) {
+    const MatBP<C> mb(sm, t);
+#pragma unroll
+    for (int k = 0; k < C::R / 4; ++k) stsm_x4(mb.addr(k), r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+  } else if constexpr (MatB<C>::ON && SPN_XPOSE_MATRIX) {
     const MatB<C> mb(sm, t);
 #pragma unroll
     for (int k = 0; k < C::R / 4; ++k) stsm_x4(mb.addr(k), r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
   } else {
 #pragma unroll
-    for (int j = 0; j < C::R; ++j) sm[z.B(t, j)] = r[j];
+    for (int j = 0; j < C::R; ++j) sm[z.B(t, j)] = r[C::template pb<PI>(j)];
   }
   group_sync<C>();
   if constexpr (C::R >= 4) {
@@ -457,6 +511,23 @@ __device__ __forceinline__ void spinner_chain(float (&r)[C::R], float* sm, const
 #endif
       reg_fwht<C::R, 0, C::LOG_R>(r);
     }
+  } else if constexpr (SIGNS && C::LOOPED_ODD) {
+    // R == 2T: the same loop with layout B's registers numbered pb(j) (see VCfg::LOOPED_ODD)
+    const uint32_t* w1p = p.d[1][L1].sgn;
+    const uint32_t* w2p = p.d[2][L0].sgn;
+    uint32_t w[C::WORDS];
+    load_words<C>(w, p.d[0][L0].sgn, tb, t);
+#pragma unroll 1
+    for (int h = 0; h < 3; ++h) {
+      xor_signs<C>(r, w);
+      if (h < 2) load_words<C>(w, h == 0 ? w1p : w2p, tb, t);
+      reg_fwht<C::R, 0, C::LOG_R, SPN_F1_REV>(r);
+      if ((L0 == LAY_A) != ((h & 1) != 0))
+        xpose_A_to_B<C, true>(r, sm, t);
+      else
+        xpose_B_to_A<C, true>(r, sm, t);
+      reg_fwht<C::R, 0, C::LOG_T>(r);
+    }
   } else if constexpr (SIGNS) {
     uint32_t w0[C::WORDS], w1[C::WORDS], w2[C::WORDS];
     load_words<C>(w0, p.d[0][L0].sgn, tb, t);
@@ -479,17 +550,17 @@ __device__ __forceinline__ void spinner_chain(float (&r)[C::R], float* sm, const
 }
 
 // Load row v in layout B (coalesced), zero padded beyond n_in (dataset.cpp:162-168).
-template <class C>
+template <class C, bool PI = false>
 __device__ __forceinline__ void load_x_B(float (&r)[C::R], const float* __restrict__ xrow,
                                          int64_t n_in, int t) {
   if (n_in >= C::N) {  // uniform fast path: no padding
 #pragma unroll
-    for (int j = 0; j < C::R; ++j) r[j] = __ldg(xrow + j * C::T + t);
+    for (int j = 0; j < C::R; ++j) r[C::template pb<PI>(j)] = __ldg(xrow + j * C::T + t);
   } else {
 #pragma unroll
     for (int j = 0; j < C::R; ++j) {
       const int i = j * C::T + t;
-      r[j] = (i < n_in) ? __ldg(xrow + i) : 0.0f;
+      r[C::template pb<PI>(j)] = (i < n_in) ? __ldg(xrow + i) : 0.0f;
     }
   }
 }
@@ -830,6 +901,7 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
   const int64_t total = p.batch * per_vec;
   const int64_t stride = (int64_t)gridDim.x * C::GPC;
   constexpr bool APPLY = OP == OP_APPLY || OP == OP_APPLY_P;
+  constexpr bool PI = SIGNS && C::LOOPED_ODD;  // layout B registers numbered pb(j) (looped R == 2T chain)
   constexpr bool PERM = OP == OP_APPLY_P;  // permuted coordinates: 16-B x loads and y stores
   static_assert(!PERM || (LOG_R == LOG_T && LOG_R >= 2), "permuted apply needs R == T");
   const bool want_ids = (OP == OP_HASH) || (APPLY && p.ids != nullptr);
@@ -882,6 +954,20 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
     const int64_t v = active ? (vmaj ? vg : item / per_vec) : 0;
     const int64_t tab = active ? (vmaj ? sub : item - v * per_vec) : 0;
     const float* xrow = p.x + v * p.ld_x;
+#if SPN_APPLY_PREFETCH
+    // apply at n >= 2^12: one thread asks L2 for the CTA's next row while this one transforms (a CTA
+    // idles through its row's load and there is no spare CTA to cover it: 3 per SM at n = 2^14):
+    // apply at n = 2^12 / 2^13 / 2^14 0.69 / 0.50 / 0.50 -> 0.70 / 0.57 / 0.52 of the HBM copy peak.  (The
+    // same one-instruction prefetch of the next vector in the 8-table hash: 276 vs 250 ms at config 3 —
+    // that kernel has no register to spare.)
+    if constexpr (OP == OP_APPLY && C::R >= 64 && C::GPC == 1) {
+      const int64_t nv = v + gridDim.x;
+      if (threadIdx.x == 0 && p.x_vec_ok && nv < p.batch && active) {
+        const uint32_t bytes = static_cast<uint32_t>(min(p.n_in, (int64_t)C::N) * 4) & ~15u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.x + nv * p.ld_x), "r"(bytes) : "memory");
+      }
+    }
+#endif
 
     float r[C::R];
     if constexpr (STAGE_X) {
@@ -959,7 +1045,7 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
         }
       } else {
 #ifdef SPN_DBG_NOLOAD  // (bound experiments only: wrong results)
-        if (base == (int64_t)blockIdx.x * C::GPC) load_x_B<C>(r, xrow, p.n_in, t);
+        if (base == (int64_t)blockIdx.x * C::GPC) load_x_B<C, PI>(r, xrow, p.n_in, t);
         else {
 #pragma unroll
           for (int j = 0; j < C::R; ++j) r[j] = __int_as_float(0x3f800000 + j * 977 + t * 131 + (int)base);
@@ -968,10 +1054,10 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
         if constexpr (PERM)
           load_x_perm<C>(r, xrow, t);
         else
-          load_x_B<C>(r, xrow, p.n_in, t);
+          load_x_B<C, PI>(r, xrow, p.n_in, t);
 #endif
         if constexpr (END_B) {
-          if constexpr (C::T > 1) xpose_B_to_A<C>(r, sm, t);
+          if constexpr (C::T > 1) xpose_B_to_A<C, PI>(r, sm, t);
         }
         if constexpr (OP == OP_EMBED_GAUSS) {
 #pragma unroll
@@ -982,6 +1068,13 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
       const int64_t row0 = (int64_t)b * p.m;
       const int64_t rows = min(p.m, p.k - row0);  // valid rows of this block (stacking, spinner.cpp:272-283)
       spinner_chain<C, END_B, SIGNS>(r, sm, p, tb, t);
+      if constexpr (PI && END_B) {  // back to the standard layout-B register order for the epilogue
+        float rs[C::R];
+#pragma unroll
+        for (int j = 0; j < C::R; ++j) rs[j] = r[C::template pb<true>(j)];
+#pragma unroll
+        for (int j = 0; j < C::R; ++j) r[j] = rs[j];
+      }
       if constexpr (!END_B) {
         // layout A: element i = t*R + j, increasing j
         if (fast_ids) {

@@ -179,7 +179,7 @@ inline int64_t perm1024_inv(int64_t ep) { return ((ep >> 5) & 3) | ((ep & 31) <<
 
 // Bit-packed sign masks of one diagonal in one layout (optionally in permuted coordinates).
 std::vector<uint32_t> pack_signs(const double* D, int64_t TB, int64_t N, int LOG_R, int LOG_T, int lay,
-                                 bool perm) {
+                                 bool perm, bool pib = false) {
   const int64_t R = int64_t(1) << LOG_R, T = int64_t(1) << LOG_T;
   const int64_t WORDS = R >= 32 ? R / 32 : 1, BITS = R >= 32 ? 32 : R;
   std::vector<uint32_t> w(static_cast<size_t>(TB * WORDS * T), 0u);
@@ -188,7 +188,10 @@ std::vector<uint32_t> pack_signs(const double* D, int64_t TB, int64_t N, int LOG
       for (int64_t t = 0; t < T; ++t) {
         uint32_t word = 0;
         for (int64_t jj = 0; jj < BITS; ++jj) {
-          int64_t e = elem(lay, LOG_R, LOG_T, t, q * 32 + jj);
+          int64_t j = q * 32 + jj;
+          // looped R == 2T chain (VCfg::LOOPED_ODD): layout-B register pb(j) holds standard register j
+          if (pib) j = ((j & (R / 2 - 1)) << 1) | (j >> (LOG_R - 1));
+          int64_t e = elem(lay, LOG_R, LOG_T, t, j);
           if (perm) e = perm1024_inv(e);
           if (D[tb * N + e] < 0.0) word |= 1u << jj;
         }
@@ -207,7 +210,9 @@ spn_status build_vec_layouts(spn_plan* p) {
     const double* D = p->d[di].data();
     for (int lay = 0; lay < 2; ++lay) {
       if (p->dsign[di]) {
-        std::vector<uint32_t> w = pack_signs(D, TB, N, LOG_R, LOG_T, lay, false);
+        // all-sign plans run the SIGNS kernels, whose R == 2T chains number layout B's registers pb(j)
+        const bool pib = all_sign && lay == spn::LAY_B && LOG_R == LOG_T + 1 && R >= SPN_LOOP_ODD_MIN_R;
+        std::vector<uint32_t> w = pack_signs(D, TB, N, LOG_R, LOG_T, lay, false, pib);
         spn_status s = upload(w.data(), w.size() * 4, reinterpret_cast<void**>(&p->vsgn[di][lay]));
         if (s) return s;
         if (N == 1024 && all_sign) {  // permuted-coordinate embed kernel
@@ -740,6 +745,8 @@ spn_status spn_apply_f32(const spn_plan* p, const float* x, int64_t batch, int64
   v.y = y;
   v.ld_y = ld_y;
   v.relu = relu;
+  // 16-B aligned rows: the apply kernel may bulk-prefetch its next row into L2
+  v.x_vec_ok = reinterpret_cast<uintptr_t>(x) % 16 == 0 && ld_x % 4 == 0;
   return run_vec(p, spn::OP_APPLY, v, static_cast<cudaStream_t>(stream));
   SPN_CATCH
 }
@@ -774,6 +781,7 @@ spn_status spn_hash_f32(const spn_plan* p, const float* x, int64_t batch, int64_
     return !(e && e[0] == '0');
   }();
   auto al16 = [](const void* q, int64_t ld) { return reinterpret_cast<uintptr_t>(q) % 16 == 0 && ld % 4 == 0; };
+  v.x_vec_ok = al16(x, ld_x);  // 16-B aligned rows: the apply kernel may bulk-prefetch its next row
   if (perm_on && y && ids && p->n == 1024 && p->vsgnP[0][0] && p->blocks == 1 && p->tables == 1 && p->m == 1024 &&
       p->k == 1024 && n_in == 1024 && al16(x, ld_x) && al16(y, ld_y)) {
     v.perm = 1;
