@@ -99,6 +99,34 @@ def test_c1_full_batch_ids_and_projection(spn, ref, torch):
     assert np.array_equal(yh, y.cpu().numpy())
 
 
+@pytest.mark.parametrize("n", [2048, 4096, 8192])
+def test_mid_sizes_many_items_per_cta(spn, ref, torch, n):
+    """n = 2^11 .. 2^13 (the looped R = T and R = 2T chains, the apply's next-row prefetch) at a batch where
+    every persistent CTA runs many items: apply + ids on the whole batch and a 3-table hash, sampled rows
+    against the reference."""
+    batch, seed = 20000, 77 + n
+    x = unit_rows(torch, batch, n, n)
+    sp = spn.StackedSpinner(spn.SpinnerVariant.hd3_hd2_hd1, n, n, n, seed, scale=1.0)
+    y = torch.empty((batch, n), device="cuda")
+    ids = sp.plan.hash(x, y_out=y)
+    assert torch.equal(sp.apply(x), y)  # the apply-only launch (no ids) gives the same rows
+    seeds = [spn.mix_seed(seed, t) for t in range(3)]
+    mt = spn.MultiTableHasher(spn.SpinnerVariant.hd3_hd2_hd1, n, n, 3, table_seeds=seeds)
+    ids3 = mt.hash_ids(x)
+    torch.cuda.synchronize()
+    rows = np.random.default_rng(n).choice(batch, 256, replace=False)
+    rows[:2] = (0, batch - 1)
+    xh = x[torch.from_numpy(rows).cuda()].cpu().numpy()
+    y_ref = ref.apply(HD3, n, n, n, seed, 1.0, xh, threads=THREADS)
+    assert row_rel(y.cpu().numpy()[rows], y_ref).max() <= RTOL
+    want, gaps = ids_and_gaps(y_ref, n)
+    check_ids(ids.cpu().numpy()[rows, 0], want, gaps, f"n={n} apply+ids")
+    for t in range(3):
+        yt = ref.apply(HD3, n, n, n, seeds[t], 1.0, xh, threads=THREADS)
+        want, gaps = ids_and_gaps(yt, n)
+        check_ids(ids3.cpu().numpy()[rows, t], want, gaps, f"n={n} table {t}")
+
+
 def test_c2_full_batch_sampled_rows(spn, ref, torch):
     n, n_in, batch, k, sigma, seed = 1024, 784, 60000, 4096, 5.0, 5
     g = torch.Generator(device="cuda")
