@@ -31,7 +31,8 @@ namespace spn {
 struct FlowParams {
   int nstripes, G;
   int wlast;  // workspace loads / stores carry an L2 evict-last hint (SPN_FLOW_WLAST)
-  int nodep;  // bound experiments only (SPN_DBG_FLOW_NODEP): skip the dependency waits (wrong results)
+  int nodep;  // bound experiments only (SPN_DBG_FLOW_NODEP, wrong results): 1 skips the dependency waits, 2 also
+              // every load of the two-group kernel (0.1475 / 0.1475 / 0.126 ms at config 4 for 0 / 1 / 2)
   uint32_t ntasks;
   const float* d1;   // [N]
   const float* d2t;  // [N], D2 transposed for the high pass: d2t[lo * 2^lsb + s] = D2[(s << lsa) + lo]
@@ -489,6 +490,10 @@ __global__ void __launch_bounds__(Flow2Cfg<LSA, LSB>::THREADS, 1)
       const int box = LS > 8 ? 256 : (1 << LS), nbox = (1 << LS) / box;
       const float* dsrc = tk.pass == 0 ? p.d1 : (tk.pass == 1 ? p.d2t : (tk.pass == 2 ? p.d3 : nullptr));
       const uint32_t bytes = (uint32_t)F::TILEB + (dsrc ? (uint32_t)nsub * (4u << LS) : 0u);
+      if (p.nodep == 2) {  // bound experiment (wrong results): no loads at all, the slot is "full" at once
+        mbar_arrive(&full[slot]);
+        continue;
+      }
       mbar_arrive_tx(&full[slot], bytes);
       for (int sb = 0; sb < nsub; ++sb) {
         const int ti = tk.idx * nsub + sb;
