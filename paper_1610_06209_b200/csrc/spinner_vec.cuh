@@ -70,6 +70,9 @@ struct VecParams {
 #ifndef SPN_TW64
 #define SPN_TW64 12  // resident warps / SM the R = 64 kernels are compiled for
 #endif
+#ifndef SPN_LOOP_ODD_HASH_MIN_R
+#define SPN_LOOP_ODD_HASH_MIN_R 64
+#endif
 #ifndef SPN_LOOP_ODD_MIN_R
 #define SPN_LOOP_ODD_MIN_R 128
 #endif
@@ -107,6 +110,12 @@ struct VCfg {
   // over register bits [0, LOG_T).  Loads, stores and the layout-B transposes index registers through
   // pb(); the host packs the all-sign plans' layout-B masks in the same order (build_vec_layouts).
   static constexpr bool LOOPED_ODD = LOG_R == LOG_T + 1 && R >= SPN_LOOP_ODD_MIN_R;
+  // n = 2^11 (R = 64, T = 32): the loop is faster for the hash (66.0 -> 71.9 adds/clk/SM) and slower for
+  // the apply (0.76 -> 0.72 of HBM), so only the hash kernels take it (the plan keeps its layout-B masks in
+  // both orders: spn_plan::vsgnL).
+  __host__ __device__ static constexpr bool looped_odd(int op) {
+    return LOOPED_ODD || (LOG_R == LOG_T + 1 && R >= SPN_LOOP_ODD_HASH_MIN_R && op == 0 /* OP_HASH */);
+  }
   template <bool PI>
   __host__ __device__ static constexpr int pb(int j) {
     return PI ? ((j >> 1) | ((j & 1) << (LOG_R - 1))) : j;
@@ -489,7 +498,7 @@ __device__ __forceinline__ void load_words(uint32_t (&w)[C::WORDS], const uint32
 //    all register bits, so the six half-transforms run as a loop over ONE copy of
 //    the butterfly code with a runtime transpose direction — a third of the SASS of
 //    the unrolled chain, which keeps the n = 16384 kernel inside the instruction cache.
-template <class C, bool END_B, bool SIGNS>
+template <class C, bool END_B, bool SIGNS, bool LODD = C::LOOPED_ODD>
 __device__ __forceinline__ void spinner_chain(float (&r)[C::R], float* sm, const VecParams& p, int64_t tb,
                                               int t) {
   constexpr int L0 = END_B ? LAY_A : LAY_B, L1 = END_B ? LAY_B : LAY_A;
@@ -511,7 +520,7 @@ __device__ __forceinline__ void spinner_chain(float (&r)[C::R], float* sm, const
 #endif
       reg_fwht<C::R, 0, C::LOG_R>(r);
     }
-  } else if constexpr (SIGNS && C::LOOPED_ODD) {
+  } else if constexpr (SIGNS && LODD) {
     // R == 2T: the same loop with layout B's registers numbered pb(j) (see VCfg::LOOPED_ODD)
     const uint32_t* w1p = p.d[1][L1].sgn;
     const uint32_t* w2p = p.d[2][L0].sgn;
@@ -901,7 +910,7 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
   const int64_t total = p.batch * per_vec;
   const int64_t stride = (int64_t)gridDim.x * C::GPC;
   constexpr bool APPLY = OP == OP_APPLY || OP == OP_APPLY_P;
-  constexpr bool PI = SIGNS && C::LOOPED_ODD;  // layout B registers numbered pb(j) (looped R == 2T chain)
+  constexpr bool PI = SIGNS && C::looped_odd(OP);  // layout B registers numbered pb(j) (looped R == 2T chain)
   constexpr bool PERM = OP == OP_APPLY_P;  // permuted coordinates: 16-B x loads and y stores
   static_assert(!PERM || (LOG_R == LOG_T && LOG_R >= 2), "permuted apply needs R == T");
   const bool want_ids = (OP == OP_HASH) || (APPLY && p.ids != nullptr);
@@ -1067,7 +1076,7 @@ __global__ void __launch_bounds__(VCfg<LOG_R, LOG_T>::THREADS, VCfg<LOG_R, LOG_T
       const int64_t tb = tab * p.blocks + b;
       const int64_t row0 = (int64_t)b * p.m;
       const int64_t rows = min(p.m, p.k - row0);  // valid rows of this block (stacking, spinner.cpp:272-283)
-      spinner_chain<C, END_B, SIGNS>(r, sm, p, tb, t);
+      spinner_chain<C, END_B, SIGNS, C::looped_odd(OP)>(r, sm, p, tb, t);
       if constexpr (PI && END_B) {  // back to the standard layout-B register order for the epilogue
         float rs[C::R];
 #pragma unroll

@@ -103,6 +103,7 @@ struct spn_plan {
   // vector-kernel layouts (n <= 2^14): [diag][layout]
   uint32_t* vsgn[3][2] = {};
   float* vflt[3][2] = {};
+  uint32_t* vsgnL[3] = {};     // n = 2^11 all-sign plans: layout-B masks in pb() order (looped hash kernel)
   uint32_t* vsgnP[3][2] = {};  // n = 1024 sign masks in permuted coordinates (OP_EMBED_GAUSS_P)
   // multi-pass layouts (n > 2^14)
   spn::BigPlan big;
@@ -141,6 +142,8 @@ spn_plan::~spn_plan() {
     for (auto& a : vsgnP)
       for (auto* p : a)
         if (p) cudaFree(p);
+    for (auto* p : vsgnL)
+      if (p) cudaFree(p);
     big.release();
     for (auto& a : hbuf)
       for (auto* p : a)
@@ -215,6 +218,12 @@ spn_status build_vec_layouts(spn_plan* p) {
         std::vector<uint32_t> w = pack_signs(D, TB, N, LOG_R, LOG_T, lay, false, pib);
         spn_status s = upload(w.data(), w.size() * 4, reinterpret_cast<void**>(&p->vsgn[di][lay]));
         if (s) return s;
+        // n = 2^11: only the hash kernels run the looped chain (VCfg::looped_odd): a second copy in pb() order
+        if (all_sign && lay == spn::LAY_B && LOG_R == LOG_T + 1 && !pib && R >= SPN_LOOP_ODD_HASH_MIN_R) {
+          w = pack_signs(D, TB, N, LOG_R, LOG_T, lay, false, true);
+          s = upload(w.data(), w.size() * 4, reinterpret_cast<void**>(&p->vsgnL[di]));
+          if (s) return s;
+        }
         if (N == 1024 && all_sign) {  // permuted-coordinate embed kernel
           w = pack_signs(D, TB, N, LOG_R, LOG_T, lay, true);
           s = upload(w.data(), w.size() * 4, reinterpret_cast<void**>(&p->vsgnP[di][lay]));
@@ -309,6 +318,8 @@ spn_status run_vec(const spn_plan* p, int op, spn::VecParams& v, cudaStream_t s)
   if (items == 0) return SPN_OK;
   DeviceGuard g(p->device);
   const int signs = p->dsign[0] && p->dsign[1] && p->dsign[2];
+  if (op == spn::OP_HASH && signs && p->vsgnL[0])  // n = 2^11: the looped hash kernel's layout-B mask order
+    for (int di = 0; di < 3; ++di) v.d[di][spn::LAY_B].sgn = p->vsgnL[di];
   const spn::LaunchFn fn = (op == spn::OP_APPLY && v.perm) ? spn::vec_launcher_apply_perm()
                                                            : vec_launcher(p->log_n, op, signs);
   cudaError_t e = fn(v, s, p->sms, items);
