@@ -70,6 +70,12 @@ struct VecParams {
 #ifndef SPN_TW64
 #define SPN_TW64 12  // resident warps / SM the R = 64 kernels are compiled for
 #endif
+#ifndef SPN_XBUF_MAX_LOGN
+#define SPN_XBUF_MAX_LOGN 12  // largest n whose embed kernels stage x in a second shared-memory buffer: at
+// n = 2^13 / 2^14 the second buffer halves / thirds the resident CTAs (2^14: one 128 KB CTA per SM) and the
+// single-block Gaussian features ran 0.44 / 0.41 of HBM; loading x per block like the apply: 0.64 / 0.67
+// (with the apply's next-row L2 prefetch on top: 0.65 / 0.63, so the embed kernels go without)
+#endif
 #ifndef SPN_LOOP_ODD_HASH_MIN_R
 #define SPN_LOOP_ODD_HASH_MIN_R 64
 #endif
@@ -123,7 +129,7 @@ struct VCfg {
   static constexpr int MIN_CTAS_BASE = TARGET_WARPS / (THREADS / 32) > 0 ? TARGET_WARPS / (THREADS / 32) : 1;
   // per group: transpose buffer (+ an x staging buffer for the embed ops, which reuse
   // x across blocks and prefetch the next row with cp.async)
-  __host__ __device__ static constexpr bool xbuf(int op) { return op == 2 || op == 3 || op == 4; }
+  __host__ __device__ static constexpr bool xbuf(int op) { return (op == 2 || op == 3 || op == 4) && LOG_N <= SPN_XBUF_MAX_LOGN; }
   __host__ __device__ static constexpr int smem_floats(int op) {
     return GPC * N * (xbuf(op) ? 2 : 1) + (T > 32 ? 4 * (T / 32) : 0);
   }
